@@ -1,0 +1,578 @@
+// api.cu — the C ABI declared in include/lco.h: argument checking, workspace layout,
+// launch sequencing, error reporting and the measurement hook.  Every device step of
+// the path runs in kernels.cu; nothing here computes on the data.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "launch.h"
+#include "lco_internal.h"
+
+namespace lco {
+const char* last_error();
+}
+
+using namespace lco;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+constexpr uint64_t kMaxOnesweepNnz = (1ull << 30) - 1;  // 30-bit look-back counters
+
+struct WsLayout {
+  size_t ctrl, statusA, statusB, kA, pA, kB, pB, flag, total;
+};
+
+WsLayout layout_for(int path, int passes, int rb, uint64_t nnz) {
+  WsLayout w;
+  memset(&w, 0, sizeof w);
+  size_t off = 0;
+  if (path == kPathOnesweep && nnz > 0) {
+    const uint64_t tiles = onesweep_tiles(nnz);
+    const size_t st = (size_t)tiles * ((size_t)1 << rb) * 4;
+    w.ctrl = off;
+    off += align_up(onesweep_ctrl_bytes(rb));
+    w.statusA = off;
+    off += align_up(st);
+    if (passes >= 2) {
+      w.statusB = off;
+      off += align_up(st);
+      w.kA = off;
+      off += align_up(nnz * 8);
+      w.pA = off;
+      off += align_up(nnz * 4);
+    }
+    if (passes >= 3) {
+      w.kB = off;
+      off += align_up(nnz * 8);
+      w.pB = off;
+      off += align_up(nnz * 4);
+    }
+  }
+  w.flag = off;
+  off += kAlign;
+  w.total = off;
+  return w;
+}
+
+int partition_rb(int world) { return world <= 256 ? 8 : (world <= 1024 ? 10 : 11); }
+
+bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
+  if (!a || !b || !na || !nb) return false;
+  const char* x = static_cast<const char*>(a);
+  const char* y = static_cast<const char*>(b);
+  return x < y + nb && y < x + na;
+}
+
+lco_status cuda_fail(cudaError_t e, const char* where) {
+  set_error("%s: %s", where, cudaGetErrorString(e));
+  return LCO_ERR_CUDA;
+}
+
+// ---- measurement hook: one CUDA event before each launch, one after the last ----
+struct ProfCtx {
+  lco_plan_s* h;
+  cudaStream_t s;
+  int call;
+  int stage;
+};
+
+void prof_mark(void* ctx, const char* name) {
+  ProfCtx* c = static_cast<ProfCtx*>(ctx);
+  lco_plan_s* h = c->h;
+  if (c->stage >= kProfStages) return;
+  cudaEvent_t ev = static_cast<cudaEvent_t>(h->prof_events[c->call * (kProfStages + 1) + c->stage]);
+  cudaEventRecord(ev, c->s);
+  if (c->call == 0) {
+    size_t len = strlen(h->prof_names);
+    snprintf(h->prof_names + len, sizeof(h->prof_names) - len, "%s%s", len ? ";" : "", name);
+  }
+  c->stage++;
+}
+
+bool prof_begin(lco_plan_s* h, cudaStream_t s, ProfCtx* c, Launch* L) {
+  if (!h->prof_events || h->prof_calls >= h->prof_calls_max) return false;
+  c->h = h;
+  c->s = s;
+  c->call = h->prof_calls;
+  c->stage = 0;
+  if (c->call == 0) h->prof_names[0] = 0;
+  L->mark = prof_mark;
+  L->ctx = c;
+  return true;
+}
+
+void prof_end(ProfCtx* c) {
+  lco_plan_s* h = c->h;
+  int st = c->stage < kProfStages ? c->stage : kProfStages;
+  cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[c->call * (kProfStages + 1) + st]), c->s);
+  h->prof_nstages[c->call < 64 ? c->call : 63] = st;
+  h->prof_calls++;
+}
+
+lco_status check_handle(lco_handle h) {
+  if (!h) {
+    set_error("NULL handle");
+    return LCO_ERR_NULL;
+  }
+  return LCO_OK;
+}
+
+lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const uint64_t* keys_in,
+                  const double* vals_in, const uint32_t* idx_in, uint64_t* keys_out,
+                  double* vals_out, uint32_t* perm_out, void* workspace, size_t ws_bytes,
+                  void* stream) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (nnz > h->max_nnz || nnz >= (1ull << 32)) {
+    set_error("nnz %llu exceeds max_nnz %llu (or 2^32-1)", (unsigned long long)nnz,
+              (unsigned long long)h->max_nnz);
+    return LCO_ERR_CAPACITY;
+  }
+  if (nnz == 0) return LCO_OK;
+  if (!keys_in || !keys_out) {
+    set_error("keys_in and keys_out are required");
+    return LCO_ERR_NULL;
+  }
+  if ((vals_in == nullptr) != (vals_out == nullptr)) {
+    set_error("vals_in and vals_out must both be given or both be NULL");
+    return LCO_ERR_ARG;
+  }
+  const size_t n8 = nnz * 8, n4 = nnz * 4;
+  const void* ins[3] = {keys_in, vals_in, idx_in};
+  const size_t insz[3] = {n8, n8, n4};
+  const void* outs[3] = {keys_out, vals_out, perm_out};
+  const size_t outsz[3] = {n8, n8, n4};
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 3; ++j)
+      if (overlaps(outs[i], outsz[i], ins[j], insz[j])) {
+        set_error("output %d overlaps input %d", i, j);
+        return LCO_ERR_ALIAS;
+      }
+    for (int j = i + 1; j < 3; ++j)
+      if (overlaps(outs[i], outsz[i], outs[j], outsz[j])) {
+        set_error("outputs %d and %d overlap", i, j);
+        return LCO_ERR_ALIAS;
+      }
+  }
+  if (op.path == kPathOnesweep && nnz > kMaxOnesweepNnz) {
+    set_error("nnz %llu above the 2^30-1 limit of the 30-bit look-back counters",
+              (unsigned long long)nnz);
+    return LCO_ERR_CAPACITY;
+  }
+  const WsLayout w = layout_for(op.path, op.passes, op.radix_bits, nnz);
+  if (!workspace || ws_bytes < w.total || (reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
+    set_error("workspace needs %zu bytes, 256-byte aligned (got %zu at %p)", w.total, ws_bytes,
+              workspace);
+    return LCO_ERR_WORKSPACE;
+  }
+  for (int i = 0; i < 3; ++i)
+    if (overlaps(outs[i], outsz[i], workspace, w.total) ||
+        overlaps(ins[i], insz[i], workspace, w.total)) {
+      set_error("workspace overlaps an input or output");
+      return LCO_ERR_ALIAS;
+    }
+  char* ws = static_cast<char*>(workspace);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (h->flags & LCO_FLAG_VALIDATE) {
+    uint32_t* flag = reinterpret_cast<uint32_t*>(ws + w.flag);
+    cudaError_t e = run_validate(nnz, keys_in, h->total, sort ? 0 : 1, flag, s);
+    if (e != cudaSuccess) return cuda_fail(e, "validate");
+    uint32_t hf = 0;
+    e = cudaMemcpyAsync(&hf, flag, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "validate");
+    if (hf & 2u) {
+      set_error("a key is >= prod(dims)");
+      return LCO_ERR_KEY_RANGE;
+    }
+    if (hf & 1u) {
+      set_error("keys_in is not strictly increasing");
+      return LCO_ERR_UNSORTED;
+    }
+  }
+  Launch L{s, nullptr, nullptr};
+  ProfCtx pc;
+  const bool prof = prof_begin(h, s, &pc, &L);
+  cudaError_t e;
+  if (op.path == kPathCopy) {
+    e = run_copy(nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, L);
+  } else {
+    OnesweepIO io;
+    memset(&io, 0, sizeof io);
+    io.nnz = nnz;
+    io.keys_in = keys_in;
+    io.vals_in = vals_in;
+    io.idx_in = idx_in;
+    io.keys_out = keys_out;
+    io.vals_out = vals_out;
+    io.perm_out = perm_out;
+    io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
+    io.statusA = reinterpret_cast<uint32_t*>(ws + w.statusA);
+    io.statusB = op.passes >= 2 ? reinterpret_cast<uint32_t*>(ws + w.statusB) : nullptr;
+    io.kA = op.passes >= 2 ? reinterpret_cast<uint64_t*>(ws + w.kA) : nullptr;
+    io.pA = op.passes >= 2 ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
+    io.kB = op.passes >= 3 ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
+    io.pB = op.passes >= 3 ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
+    e = run_onesweep(op.radix_bits, op.kp, io, L);
+  }
+  if (prof) prof_end(&pc);
+  if (e != cudaSuccess) return cuda_fail(e, sort ? "lco_sort" : "lco_permute");
+  return LCO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+lco_status lco_create(lco_handle* out, int order, const uint64_t* dims, const int32_t* perm,
+                      uint64_t max_nnz, uint32_t flags) {
+  if (!out || !dims) {
+    set_error("out and dims are required");
+    return LCO_ERR_NULL;
+  }
+  *out = nullptr;
+  if (order < 1 || order > LCO_MAX_ORDER) {
+    set_error("order %d outside 1..%d", order, LCO_MAX_ORDER);
+    return LCO_ERR_ORDER;
+  }
+  if (max_nnz >= (1ull << 32)) {
+    set_error("max_nnz must be < 2^32 (uint32 permutation vector)");
+    return LCO_ERR_CAPACITY;
+  }
+  if (flags & ~LCO_FLAG_VALIDATE) {
+    set_error("unknown flags 0x%x", flags);
+    return LCO_ERR_ARG;
+  }
+  lco_plan_s* h = new (std::nothrow) lco_plan_s;
+  if (!h) {
+    set_error("out of host memory");
+    return LCO_ERR_ARG;
+  }
+  memset(h, 0, sizeof *h);
+  lco_status st = build_plan(h, order, dims, perm);
+  if (st != LCO_OK) {
+    delete h;
+    return st;
+  }
+  h->max_nnz = max_nnz;
+  h->flags = flags;
+  *out = h;
+  return LCO_OK;
+}
+
+lco_status lco_destroy(lco_handle h) {
+  if (!h) return LCO_OK;
+  if (h->prof_events) {
+    for (int i = 0; i < h->prof_calls_max * (kProfStages + 1); ++i)
+      if (h->prof_events[i]) cudaEventDestroy(static_cast<cudaEvent_t>(h->prof_events[i]));
+    delete[] h->prof_events;
+  }
+  delete h;
+  return LCO_OK;
+}
+
+lco_status lco_workspace_size(lco_handle h, uint64_t nnz, size_t* bytes) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (!bytes) {
+    set_error("bytes is NULL");
+    return LCO_ERR_NULL;
+  }
+  const OpPlan& a = h->op_permute;
+  const OpPlan& b = h->op_sort;
+  size_t x = layout_for(a.path, a.passes, a.radix_bits, nnz).total;
+  size_t y = layout_for(b.path, b.passes, b.radix_bits, nnz).total;
+  // partition (up to 2048 ranks) uses at most a single 11-bit pass
+  size_t z = layout_for(kPathOnesweep, 1, 11, nnz).total;
+  size_t m = x > y ? x : y;
+  *bytes = m > z ? m : z;
+  return LCO_OK;
+}
+
+lco_status lco_permute(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
+                       const double* vals_in, const uint32_t* idx_in, uint64_t* keys_out,
+                       double* vals_out, uint32_t* perm_out, void* workspace,
+                       size_t workspace_bytes, void* stream) {
+  if (!h) return check_handle(h);
+  return run_op(h, h->op_permute, false, nnz, keys_in, vals_in, idx_in, keys_out, vals_out,
+                perm_out, workspace, workspace_bytes, stream);
+}
+
+lco_status lco_sort(lco_handle h, uint64_t nnz, const uint64_t* keys_in, const double* vals_in,
+                    const uint32_t* idx_in, uint64_t* keys_out, double* vals_out,
+                    uint32_t* perm_out, void* workspace, size_t workspace_bytes, void* stream) {
+  if (!h) return check_handle(h);
+  return run_op(h, h->op_sort, true, nnz, keys_in, vals_in, idx_in, keys_out, vals_out,
+                perm_out, workspace, workspace_bytes, stream);
+}
+
+lco_status lco_host_workspace_size(lco_handle h, uint64_t nnz, size_t* bytes) {
+  size_t inner = 0;
+  lco_status st = lco_workspace_size(h, nnz, &inner);
+  if (st) return st;
+  *bytes = 4 * align_up(nnz * 8) + align_up(nnz * 4) + inner;
+  return LCO_OK;
+}
+
+lco_status lco_permute_host(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
+                            const double* vals_in, uint64_t* keys_out, double* vals_out,
+                            uint32_t* perm_out, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (nnz == 0) return LCO_OK;
+  if (!keys_in || !keys_out) {
+    set_error("keys_in and keys_out are required");
+    return LCO_ERR_NULL;
+  }
+  if ((vals_in == nullptr) != (vals_out == nullptr)) {
+    set_error("vals_in and vals_out must both be given or both be NULL");
+    return LCO_ERR_ARG;
+  }
+  size_t need = 0;
+  lco_host_workspace_size(h, nnz, &need);
+  if (!workspace || workspace_bytes < need || reinterpret_cast<uintptr_t>(workspace) % kAlign) {
+    set_error("host-path workspace needs %zu bytes, 256-byte aligned", need);
+    return LCO_ERR_WORKSPACE;
+  }
+  char* ws = static_cast<char*>(workspace);
+  const size_t a8 = align_up(nnz * 8), a4 = align_up(nnz * 4);
+  uint64_t* dk = reinterpret_cast<uint64_t*>(ws);
+  double* dv = reinterpret_cast<double*>(ws + a8);
+  uint64_t* ok = reinterpret_cast<uint64_t*>(ws + 2 * a8);
+  double* ov = reinterpret_cast<double*>(ws + 3 * a8);
+  uint32_t* op = reinterpret_cast<uint32_t*>(ws + 4 * a8);
+  char* inner = ws + 4 * a8 + a4;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemcpyAsync(dk, keys_in, nnz * 8, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && vals_in) e = cudaMemcpyAsync(dv, vals_in, nnz * 8, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "lco_permute_host H2D");
+  st = lco_permute(h, nnz, dk, vals_in ? dv : nullptr, nullptr, ok, vals_in ? ov : nullptr,
+                   perm_out ? op : nullptr, inner, workspace_bytes - (inner - ws), stream);
+  if (st) return st;
+  e = cudaMemcpyAsync(keys_out, ok, nnz * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && vals_out) e = cudaMemcpyAsync(vals_out, ov, nnz * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && perm_out) e = cudaMemcpyAsync(perm_out, op, nnz * 4, cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e, "lco_permute_host D2H");
+  return LCO_OK;
+}
+
+lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
+                         const double* vals_in, uint32_t idx_base, int world,
+                         const uint64_t* splitters, uint64_t* send_keys, double* send_vals,
+                         uint32_t* send_idx, uint64_t* send_counts, void* workspace,
+                         size_t workspace_bytes, void* stream) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (world < 1 || world > 2048) {
+    set_error("world %d outside 1..2048", world);
+    return LCO_ERR_ARG;
+  }
+  if (nnz > h->max_nnz || nnz > kMaxOnesweepNnz) {
+    set_error("nnz above max_nnz or 2^30-1");
+    return LCO_ERR_CAPACITY;
+  }
+  if (!send_counts || (world > 1 && !splitters)) {
+    set_error("send_counts (and splitters when world > 1) are required");
+    return LCO_ERR_NULL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nnz == 0) {
+    cudaError_t e = cudaMemsetAsync(send_counts, 0, (size_t)world * 8, s);
+    return e == cudaSuccess ? LCO_OK : cuda_fail(e, "lco_partition");
+  }
+  if (!keys_in || !send_keys || !send_idx) {
+    set_error("keys_in, send_keys and send_idx are required");
+    return LCO_ERR_NULL;
+  }
+  if ((vals_in == nullptr) != (send_vals == nullptr)) {
+    set_error("vals_in and send_vals must both be given or both be NULL");
+    return LCO_ERR_ARG;
+  }
+  const int rb = partition_rb(world);
+  const WsLayout w = layout_for(kPathOnesweep, 1, rb, nnz);
+  if (!workspace || workspace_bytes < w.total || reinterpret_cast<uintptr_t>(workspace) % kAlign) {
+    set_error("workspace needs %zu bytes, 256-byte aligned", w.total);
+    return LCO_ERR_WORKSPACE;
+  }
+  char* ws = static_cast<char*>(workspace);
+  // world == 1: every record goes to rank 0; a single splitter-free pass still applies
+  // (rank_of returns 0 for world 1), so the same kernels run.
+  OnesweepIO io;
+  memset(&io, 0, sizeof io);
+  io.nnz = nnz;
+  io.keys_in = keys_in;
+  io.vals_in = vals_in;
+  io.keys_out = send_keys;
+  io.vals_out = send_vals;
+  io.perm_out = send_idx;
+  io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
+  io.statusA = reinterpret_cast<uint32_t*>(ws + w.statusA);
+  // world == 1: rank_of never reads the splitters, any non-null marker selects the
+  // partition mode of the kernels.
+  io.splitters = world > 1 ? splitters : reinterpret_cast<const uint64_t*>(send_counts);
+  io.world = world;
+  io.idx_base = idx_base;
+  io.counts64 = send_counts;
+  Launch L{s, nullptr, nullptr};
+  ProfCtx pc;
+  const bool prof = prof_begin(h, s, &pc, &L);
+  cudaError_t e = run_onesweep(rb, h->kp_full, io, L);
+  if (prof) prof_end(&pc);
+  if (e != cudaSuccess) return cuda_fail(e, "lco_partition");
+  return LCO_OK;
+}
+
+lco_status lco_key_histogram(lco_handle h, uint64_t nnz, const uint64_t* keys_in, int bits,
+                             uint64_t* counts, void* stream) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (bits < 1 || bits > 14) {
+    set_error("bits %d outside 1..14", bits);
+    return LCO_ERR_ARG;
+  }
+  if (nnz == 0) return LCO_OK;
+  if (!keys_in || !counts) {
+    set_error("keys_in and counts are required");
+    return LCO_ERR_NULL;
+  }
+  const int shift = h->key_bits > bits ? h->key_bits - bits : 0;
+  cudaError_t e = run_keyhist(h->kp_full, nnz, keys_in, shift, 1 << bits, counts,
+                              static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? LCO_OK : cuda_fail(e, "lco_key_histogram");
+}
+
+lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* info) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (!info) {
+    set_error("info is NULL");
+    return LCO_ERR_NULL;
+  }
+  memset(info, 0, sizeof *info);
+  const OpPlan& op = sort ? h->op_sort : h->op_permute;
+  info->order = h->order;
+  for (int t = 0; t < h->order; ++t) info->rearrangement[t] = h->rearr[t];
+  info->norm_order = h->norm_n;
+  for (int m = 0; m < h->norm_n; ++m) {
+    info->norm_dims[m] = h->norm_dims[m];
+    info->norm_perm[m] = h->norm_perm[m];
+  }
+  info->prefix_len = h->prefix_len;
+  info->suffix_start = h->suffix_start;
+  info->segment_divisor = op.segdiv;
+  info->trailing = op.trailing;
+  info->middle_size = op.middle;
+  info->num_segments = op.segments;
+  info->sort_bits = op.sort_bits;
+  info->passes = op.passes;
+  for (int j = 0; j < op.passes && j < 8; ++j) info->digit_bits[j] = op.kp.dbits[j];
+  info->radix_bits = op.radix_bits;
+  info->path = op.path;
+  info->tile = op.path == kPathOnesweep ? onesweep_tile() : 0;
+  info->launches = nnz == 0 ? 0 : (op.path == kPathCopy ? 1 : 1 + op.passes);
+  return LCO_OK;
+}
+
+lco_status lco_fastdiv_host(uint64_t d, uint64_t n, const uint64_t* x, uint64_t* q) {
+  if (d == 0) {
+    set_error("divisor 0");
+    return LCO_ERR_ARG;
+  }
+  if (n && (!x || !q)) {
+    set_error("x and q are required");
+    return LCO_ERR_NULL;
+  }
+  const FastDiv f = make_fastdiv(d);
+  for (uint64_t i = 0; i < n; ++i) q[i] = fdiv(f, x[i]);
+  return LCO_OK;
+}
+
+lco_status lco_profile_enable(lco_handle h, int calls) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (calls < 0 || calls > 64) {
+    set_error("calls %d outside 0..64", calls);
+    return LCO_ERR_ARG;
+  }
+  if (h->prof_events) {
+    for (int i = 0; i < h->prof_calls_max * (kProfStages + 1); ++i)
+      if (h->prof_events[i]) cudaEventDestroy(static_cast<cudaEvent_t>(h->prof_events[i]));
+    delete[] h->prof_events;
+    h->prof_events = nullptr;
+  }
+  h->prof_calls_max = calls;
+  h->prof_calls = 0;
+  h->prof_names[0] = 0;
+  if (!calls) return LCO_OK;
+  const int n = calls * (kProfStages + 1);
+  h->prof_events = new (std::nothrow) void*[n];
+  if (!h->prof_events) {
+    set_error("out of host memory");
+    return LCO_ERR_ARG;
+  }
+  memset(h->prof_events, 0, sizeof(void*) * n);
+  for (int i = 0; i < n; ++i) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreate(&ev);
+    if (e != cudaSuccess) return cuda_fail(e, "lco_profile_enable");
+    h->prof_events[i] = ev;
+  }
+  return LCO_OK;
+}
+
+lco_status lco_profile_read(lco_handle h, int max_calls, int max_stages, float* ms,
+                            int* n_calls, int* n_stages, char* names, size_t names_len) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  const int calls = h->prof_calls < max_calls ? h->prof_calls : max_calls;
+  int stages = 0;
+  for (int c = 0; c < calls; ++c) {
+    const int ns = h->prof_nstages[c < 64 ? c : 63];
+    if (ns > stages) stages = ns;
+    for (int s = 0; s < ns && s < max_stages; ++s) {
+      float t = 0.f;
+      cudaError_t e = cudaEventElapsedTime(
+          &t, static_cast<cudaEvent_t>(h->prof_events[c * (kProfStages + 1) + s]),
+          static_cast<cudaEvent_t>(h->prof_events[c * (kProfStages + 1) + s + 1]));
+      if (e != cudaSuccess) return cuda_fail(e, "lco_profile_read");
+      if (ms) ms[c * max_stages + s] = t;
+    }
+  }
+  if (n_calls) *n_calls = calls;
+  if (n_stages) *n_stages = stages;
+  if (names && names_len) {
+    strncpy(names, h->prof_names, names_len - 1);
+    names[names_len - 1] = 0;
+  }
+  return LCO_OK;
+}
+
+const char* lco_status_string(lco_status s) {
+  switch (s) {
+    case LCO_OK: return "LCO_OK";
+    case LCO_ERR_NULL: return "LCO_ERR_NULL";
+    case LCO_ERR_ORDER: return "LCO_ERR_ORDER";
+    case LCO_ERR_DIM: return "LCO_ERR_DIM";
+    case LCO_ERR_PERM: return "LCO_ERR_PERM";
+    case LCO_ERR_OVERFLOW: return "LCO_ERR_OVERFLOW";
+    case LCO_ERR_CAPACITY: return "LCO_ERR_CAPACITY";
+    case LCO_ERR_WORKSPACE: return "LCO_ERR_WORKSPACE";
+    case LCO_ERR_ALIAS: return "LCO_ERR_ALIAS";
+    case LCO_ERR_UNSORTED: return "LCO_ERR_UNSORTED";
+    case LCO_ERR_KEY_RANGE: return "LCO_ERR_KEY_RANGE";
+    case LCO_ERR_CUDA: return "LCO_ERR_CUDA";
+    case LCO_ERR_ARG: return "LCO_ERR_ARG";
+  }
+  return "LCO_ERR_UNKNOWN";
+}
+
+const char* lco_last_error(void) { return last_error(); }
+
+const char* lco_version(void) { return "lco-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// lco_internal.h — plan structures shared by the host planner (plan.cpp), the C ABI
+// (api.cu) and the kernels (kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/lco.h"
+
+#if defined(__CUDACC__)
+#define LCO_HD __host__ __device__ __forceinline__
+#else
+#define LCO_HD inline
+#endif
+
+namespace lco {
+
+// ---------------------------------------------------------------------------------
+// FastDiv: exact unsigned 64-bit division by a runtime-invariant divisor, the role
+// libdivide plays in the paper ("we use a fast division library",
+// PAPER.md:249).  Written from the Granlund-Montgomery round-up method: for d not a
+// power of two, l = ceil(log2 d), m = floor(2^64 (2^l - d) / d) + 1, and
+//   q = (t + ((x - t) >> 1)) >> (l - 1),  t = mulhi(m, x),
+// exact for every x < 2^64.  Powers of two use a shift.
+// ---------------------------------------------------------------------------------
+struct FastDiv {
+  uint64_t d;
+  uint64_t m;
+  uint32_t s;
+  uint32_t kind;  // 0: d == 1, 1: power of two (x >> s), 2: magic with add
+};
+
+LCO_HD uint64_t mulhi64(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+LCO_HD uint64_t fdiv(const FastDiv& f, uint64_t x) {
+  if (f.kind == 1) return x >> f.s;
+  if (f.kind == 0) return x;
+  uint64_t t = mulhi64(f.m, x);
+  return (t + ((x - t) >> 1)) >> f.s;
+}
+
+FastDiv make_fastdiv(uint64_t d);  // host (plan.cpp); d >= 1
+
+// ---------------------------------------------------------------------------------
+// Device-side plan: everything a kernel needs to turn an old key K into the new key
+// K' and the sort key q = K' div T (the shaved key), and to cut q into radix digits.
+// ---------------------------------------------------------------------------------
+constexpr int kMaxModes = LCO_MAX_ORDER;
+constexpr int kMaxPasses = 8;
+
+struct KeyPlan {
+  int n;                          // normalized order (>= 2 on the radix path)
+  FastDiv div[kMaxModes];         // div[m] divides by n_m (old normalized mode m)
+  uint64_t dim[kMaxModes];        // n_m
+  uint64_t nstride[kMaxModes];    // new-key stride of old mode m
+  FastDiv divT;                   // q = K' div T
+  int passes;                     // P
+  int dshift[kMaxPasses];         // digit j = (q >> dshift[j]) & ((1 << dbits[j]) - 1)
+  int dbits[kMaxPasses];
+};
+
+// LIV shuffle of one key: decode old coordinates from the last mode
+// with fast division, accumulate the new key with the new strides.
+LCO_HD uint64_t reencode(const KeyPlan& p, uint64_t k) {
+  uint64_t out = 0;
+#pragma unroll 1
+  for (int m = p.n - 1; m > 0; --m) {
+    uint64_t q = fdiv(p.div[m], k);
+    out += (k - q * p.dim[m]) * p.nstride[m];
+    k = q;
+  }
+  return out + k * p.nstride[0];
+}
+
+LCO_HD uint32_t digit_of(const KeyPlan& p, uint64_t q, int pass) {
+  return (uint32_t)(q >> p.dshift[pass]) & ((1u << p.dbits[pass]) - 1u);
+}
+
+enum Path { kPathCopy = 0, kPathOnesweep = 1, kPathLocal = 2 };
+
+// Host plan for one operation (permute or sort) of a handle.
+struct OpPlan {
+  int path;
+  int sort_bits;
+  int passes;
+  int radix_bits;   // kernel instantiation: bins per pass = 2^radix_bits
+  int tile;         // nonzeros per tile
+  KeyPlan kp;
+  uint64_t trailing, middle, segments, segdiv;
+};
+
+}  // namespace lco
+
+struct lco_plan_s {
+  int order;
+  uint64_t dims[LCO_MAX_ORDER];
+  int32_t perm[LCO_MAX_ORDER];
+  uint64_t total;      // prod dims
+  int key_bits;        // ceil(log2(total))
+  int32_t rearr[LCO_MAX_ORDER];
+  int norm_n;
+  uint64_t norm_dims[LCO_MAX_ORDER];
+  int32_t norm_perm[LCO_MAX_ORDER];
+  int prefix_len, suffix_start;
+  uint64_t max_nnz;
+  uint32_t flags;
+  lco::OpPlan op_permute;  // nnz-independent parts; path refined per call
+  lco::OpPlan op_sort;
+  lco::KeyPlan kp_full;    // re-encode only (partition, histogram)
+  // profiling
+  int prof_calls_max;
+  int prof_calls;
+  int prof_stages;
+  void** prof_events;      // cudaEvent_t[prof_calls_max * (kProfStages + 1)]
+  int prof_nstages[64];
+  char prof_names[512];
+};
+
+namespace lco {
+constexpr int kProfStages = 16;
+// Host planning (plan.cpp)
+lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int32_t* perm);
+void choose_passes(OpPlan* op, int sort_bits);
+int ceil_log2(uint64_t x);  // smallest b with 2^b >= x
+void set_error(const char* fmt, ...);
+}  // namespace lco

@@ -1,0 +1,225 @@
+// plan.cpp — host planning for the LCO permutation (no CUDA calls).
+//
+// Implements RP step 1 (classify indices, §4.1) and the key shaving
+// of step 2 ("(LIV mod 30) div 3") as a normalized plan:
+//   1. drop size-1 modes (their coordinate is always 0);
+//   2. fuse modes that are adjacent in both the old and the new order (they move as
+//      one mixed-radix digit);
+//   3. prefix a = identity run (those modes keep their significance: segments of
+//      constant prefix are the paper's "regions where k is constant", and they occupy
+//      the same positions before and after), suffix b = longest strictly increasing
+//      tail of the perm (already in new relative order inside every run of equal
+//      prefix+middle, hence "ignored", "the final index j can be
+//      ignored"); the radix passes sort on q = K' div T, T = prod of suffix dims.
+// DESIGN.md §"Plan" proves that a stable sort of the (sorted) input by q yields the
+// new order; tests/test_plan.py checks it against the oracle on every permutation of
+// orders 1-6.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "lco_internal.h"
+
+namespace lco {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+const char* last_error() { return g_last_error.c_str(); }
+
+int ceil_log2(uint64_t x) {
+  int b = 0;
+  while (b < 64 && (1ull << b) < x) ++b;
+  return b;
+}
+
+FastDiv make_fastdiv(uint64_t d) {
+  FastDiv f{d, 0, 0, 0};
+  if (d <= 1) return f;  // kind 0: identity (d == 1)
+  if ((d & (d - 1)) == 0) {
+    f.kind = 1;
+    f.s = (uint32_t)__builtin_ctzll(d);
+    return f;
+  }
+  int l = ceil_log2(d);  // 2^(l-1) < d < 2^l, l <= 63 because d <= 2^63-1
+  unsigned __int128 num = ((unsigned __int128)((1ull << l) - d)) << 64;
+  f.m = (uint64_t)(num / d) + 1;
+  f.s = (uint32_t)(l - 1);
+  f.kind = 2;
+  return f;
+}
+
+// Digit schedule: P = ceil(bits / 11) passes of <= 11 bits, as even as possible
+// (results do not depend on the digit size).
+void choose_passes(OpPlan* op, int bits) {
+  op->sort_bits = bits;
+  if (bits <= 0) {
+    op->passes = 0;
+    op->radix_bits = 0;
+    return;
+  }
+  const int kMaxDigit = 11;
+  int P = (bits + kMaxDigit - 1) / kMaxDigit;
+  int b = (bits + P - 1) / P;
+  op->passes = P;
+  op->radix_bits = b <= 8 ? 8 : (b <= 10 ? 10 : 11);
+  op->kp.passes = P;
+  for (int j = 0; j < P; ++j) {
+    op->kp.dshift[j] = j * b;
+    op->kp.dbits[j] = (j < P - 1) ? b : bits - (P - 1) * b;
+  }
+  op->tile = 4096;
+}
+
+static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64_t T) {
+  KeyPlan kp;
+  memset(&kp, 0, sizeof kp);
+  kp.n = n;
+  uint64_t stride_at[kMaxModes];
+  uint64_t acc = 1;
+  for (int t = n - 1; t >= 0; --t) {
+    stride_at[t] = acc;
+    acc *= nd[np[t]];
+  }
+  for (int t = 0; t < n; ++t) kp.nstride[np[t]] = stride_at[t];
+  for (int m = 0; m < n; ++m) {
+    kp.dim[m] = nd[m];
+    kp.div[m] = make_fastdiv(nd[m]);
+  }
+  if (n == 0) kp.nstride[0] = 1;
+  kp.divT = make_fastdiv(T);
+  return kp;
+}
+
+lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int32_t* perm) {
+  h->order = order;
+  uint64_t total = 1;
+  for (int m = 0; m < order; ++m) {
+    h->dims[m] = dims[m];
+    h->perm[m] = perm ? perm[m] : m;
+    if (dims[m] == 0) {
+      set_error("dims[%d] == 0", m);
+      return LCO_ERR_DIM;
+    }
+  }
+  int seen[LCO_MAX_ORDER] = {0};
+  for (int t = 0; t < order; ++t) {
+    int p = h->perm[t];
+    if (p < 0 || p >= order || seen[p]) {
+      set_error("perm is not a bijection on 0..%d (perm[%d] = %d)", order - 1, t, p);
+      return LCO_ERR_PERM;
+    }
+    seen[p] = 1;
+  }
+  for (int m = 0; m < order; ++m) {
+    if (total > 0x7fffffffffffffffull / dims[m]) {
+      set_error("product of dims exceeds 2^63-1 (PAPER.md:173)");
+      return LCO_ERR_OVERFLOW;
+    }
+    total *= dims[m];
+  }
+  h->total = total;
+  h->key_bits = ceil_log2(total);
+
+  // RP step 1: perm[t] is a rearrangement index iff it crosses a mode
+  // that was more significant before, i.e. iff it is not the minimum of perm[t..].
+  for (int t = 0; t < order; ++t) {
+    int mn = h->perm[t];
+    for (int u = t + 1; u < order; ++u)
+      if (h->perm[u] < mn) mn = h->perm[u];
+    h->rearr[t] = h->perm[t] != mn;
+  }
+
+  // normalization 1: drop size-1 modes
+  int keep[LCO_MAX_ORDER];
+  uint64_t d1[LCO_MAX_ORDER];
+  int n1 = 0;
+  for (int m = 0; m < order; ++m) {
+    keep[m] = dims[m] > 1 ? n1 : -1;
+    if (dims[m] > 1) d1[n1++] = dims[m];
+  }
+  int p1[LCO_MAX_ORDER];
+  int k = 0;
+  for (int t = 0; t < order; ++t)
+    if (keep[h->perm[t]] >= 0) p1[k++] = keep[h->perm[t]];
+  // normalization 2: fuse runs m, m+1, ... that are consecutive in the new order
+  int gfirst[LCO_MAX_ORDER], glen[LCO_MAX_ORDER], ng = 0;
+  for (int t = 0; t < n1; ++t) {
+    if (t > 0 && p1[t] == p1[t - 1] + 1) {
+      glen[ng - 1]++;
+    } else {
+      gfirst[ng] = p1[t];
+      glen[ng] = 1;
+      ng++;
+    }
+  }
+  h->norm_n = ng;
+  for (int g = 0; g < ng; ++g) {
+    int rank = 0;
+    for (int g2 = 0; g2 < ng; ++g2)
+      if (gfirst[g2] < gfirst[g]) rank++;
+    uint64_t d = 1;
+    for (int i = 0; i < glen[g]; ++i) d *= d1[gfirst[g] + i];
+    h->norm_dims[rank] = d;
+    h->norm_perm[g] = rank;
+  }
+  const int n = ng;
+  const uint64_t* nd = h->norm_dims;
+  const int32_t* np = h->norm_perm;
+  int a = 0;
+  while (a < n && np[a] == a) ++a;
+  int b = n > 0 ? n - 1 : 0;
+  while (b > 0 && np[b - 1] < np[b]) --b;
+  h->prefix_len = a;
+  h->suffix_start = b;
+
+  uint64_t T = 1, S = 1, G = 1, D = 1;
+  for (int t = b; t < n; ++t) T *= nd[np[t]];
+  for (int t = a; t < b; ++t) S *= nd[np[t]];
+  for (int m = 0; m < a && m < n; ++m) G *= nd[m];
+  for (int m = a; m < n; ++m) D *= nd[m];
+
+  // permute: sort on q = K' div T (prefix + middle digits)
+  OpPlan& op = h->op_permute;
+  memset(&op, 0, sizeof op);
+  op.kp = make_keyplan(n, nd, np, n >= 2 ? T : 1);
+  op.trailing = T;
+  op.middle = S;
+  op.segments = G;
+  op.segdiv = D;
+  if (n <= 1) {
+    op.path = kPathCopy;
+    choose_passes(&op, 0);
+  } else {
+    op.path = kPathOnesweep;
+    choose_passes(&op, ceil_log2(G * S));
+  }
+  // sort: q = K' (all key digits)
+  OpPlan& os = h->op_sort;
+  memset(&os, 0, sizeof os);
+  os.kp = make_keyplan(n, nd, np, 1);
+  os.trailing = 1;
+  os.middle = total;
+  os.segments = 1;
+  os.segdiv = total;
+  if (total <= 1) {
+    os.path = kPathCopy;
+    choose_passes(&os, 0);
+  } else {
+    os.path = kPathOnesweep;
+    choose_passes(&os, h->key_bits);
+  }
+  h->kp_full = make_keyplan(n, nd, np, 1);
+  return LCO_OK;
+}
+
+}  // namespace lco

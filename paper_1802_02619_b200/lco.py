@@ -1,0 +1,349 @@
+"""Thin Python binding of liblco.so (include/lco.h) — argument marshalling only.
+
+Every step of the permutation runs in the library's CUDA kernels; this module only
+turns torch tensors into pointers, allocates outputs and the workspace through
+PyTorch's caching allocator, and maps status codes to exceptions.  There is no CPU
+fallback: if liblco.so is missing or the tensors are not on a CUDA device, calls fail.
+
+Names follow the C ABI: ``permute`` (lco_permute), ``sort`` (lco_sort),
+``permute_host`` (lco_permute_host), ``partition`` (lco_partition),
+``key_histogram`` (lco_key_histogram), ``Plan.info`` (lco_plan_query).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblco.so")
+
+FLAG_VALIDATE = 1
+MAX_ORDER = 16
+PATHS = {0: "copy", 1: "onesweep", 2: "local"}
+
+_STATUS = {
+    0: "LCO_OK", 1: "LCO_ERR_NULL", 2: "LCO_ERR_ORDER", 3: "LCO_ERR_DIM", 4: "LCO_ERR_PERM",
+    5: "LCO_ERR_OVERFLOW", 6: "LCO_ERR_CAPACITY", 7: "LCO_ERR_WORKSPACE", 8: "LCO_ERR_ALIAS",
+    9: "LCO_ERR_UNSORTED", 10: "LCO_ERR_KEY_RANGE", 11: "LCO_ERR_CUDA", 12: "LCO_ERR_ARG",
+}
+
+
+class LcoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class LcoValueError(LcoError, ValueError):
+    pass
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("order", ctypes.c_int),
+        ("rearrangement", ctypes.c_int32 * MAX_ORDER),
+        ("norm_order", ctypes.c_int),
+        ("norm_dims", ctypes.c_uint64 * MAX_ORDER),
+        ("norm_perm", ctypes.c_int32 * MAX_ORDER),
+        ("prefix_len", ctypes.c_int),
+        ("suffix_start", ctypes.c_int),
+        ("segment_divisor", ctypes.c_uint64),
+        ("trailing", ctypes.c_uint64),
+        ("middle_size", ctypes.c_uint64),
+        ("num_segments", ctypes.c_uint64),
+        ("sort_bits", ctypes.c_int),
+        ("passes", ctypes.c_int),
+        ("digit_bits", ctypes.c_int * 8),
+        ("radix_bits", ctypes.c_int),
+        ("path", ctypes.c_int),
+        ("launches", ctypes.c_int),
+        ("tile", ctypes.c_int),
+    ]
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+_P = ctypes.c_void_p
+_U64 = ctypes.c_uint64
+_SIGS = {
+    "lco_create": (ctypes.c_int, [ctypes.POINTER(_P), ctypes.c_int, ctypes.POINTER(_U64),
+                                  ctypes.POINTER(ctypes.c_int32), _U64, ctypes.c_uint32]),
+    "lco_destroy": (ctypes.c_int, [_P]),
+    "lco_workspace_size": (ctypes.c_int, [_P, _U64, ctypes.POINTER(ctypes.c_size_t)]),
+    "lco_host_workspace_size": (ctypes.c_int, [_P, _U64, ctypes.POINTER(ctypes.c_size_t)]),
+    "lco_permute": (ctypes.c_int, [_P, _U64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "lco_sort": (ctypes.c_int, [_P, _U64, _P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "lco_permute_host": (ctypes.c_int, [_P, _U64, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
+    "lco_partition": (ctypes.c_int, [_P, _U64, _P, _P, ctypes.c_uint32, ctypes.c_int, _P, _P, _P,
+                                     _P, _P, _P, ctypes.c_size_t, _P]),
+    "lco_key_histogram": (ctypes.c_int, [_P, _U64, _P, ctypes.c_int, _P, _P]),
+    "lco_plan_query": (ctypes.c_int, [_P, _U64, ctypes.c_int, ctypes.POINTER(PlanInfo)]),
+    "lco_fastdiv_host": (ctypes.c_int, [_U64, _U64, _P, _P]),
+    "lco_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
+    "lco_profile_read": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P,
+                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                        ctypes.c_char_p, ctypes.c_size_t]),
+    "lco_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "lco_last_error": (ctypes.c_char_p, []),
+    "lco_version": (ctypes.c_char_p, []),
+}
+
+
+def lib():
+    """Load liblco.so (raises if it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        with _lib_lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError(
+                        f"{LIB_PATH} is missing; build it with "
+                        "`python -c 'import __graft_entry__ as g; g.build()'`")
+                L = ctypes.CDLL(LIB_PATH)
+                for name, (res, args) in _SIGS.items():
+                    f = getattr(L, name)
+                    f.restype = res
+                    f.argtypes = args
+                _lib = L
+    return _lib
+
+
+def _check(status):
+    if status != 0:
+        msg = lib().lco_last_error().decode(errors="replace")
+        cls = LcoValueError if status in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12) else LcoError
+        raise cls(status, msg)
+
+
+def version() -> str:
+    return lib().lco_version().decode()
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream, device):
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _workspace(nbytes, device):
+    if nbytes == 0:
+        return None, 0
+    buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+    off = (-buf.data_ptr()) % 256
+    return buf, off
+
+
+class Plan:
+    """An lco_handle: the host plan for (dims, perm).  Immutable; reusable."""
+
+    def __init__(self, dims, perm=None, max_nnz=(1 << 32) - 1, validate=False):
+        self.dims = tuple(int(d) for d in dims)
+        order = len(self.dims)
+        self.perm = tuple(range(order)) if perm is None else tuple(int(p) for p in perm)
+        d = (ctypes.c_uint64 * max(order, 1))(*self.dims)
+        p = (ctypes.c_int32 * max(order, 1))(*self.perm)
+        h = ctypes.c_void_p()
+        _check(lib().lco_create(ctypes.byref(h), order, d, p, int(max_nnz),
+                                FLAG_VALIDATE if validate else 0))
+        self._h = h
+        self.max_nnz = int(max_nnz)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.lco_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def new_dims(self):
+        return tuple(self.dims[p] for p in self.perm)
+
+    def workspace_size(self, nnz: int) -> int:
+        n = ctypes.c_size_t()
+        _check(lib().lco_workspace_size(self._h, int(nnz), ctypes.byref(n)))
+        return n.value
+
+    def host_workspace_size(self, nnz: int) -> int:
+        n = ctypes.c_size_t()
+        _check(lib().lco_host_workspace_size(self._h, int(nnz), ctypes.byref(n)))
+        return n.value
+
+    def info(self, nnz: int, sort: bool = False) -> dict:
+        pi = PlanInfo()
+        _check(lib().lco_plan_query(self._h, int(nnz), 1 if sort else 0, ctypes.byref(pi)))
+        n = pi.norm_order
+        return {
+            "order": pi.order,
+            "rearrangement": list(pi.rearrangement[:pi.order]),
+            "norm_dims": [int(x) for x in pi.norm_dims[:n]],
+            "norm_perm": list(pi.norm_perm[:n]),
+            "prefix_len": pi.prefix_len,
+            "suffix_start": pi.suffix_start,
+            "segment_divisor": int(pi.segment_divisor),
+            "trailing": int(pi.trailing),
+            "middle_size": int(pi.middle_size),
+            "num_segments": int(pi.num_segments),
+            "sort_bits": pi.sort_bits,
+            "passes": pi.passes,
+            "digit_bits": list(pi.digit_bits[:pi.passes]),
+            "radix_bits": pi.radix_bits,
+            "path": PATHS.get(pi.path, pi.path),
+            "launches": pi.launches,
+            "tile": pi.tile,
+        }
+
+    # ---------------------------------------------------------------- device calls
+    def _run(self, fn, keys, vals, idx, return_perm, stream, out, workspace):
+        if not keys.is_cuda:
+            raise ValueError("keys must be a CUDA tensor (no CPU fallback)")
+        if keys.dtype not in (torch.int64, torch.uint64) or keys.dim() != 1:
+            raise ValueError("keys must be a 1-D int64/uint64 tensor")
+        keys = keys.contiguous()
+        dev = keys.device
+        n = keys.numel()
+        if vals is not None:
+            if vals.dtype != torch.float64 or vals.numel() != n or vals.device != dev:
+                raise ValueError("vals must be float64, same length and device as keys")
+            vals = vals.contiguous()
+        if idx is not None:
+            if idx.dtype not in (torch.int32, torch.uint32) or idx.numel() != n or idx.device != dev:
+                raise ValueError("idx must be int32/uint32, same length and device as keys")
+            idx = idx.contiguous()
+        if out is None:
+            ko = torch.empty_like(keys)
+            vo = None if vals is None else torch.empty_like(vals)
+            po = torch.empty(n, dtype=torch.int32, device=dev) if return_perm else None
+        else:
+            ko, vo, po = out
+        if workspace is None:
+            ws, off = _workspace(self.workspace_size(n), dev)
+        else:
+            ws, off = workspace, (-workspace.data_ptr()) % 256
+        wptr = None if ws is None else ctypes.c_void_p(ws.data_ptr() + off)
+        wlen = 0 if ws is None else ws.numel() - off
+        with torch.cuda.device(dev):
+            _check(fn(self._h, n, _ptr(keys), _ptr(vals), _ptr(idx), _ptr(ko), _ptr(vo), _ptr(po),
+                      wptr, wlen, _stream_ptr(stream, dev)))
+        return ko, vo, po
+
+    def permute(self, keys, vals=None, idx=None, return_perm=True, stream=None, out=None,
+                workspace=None):
+        return self._run(lib().lco_permute, keys, vals, idx, return_perm, stream, out, workspace)
+
+    def sort(self, keys, vals=None, idx=None, return_perm=True, stream=None, out=None,
+             workspace=None):
+        return self._run(lib().lco_sort, keys, vals, idx, return_perm, stream, out, workspace)
+
+    def permute_host(self, keys, vals=None, return_perm=True, device=None, stream=None,
+                     out=None, workspace=None):
+        """Host (ideally pinned) tensors in and out; copies run inside the call."""
+        if keys.is_cuda:
+            raise ValueError("permute_host takes host tensors")
+        dev = torch.device(device or "cuda")
+        n = keys.numel()
+        if out is None:
+            pin = keys.is_pinned()
+            ko = torch.empty(n, dtype=keys.dtype, pin_memory=pin)
+            vo = None if vals is None else torch.empty(n, dtype=torch.float64, pin_memory=pin)
+            po = torch.empty(n, dtype=torch.int32, pin_memory=pin) if return_perm else None
+        else:
+            ko, vo, po = out
+        if workspace is None:
+            ws, off = _workspace(self.host_workspace_size(n), dev)
+        else:
+            ws, off = workspace, (-workspace.data_ptr()) % 256
+        wptr = None if ws is None else ctypes.c_void_p(ws.data_ptr() + off)
+        wlen = 0 if ws is None else ws.numel() - off
+        with torch.cuda.device(dev):
+            _check(lib().lco_permute_host(self._h, n, _ptr(keys), _ptr(vals), _ptr(ko), _ptr(vo),
+                                          _ptr(po), wptr, wlen, _stream_ptr(stream, dev)))
+        return ko, vo, po
+
+    def partition(self, keys, vals, idx_base, splitters, stream=None, workspace=None):
+        """Stable multisplit by new-key range: returns (send_keys, send_vals, send_idx,
+        send_counts) on the device; send_keys are OLD keys."""
+        dev = keys.device
+        n = keys.numel()
+        world = 1 if splitters is None else splitters.numel() + 1
+        sk = torch.empty_like(keys)
+        sv = None if vals is None else torch.empty_like(vals)
+        si = torch.empty(n, dtype=torch.int32, device=dev)
+        cnt = torch.zeros(world, dtype=torch.int64, device=dev)
+        if workspace is None:
+            ws, off = _workspace(self.workspace_size(n), dev)
+        else:
+            ws, off = workspace, (-workspace.data_ptr()) % 256
+        wptr = None if ws is None else ctypes.c_void_p(ws.data_ptr() + off)
+        wlen = 0 if ws is None else ws.numel() - off
+        sp = None if splitters is None else splitters.contiguous()
+        with torch.cuda.device(dev):
+            _check(lib().lco_partition(self._h, n, _ptr(keys), _ptr(vals), int(idx_base), world,
+                                       _ptr(sp), _ptr(sk), _ptr(sv), _ptr(si), _ptr(cnt), wptr,
+                                       wlen, _stream_ptr(stream, dev)))
+        return sk, sv, si, cnt
+
+    def key_histogram(self, keys, bits, counts=None, stream=None):
+        dev = keys.device
+        if counts is None:
+            counts = torch.zeros(1 << bits, dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            _check(lib().lco_key_histogram(self._h, keys.numel(), _ptr(keys), int(bits),
+                                           _ptr(counts), _stream_ptr(stream, dev)))
+        return counts
+
+    # ---------------------------------------------------------------- measurement hook
+    def profile_enable(self, calls: int):
+        _check(lib().lco_profile_enable(self._h, int(calls)))
+
+    def profile_read(self, max_calls=64, max_stages=17):
+        ms = (ctypes.c_float * (max_calls * max_stages))()
+        nc, ns = ctypes.c_int(), ctypes.c_int()
+        names = ctypes.create_string_buffer(1024)
+        _check(lib().lco_profile_read(self._h, max_calls, max_stages, ctypes.cast(ms, _P),
+                                      ctypes.byref(nc), ctypes.byref(ns), names, 1024))
+        stage_names = names.value.decode().split(";") if names.value else []
+        rows = [[ms[c * max_stages + s] for s in range(ns.value)] for c in range(nc.value)]
+        return stage_names, rows
+
+
+_plan_cache: dict = {}
+
+
+def plan(dims, perm=None, max_nnz=(1 << 32) - 1, validate=False) -> Plan:
+    key = (tuple(int(d) for d in dims), None if perm is None else tuple(int(p) for p in perm),
+           int(max_nnz), bool(validate))
+    p = _plan_cache.get(key)
+    if p is None:
+        p = _plan_cache[key] = Plan(dims, perm, max_nnz, validate)
+    return p
+
+
+def permute(keys, vals, dims, perm, idx=None, return_perm=True, validate=False, stream=None):
+    """Permute a sorted LCO tensor: returns (keys_out, vals_out, perm_out)."""
+    return plan(dims, perm, validate=validate).permute(keys, vals, idx, return_perm, stream)
+
+
+def sort(keys, vals, dims, perm=None, idx=None, return_perm=True, validate=False, stream=None):
+    """Sort an LCO tensor in any order into the order given by perm (stable)."""
+    return plan(dims, perm, validate=validate).sort(keys, vals, idx, return_perm, stream)
+
+
+def fastdiv_host(d: int, xs) -> list:
+    """Host reference of the device fast divisor (test hook)."""
+    n = len(xs)
+    xa = (ctypes.c_uint64 * max(n, 1))(*[int(x) for x in xs])
+    qa = (ctypes.c_uint64 * max(n, 1))()
+    _check(lib().lco_fastdiv_host(int(d), n, ctypes.cast(xa, _P), ctypes.cast(qa, _P)))
+    return [int(qa[i]) for i in range(n)]

@@ -1,0 +1,287 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Keys and the permutation vector must be identical; values are compared as 64-bit
+patterns (they are moved, never computed on).  Sizes span several tiles and a ragged
+tail; full BASELINE sizes are checked against the oracle where it finishes in seconds
+(C1-C3), and at C4/C5 scale with the certificate (perm bijection, key = re-encode of its
+source, value bits, strict increase), which with unique keys implies equality with the
+oracle, plus oracle re-encodes of sampled outputs.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1802_02619_b200 as lco
+import workloads
+from tests import brute
+
+pytestmark = pytest.mark.gpu
+
+TILE = 4096
+
+
+def _np_u64(t):
+    return t.detach().cpu().numpy().view(np.uint64) if t.dtype == torch.int64 else \
+        t.detach().cpu().numpy().astype(np.uint64)
+
+
+def check(dims, perm, keys, vals, idx=None, sort=False, dev="cuda:0", return_perm=True):
+    """Run the CUDA path and the oracle on the same inputs; compare bit-exactly."""
+    k = torch.as_tensor(np.asarray(keys, dtype=np.uint64).view(np.int64)).to(dev)
+    v = None if vals is None else torch.as_tensor(np.asarray(vals, dtype=np.float64)).to(dev)
+    ix = None if idx is None else torch.as_tensor(np.asarray(idx, dtype=np.uint32).view(np.int32)).to(dev)
+    p = lco.plan(dims, perm)
+    fn = p.sort if sort else p.permute
+    ko, vo, po = fn(k, v, ix, return_perm=return_perm)
+    torch.cuda.synchronize()
+    ofn = oracle.sort if sort else oracle.permute
+    ek, ev, ep = ofn(dims, perm, np.asarray(keys, dtype=np.uint64), vals, idx)
+    assert np.array_equal(_np_u64(ko), ek), ("keys", dims, perm)
+    if vals is not None:
+        assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64)), ("vals", dims, perm)
+    if return_perm:
+        assert np.array_equal(po.cpu().numpy().view(np.uint32), ep), ("perm", dims, perm)
+    return ko, vo, po
+
+
+def _rand_sorted(rng, dims, nnz):
+    total = int(np.prod(dims))
+    if total <= 4 * nnz:
+        keys = np.sort(rng.choice(total, min(nnz, total), replace=False))
+    else:
+        keys = np.unique(rng.integers(0, total, int(nnz * 1.1), dtype=np.int64))[:nnz]
+    return keys.astype(np.uint64), rng.standard_normal(len(keys))
+
+
+# ------------------------------------------------------------------ random shapes
+@pytest.mark.parametrize("order", [2, 3, 4, 5])
+def test_all_perms_random(order, cuda_device):
+    """Every permutation of orders 2-5, multi-tile with a ragged tail, non-pow2 dims."""
+    rng = np.random.default_rng(10 + order)
+    dims = {2: (1500, 997), 3: (120, 77, 96), 4: (37, 64, 29, 50), 5: (13, 16, 11, 9, 20)}[order]
+    keys, vals = _rand_sorted(rng, dims, 3 * TILE + 1234)
+    for perm in itertools.permutations(range(order)):
+        check(dims, perm, keys, vals)
+
+
+def test_fig2_shape_nonpow2(cuda_device):
+    """Paper Fig 2 shape: order 5, N = 2^10-1 per mode, random support,
+    non-power-of-two division on every mode; all 120 perms on a subsample."""
+    rng = np.random.default_rng(7)
+    dims = (1023,) * 5
+    keys, vals = _rand_sorted(rng, dims, 40_000)
+    for perm in itertools.permutations(range(5)):
+        check(dims, perm, keys, vals)
+
+
+def test_tile_boundaries_and_tiny(cuda_device):
+    rng = np.random.default_rng(3)
+    dims, perm = (64, 64, 64), (2, 0, 1)
+    for nnz in (1, 2, 31, 32, 33, TILE - 1, TILE, TILE + 1, 2 * TILE, 5 * TILE + 17):
+        keys, vals = _rand_sorted(rng, dims, nnz)
+        check(dims, perm, keys, vals)
+
+
+def test_empty(cuda_device):
+    p = lco.plan((8, 8), (1, 0))
+    k = torch.empty(0, dtype=torch.int64, device=cuda_device)
+    v = torch.empty(0, dtype=torch.float64, device=cuda_device)
+    ko, vo, po = p.permute(k, v)
+    assert ko.numel() == 0 and vo.numel() == 0 and po.numel() == 0
+
+
+def test_copy_paths(cuda_device):
+    rng = np.random.default_rng(4)
+    keys, vals = _rand_sorted(rng, (40, 1, 50), 1500)
+    check((40, 1, 50), (0, 1, 2), keys, vals)   # identity
+    check((40, 1, 50), (1, 0, 2), keys, vals)   # only a size-1 mode moves
+    check((2000,), (0,), keys[keys < 2000], vals[keys < 2000])  # order 1
+
+
+def test_options(cuda_device):
+    """idx_in passthrough, keys-only, no perm output."""
+    rng = np.random.default_rng(5)
+    dims = (100, 90, 80)
+    keys, vals = _rand_sorted(rng, dims, 3 * TILE)
+    idx = rng.permutation(len(keys)).astype(np.uint32) + 7
+    for perm in ((2, 1, 0), (1, 0, 2), (0, 2, 1)):
+        check(dims, perm, keys, vals, idx=idx)
+        check(dims, perm, keys, None)
+        check(dims, perm, keys, vals, return_perm=False)
+
+
+def test_max_order_and_special_values(cuda_device):
+    rng = np.random.default_rng(6)
+    dims = (2,) * 16
+    keys, _ = _rand_sorted(rng, dims, 20_000)
+    vals = np.array([np.nan, -0.0, np.inf, -np.inf, 5e-324] * 4000)[:len(keys)]
+    vals[0] = np.frombuffer(np.uint64(0x7ff8dead0000beef).tobytes(), dtype=np.float64)[0]
+    for perm in (tuple(range(15, -1, -1)), (1, 0) + tuple(range(2, 16)), (8,) + tuple(range(8)) + tuple(range(9, 16))):
+        check(dims, perm, keys, vals)
+
+
+def test_large_keys_near_limit(cuda_device):
+    """prod(dims) close to 2^63-1 with non-pow2 modes."""
+    rng = np.random.default_rng(8)
+    dims = (3037000499, 3037000499)  # product 9223372030926249001 < 2^63-1
+    keys = np.unique(rng.integers(0, 2 ** 63 - 2 ** 40, 30_000, dtype=np.int64)).astype(np.uint64)
+    keys = keys[keys < dims[0] * dims[1]]
+    check(dims, (1, 0), keys, rng.standard_normal(len(keys)))
+
+
+# ------------------------------------------------------------------ lco_sort
+def test_sort_unsorted_with_duplicates(cuda_device):
+    rng = np.random.default_rng(9)
+    dims = (50, 60, 70)
+    keys = rng.integers(0, 50 * 60 * 70, 30_000).astype(np.uint64)  # duplicates likely
+    vals = rng.standard_normal(len(keys))
+    for perm in ((0, 1, 2), (2, 1, 0), (1, 2, 0)):
+        check(dims, perm, keys, vals, sort=True)
+
+
+def test_sort_equals_permute_on_sorted(cuda_device):
+    rng = np.random.default_rng(12)
+    dims = (64, 32, 48, 16)
+    keys, vals = _rand_sorted(rng, dims, 50_000)
+    for perm in ((3, 1, 2, 0), (0, 2, 1, 3)):
+        a = check(dims, perm, keys, vals)
+        b = check(dims, perm, keys, vals, sort=True)
+        assert all(torch.equal(x, y) for x, y in zip(a, b))
+
+
+# ------------------------------------------------------------------ BASELINE configs
+@pytest.mark.parametrize("name,scale", [("C1", None), ("C2", 96), ("C3", 20), ("C4", 100),
+                                        ("C5", 300_000)])
+def test_baseline_configs_scaled(name, scale, cuda_device):
+    w = workloads.config(name, scale=scale)
+    for perm in w.perms:
+        check(w.dims, perm, _np_u64(w.keys), w.vals.numpy())
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_baseline_full_vs_oracle(name, cuda_device):
+    w = workloads.config(name)
+    for perm in w.perms:
+        check(w.dims, perm, _np_u64(w.keys), w.vals.numpy())
+
+
+def _torch_reencode(keys, dims, perm):
+    """Independent re-encode with torch // and % (test-side, not the kernels)."""
+    c = []
+    k = keys.clone()
+    for d in reversed(dims):
+        c.append(k % d)
+        k = k // d
+    c = c[::-1]
+    out = torch.zeros_like(keys)
+    for p in perm:
+        out = out * dims[p] + c[p]
+    return out
+
+
+def certificate_gpu(w, perm, ko, vo, po):
+    n = w.keys.numel()
+    dev = ko.device
+    kin = w.keys.to(dev)
+    src = po.long()
+    assert torch.equal(torch.sort(src).values, torch.arange(n, device=dev)), "perm not a bijection"
+    assert torch.equal(ko, _torch_reencode(kin[src], w.dims, perm)), "key != re-encode(source)"
+    assert torch.equal(vo.view(torch.int64), w.vals.to(dev)[src].view(torch.int64)), "vals"
+    assert bool((ko[1:] > ko[:-1]).all()), "not strictly increasing"
+    # sampled outputs re-encoded by the oracle itself
+    g = torch.Generator().manual_seed(1)
+    s = torch.randint(0, n, (2000,), generator=g)
+    ks = _np_u64(kin[src[s.to(dev)]])
+    assert np.array_equal(oracle.shuffle(w.dims, perm, ks), _np_u64(ko[s.to(dev)]))
+
+
+def test_c4_full_certificate(cuda_device):
+    w = workloads.config("C4", device=cuda_device)
+    for perm in w.perms:
+        ko, vo, po = lco.permute(w.keys, w.vals, w.dims, perm)
+        torch.cuda.synchronize()
+        certificate_gpu(w, perm, ko, vo, po)
+        # closed form: 13 nonzeros per grid point, output ordered by (y, x, x', y')
+        n = w.dims[0]
+        y = ko // (n ** 3)
+        assert torch.equal(torch.bincount(y, minlength=n).cpu()[2:-2],
+                           torch.full((n - 4,), 13 * n - 20, dtype=torch.int64))
+
+
+def test_c5_full_certificate(cuda_device):
+    w = workloads.config("C5", device=cuda_device)
+    perm = w.perms[0]
+    ko, vo, po = lco.permute(w.keys, w.vals, w.dims, perm)
+    torch.cuda.synchronize()
+    certificate_gpu(w, perm, ko, vo, po)
+    del ko, vo, po
+    # full-size oracle parity on a contiguous slice (itself a sorted LCO tensor)
+    sl = slice(123_456_789, 123_456_789 + 3_000_000)
+    ks, vs = w.keys[sl].contiguous(), w.vals[sl].contiguous()
+    ko, vo, po = lco.permute(ks, vs, w.dims, perm)
+    ek, ev, ep = oracle.permute(w.dims, perm, _np_u64(ks), vs.cpu().numpy())
+    assert np.array_equal(_np_u64(ko), ek) and np.array_equal(po.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64))
+
+
+# ------------------------------------------------------------------ other entry points
+def test_permute_host_matches_device(cuda_device):
+    w = workloads.config("C2", scale=64)
+    perm = w.perms[0]
+    p = lco.plan(w.dims, perm)
+    kh, vh = w.keys.pin_memory(), w.vals.pin_memory()
+    ko, vo, po = p.permute_host(kh, vh)
+    torch.cuda.synchronize()
+    ek, ev, ep = oracle.permute(w.dims, perm, _np_u64(w.keys), w.vals.numpy())
+    assert np.array_equal(_np_u64(ko), ek) and np.array_equal(po.numpy().view(np.uint32), ep)
+    assert np.array_equal(vo.numpy().view(np.uint64), ev.view(np.uint64))
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_partition_vs_oracle(world, cuda_device):
+    rng = np.random.default_rng(world)
+    dims, perm = (256, 128, 64), (2, 0, 1)
+    keys, vals = _rand_sorted(rng, dims, 5 * TILE + 99)
+    total = int(np.prod(dims))
+    spl = np.sort(rng.choice(total, world - 1, replace=False)).astype(np.uint64)
+    p = lco.plan(dims, perm)
+    k = torch.as_tensor(keys.view(np.int64)).to(cuda_device)
+    v = torch.as_tensor(vals).to(cuda_device)
+    sk, sv, si, cnt = p.partition(k, v, 1000, torch.as_tensor(spl.view(np.int64)).to(cuda_device))
+    ek, ev, ei, ec = oracle.partition(dims, perm, keys, vals, 1000, spl)
+    assert np.array_equal(_np_u64(sk), ek) and np.array_equal(si.cpu().numpy().view(np.uint32), ei)
+    assert np.array_equal(sv.cpu().numpy().view(np.uint64), ev.view(np.uint64))
+    assert cnt.cpu().numpy().tolist() == ec.tolist()
+
+
+def test_key_histogram(cuda_device):
+    rng = np.random.default_rng(2)
+    dims, perm = (100, 200, 300), (1, 2, 0)
+    keys, _ = _rand_sorted(rng, dims, 50_000)
+    p = lco.plan(dims, perm)
+    c = p.key_histogram(torch.as_tensor(keys.view(np.int64)).to(cuda_device), 8)
+    new = brute.reencode_np(dims, perm)(keys)
+    kb = int(np.ceil(np.log2(100 * 200 * 300)))
+    exp = np.bincount((new >> np.uint64(kb - 8)).astype(np.int64), minlength=256)
+    assert c.cpu().numpy().tolist() == exp.tolist()
+
+
+def test_validate_flag(cuda_device):
+    p = lco.Plan((8, 8), (1, 0), validate=True)
+    k = torch.tensor([3, 2, 9], dtype=torch.int64, device=cuda_device)
+    with pytest.raises(ValueError, match="UNSORTED"):
+        p.permute(k)
+    with pytest.raises(ValueError, match="KEY_RANGE"):
+        p.permute(torch.tensor([3, 64], dtype=torch.int64, device=cuda_device))
+    ko, _, po = p.permute(torch.tensor([2, 3, 9], dtype=torch.int64, device=cuda_device))
+    assert ko.tolist() == [9, 16, 24] and po.tolist() == [2, 0, 1]
+
+
+def test_alias_rejected(cuda_device):
+    p = lco.plan((8, 8), (1, 0))
+    k = torch.arange(10, dtype=torch.int64, device=cuda_device)
+    with pytest.raises(ValueError, match="ALIAS"):
+        p.permute(k, out=(k, None, None))

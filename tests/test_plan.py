@@ -1,0 +1,150 @@
+"""Host logic of liblco.so (CPU only: no device call is made).
+
+* every symbol declared in include/lco.h is exported;
+* the host fast divisor equals plain // (the device kernels use the same arithmetic);
+* the plan: rearrangement/resting classification equals the oracle's,
+  the Fig 3 plan constants, and — the property the GPU path relies on —
+  a stable sort of the sorted input by q = K' div T (T = plan "trailing") reproduces the
+  oracle's output for every permutation of orders 1-6 (the suffix modes are free);
+* argument errors map to the documented statuses.
+"""
+import itertools
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1802_02619_b200 as lco
+from paper_1802_02619_b200 import lco as L
+from tests import brute
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_header_symbols_exported():
+    hdr = open(os.path.join(ROOT, "include", "lco.h")).read()
+    names = re.findall(r"^LCO_API\s+[\w\s\*]+?\b(lco_\w+)\s*\(", hdr, flags=re.M)
+    assert len(names) >= 16
+    lib = lco.lib()
+    for n in names:
+        assert hasattr(lib, n), n
+    assert lco.version().startswith("lco-b200")
+
+
+def test_fastdiv_matches_plain_division():
+    rng = np.random.default_rng(0)
+    divisors = [1, 2, 3, 5, 6, 7, 10, 30, 48, 641, 1023, 3072, 2 ** 10 - 1, 2 ** 10 + 1,
+                2 ** 31 - 1, 2 ** 32 + 1, 2 ** 40 - 3, 2 ** 62 + 1, 2 ** 63 - 1, 6700417]
+    divisors += [int(x) for x in rng.integers(1, 2 ** 63 - 1, 30, dtype=np.int64)]
+    divisors += [int(x) for x in rng.integers(1, 5000, 30)]
+    edge = [0, 1, 2, 2 ** 32 - 1, 2 ** 32, 2 ** 63 - 1, 2 ** 63, 2 ** 64 - 1, 2 ** 64 - 2]
+    for d in divisors:
+        xs = edge + [d - 1, d, d + 1, 2 * d - 1, 2 * d, (2 ** 64 - 1) // d * d,
+                     (2 ** 64 - 1) // d * d - 1]
+        xs += [int(x) for x in rng.integers(0, 2 ** 63, 400, dtype=np.int64)]
+        xs += [int(x) * 2 + 1 for x in rng.integers(0, 2 ** 62, 100, dtype=np.int64)]
+        xs = [x % 2 ** 64 for x in xs]
+        assert lco.fastdiv_host(d, xs) == [x // d for x in xs], d
+    # exhaustive small range
+    for d in range(1, 200):
+        xs = list(range(0, 5000))
+        assert lco.fastdiv_host(d, xs) == [x // d for x in xs]
+
+
+def test_fig3_plan_constants():
+    """10x3x2 a_ijk, {0,1,2}->{1,0,2}: regions of constant k by dividing
+    by n_j n_i = 30; the shaved key (LIV mod 30) div 3 = i; i rearrangement."""
+    p = lco.Plan((2, 3, 10), (0, 2, 1))
+    info = p.info(60)
+    assert info["rearrangement"] == [0, 1, 0]
+    assert info["prefix_len"] == 1 and info["num_segments"] == 2
+    assert info["segment_divisor"] == 30
+    assert info["trailing"] == 3 and info["middle_size"] == 10
+
+
+def _random_dims(rng, order):
+    return tuple(int(x) for x in rng.integers(1, 6 if order <= 4 else 4, order))
+
+
+@pytest.mark.parametrize("order", [1, 2, 3, 4, 5, 6])
+def test_plan_stable_sort_on_shaved_key_equals_oracle(order):
+    rng = np.random.default_rng(order)
+    perms = list(itertools.permutations(range(order)))
+    if len(perms) > 240:
+        perms = [perms[i] for i in rng.choice(len(perms), 240, replace=False)]
+    for perm in perms:
+        dims = _random_dims(rng, order)
+        total = int(np.prod(dims))
+        nnz = int(rng.integers(0, total + 1))
+        keys = np.sort(rng.choice(total, nnz, replace=False)).astype(np.uint64)
+        p = lco.Plan(dims, perm)
+        info = p.info(nnz)
+        assert info["rearrangement"] == oracle.classify(perm)
+        new = brute.reencode_np(dims, perm)(keys)
+        _, _, ep = oracle.permute(dims, perm, keys)
+        if info["path"] == "copy":
+            assert np.array_equal(ep, np.arange(nnz))
+            continue
+        q = new // np.uint64(info["trailing"])
+        assert int(q.max(initial=0)) < 2 ** info["sort_bits"]
+        assert sum(info["digit_bits"]) == info["sort_bits"]
+        assert np.array_equal(np.argsort(q, kind="stable"), ep), (dims, perm)
+        # the sort plan sorts on every key bit (T = 1)
+        si = p.info(nnz, sort=True)
+        assert si["trailing"] == 1 and si["sort_bits"] >= info["sort_bits"]
+
+
+def test_baseline_config_plans():
+    """Key bits the passes sort per BASELINE config (SURVEY.md §8(a) sizes table)."""
+    cases = {
+        ("C1", (64, 48, 32), (2, 0, 1)): (5, 1),
+        ("C2a", (512,) * 4, (2, 3, 0, 1)): (18, 2),
+        ("C2b", (512,) * 4, (0, 2, 1, 3)): (18, 2),
+        ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2)): (21, 2),
+        ("C3b", (128,) * 6, (0, 3, 1, 4, 2, 5)): (28, 3),
+        ("C4", (2048,) * 4, (1, 0, 2, 3)): (11, 1),
+        ("C5", (4096,) * 5, (4, 3, 2, 1, 0)): (48, 5),
+    }
+    for (name, dims, perm), (bits, passes) in cases.items():
+        info = lco.Plan(dims, perm).info(1000)
+        assert (info["sort_bits"], info["passes"]) == (bits, passes), (name, info)
+    c4 = lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(10)
+    assert c4["norm_dims"] == [2048, 2048, 2 ** 22] and c4["norm_perm"] == [1, 0, 2]
+    assert c4["trailing"] == 2048 * 2 ** 22
+
+
+def test_identity_and_size1_moves_are_copies():
+    assert lco.Plan((4, 5, 6), (0, 1, 2)).info(10)["path"] == "copy"
+    assert lco.Plan((4, 1, 6), (1, 0, 2)).info(10)["path"] == "copy"  # only a size-1 mode moves
+    assert lco.Plan((7,), (0,)).info(10)["path"] == "copy"
+
+
+def test_argument_errors():
+    with pytest.raises(ValueError, match="PERM"):
+        lco.Plan((4, 4), (0, 0))
+    with pytest.raises(ValueError, match="OVERFLOW"):
+        lco.Plan((2 ** 32, 2 ** 32), (1, 0))
+    with pytest.raises(ValueError, match="ORDER"):
+        lco.Plan((2,) * 17)
+    with pytest.raises(ValueError, match="DIM"):
+        lco.Plan((4, 0), (1, 0))
+    with pytest.raises(ValueError, match="CAPACITY"):
+        lco.Plan((4, 4), (1, 0), max_nnz=2 ** 32)
+
+
+def test_workspace_sizes():
+    p = lco.Plan((4096,) * 5, (4, 3, 2, 1, 0))
+    ws = p.workspace_size(500_000_000)
+    # two ping-pong (key, position) buffers + two look-back status arrays
+    assert 2 * 12 * 500_000_000 < ws < 2 * 12 * 500_000_000 + 2 * 10 ** 9
+    assert lco.Plan((4, 4), (0, 1)).workspace_size(100) < 1 << 20
+    assert p.host_workspace_size(10) > p.workspace_size(10)
+
+
+def test_no_cpu_fallback():
+    import torch
+    p = lco.Plan((4, 4), (1, 0))
+    with pytest.raises(ValueError, match="CUDA"):
+        p.permute(torch.zeros(3, dtype=torch.int64))
