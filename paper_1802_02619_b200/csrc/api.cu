@@ -20,33 +20,32 @@ namespace {
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
-constexpr uint64_t kMaxOnesweepNnz = (1ull << 30) - 1;  // 30-bit look-back counters
 
 struct WsLayout {
-  size_t ctrl, statusA, statusB, kA, pA, kB, pB, flag, total;
+  size_t ctrl, kA, vA, pA, kB, vB, pB, flag, total;
 };
 
+// Ping-pong buffers carry (K', V, position); V only when values are moved and the
+// position only when a permutation vector is requested (sizes assume both).
 WsLayout layout_for(int path, int passes, int rb, uint64_t nnz) {
   WsLayout w;
   memset(&w, 0, sizeof w);
   size_t off = 0;
   if (path == kPathOnesweep && nnz > 0) {
-    const uint64_t tiles = onesweep_tiles(nnz);
-    const size_t st = (size_t)tiles * ((size_t)1 << rb) * 4;
     w.ctrl = off;
-    off += align_up(onesweep_ctrl_bytes(rb));
-    w.statusA = off;
-    off += align_up(st);
+    off += align_up(pass_ctrl_bytes(rb, nnz));
     if (passes >= 2) {
-      w.statusB = off;
-      off += align_up(st);
       w.kA = off;
+      off += align_up(nnz * 8);
+      w.vA = off;
       off += align_up(nnz * 8);
       w.pA = off;
       off += align_up(nnz * 4);
     }
     if (passes >= 3) {
       w.kB = off;
+      off += align_up(nnz * 8);
+      w.vB = off;
       off += align_up(nnz * 8);
       w.pB = off;
       off += align_up(nnz * 4);
@@ -158,11 +157,6 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
         return LCO_ERR_ALIAS;
       }
   }
-  if (op.path == kPathOnesweep && nnz > kMaxOnesweepNnz) {
-    set_error("nnz %llu above the 2^30-1 limit of the 30-bit look-back counters",
-              (unsigned long long)nnz);
-    return LCO_ERR_CAPACITY;
-  }
   const WsLayout w = layout_for(op.path, op.passes, op.radix_bits, nnz);
   if (!workspace || ws_bytes < w.total || (reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
     set_error("workspace needs %zu bytes, 256-byte aligned (got %zu at %p)", w.total, ws_bytes,
@@ -201,7 +195,7 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
   if (op.path == kPathCopy) {
     e = run_copy(nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, L);
   } else {
-    OnesweepIO io;
+    PassIO io;
     memset(&io, 0, sizeof io);
     io.nnz = nnz;
     io.keys_in = keys_in;
@@ -211,13 +205,14 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
     io.vals_out = vals_out;
     io.perm_out = perm_out;
     io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
-    io.statusA = reinterpret_cast<uint32_t*>(ws + w.statusA);
-    io.statusB = op.passes >= 2 ? reinterpret_cast<uint32_t*>(ws + w.statusB) : nullptr;
+    const bool mv = vals_out != nullptr, mp = perm_out != nullptr;
     io.kA = op.passes >= 2 ? reinterpret_cast<uint64_t*>(ws + w.kA) : nullptr;
-    io.pA = op.passes >= 2 ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
+    io.vA = op.passes >= 2 && mv ? reinterpret_cast<double*>(ws + w.vA) : nullptr;
+    io.pA = op.passes >= 2 && mp ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
     io.kB = op.passes >= 3 ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
-    io.pB = op.passes >= 3 ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
-    e = run_onesweep(op.radix_bits, op.kp, io, L);
+    io.vB = op.passes >= 3 && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
+    io.pB = op.passes >= 3 && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
+    e = run_passes(op.radix_bits, op.kp, io, L);
   }
   if (prof) prof_end(&pc);
   if (e != cudaSuccess) return cuda_fail(e, sort ? "lco_sort" : "lco_permute");
@@ -372,8 +367,8 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
     set_error("world %d outside 1..2048", world);
     return LCO_ERR_ARG;
   }
-  if (nnz > h->max_nnz || nnz > kMaxOnesweepNnz) {
-    set_error("nnz above max_nnz or 2^30-1");
+  if (nnz > h->max_nnz || nnz >= (1ull << 32)) {
+    set_error("nnz above max_nnz or 2^32-1");
     return LCO_ERR_CAPACITY;
   }
   if (!send_counts || (world > 1 && !splitters)) {
@@ -402,7 +397,7 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
   char* ws = static_cast<char*>(workspace);
   // world == 1: every record goes to rank 0; a single splitter-free pass still applies
   // (rank_of returns 0 for world 1), so the same kernels run.
-  OnesweepIO io;
+  PassIO io;
   memset(&io, 0, sizeof io);
   io.nnz = nnz;
   io.keys_in = keys_in;
@@ -411,7 +406,6 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
   io.vals_out = send_vals;
   io.perm_out = send_idx;
   io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
-  io.statusA = reinterpret_cast<uint32_t*>(ws + w.statusA);
   // world == 1: rank_of never reads the splitters, any non-null marker selects the
   // partition mode of the kernels.
   io.splitters = world > 1 ? splitters : reinterpret_cast<const uint64_t*>(send_counts);
@@ -421,7 +415,7 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
   Launch L{s, nullptr, nullptr};
   ProfCtx pc;
   const bool prof = prof_begin(h, s, &pc, &L);
-  cudaError_t e = run_onesweep(rb, h->kp_full, io, L);
+  cudaError_t e = run_passes(rb, h->kp_full, io, L);
   if (prof) prof_end(&pc);
   if (e != cudaSuccess) return cuda_fail(e, "lco_partition");
   return LCO_OK;
@@ -473,8 +467,8 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   for (int j = 0; j < op.passes && j < 8; ++j) info->digit_bits[j] = op.kp.dbits[j];
   info->radix_bits = op.radix_bits;
   info->path = op.path;
-  info->tile = op.path == kPathOnesweep ? onesweep_tile() : 0;
-  info->launches = nnz == 0 ? 0 : (op.path == kPathCopy ? 1 : 1 + op.passes);
+  info->tile = op.path == kPathOnesweep ? pass_tile() : 0;
+  info->launches = nnz == 0 ? 0 : (op.path == kPathCopy ? 1 : 3 * op.passes);
   return LCO_OK;
 }
 

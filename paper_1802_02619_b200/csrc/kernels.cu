@@ -1,57 +1,74 @@
 // kernels.cu — sm_100a kernels of the LCO permutation hot path.
 //
-//   k_copy        identity after normalization: copy keys/values, perm = idx or iota
-//                 ("no data movement" case)
-//   k_hist        one read of the input keys: LIV shuffle + shaved key
-//                 q = K' div T + digit histograms of all radix passes;
-//                 the last CTA scans them into bucket starts
-//   k_pass        one stable LSD radix pass over a digit of q ("stably
-//                 sorted ... original relative ordering is used to break ties"):
-//                 tile load -> (first pass) decode + re-encode -> warp match_any
-//                 ranking -> decoupled look-back across tiles -> shared-memory reorder
-//                 -> coalesced scatter; the last pass writes keys/perm and moves the
-//                 values
-//   k_partition   stable multisplit by new-key range for the sharded path (§8(e))
-//   k_keyhist     histogram of the top bits of K' (splitter selection, §8(e))
-//   k_validate    LCO_FLAG_VALIDATE precondition check
+// One stable radix pass over a digit of the shaved key q = K' div T is a
+// tile-granular reduce-then-scan:
+//   k_count    per tile (4096 nonzeros): LIV shuffle on the first pass,
+//              digit, tile histogram (row of thist) and, per chunk of kChunkTiles tiles,
+//              the chunk sums;
+//   k_scan     per digit, exclusive scan of the chunk sums; the last CTA turns the digit
+//              totals into bucket starts;
+//   k_offsets  per chunk, per digit: running sum over the chunk's tile rows -> the global
+//              position of each tile's first nonzero of each digit (toff);
+//   k_scatter  per tile, in launch order: load -> (first pass) decode + re-encode ->
+//              warp ranking with ballots -> shared-memory reorder -> coalesced scatter of
+//              keys, values and source positions to toff + rank.  Tiles are ranked stably
+//              and their offsets come from the exclusive scan, so the pass is stable
+//              ("original relative ordering is used to break ties"); no
+//              CTA waits on another.
+// Other kernels:
+//   k_copy     identity after normalization
+//   k_keyhist  histogram of the top bits of K' (splitter selection, §8(e))
+//   k_validate LCO_FLAG_VALIDATE precondition check
 //
-// No tensor cores: nothing here is a dense contraction (SURVEY.md §8(d) roofline is
-// HBM bandwidth).
+// No tensor cores: nothing here is a dense contraction (HBM bound).
+// Measured alternatives that were replaced: a decoupled
+// look-back (onesweep) pass, whose look-back chain over 1024-2048 bins advanced a few
+// tiles per L2 round trip; static per-CTA chunks, whose 296 x bins write frontiers
+// overflowed L2 write combining (1.8x DRAM write traffic); match_any ranking, which is
+// MIO-bound on sm_100a.
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 #include "launch.h"
 #include "lco_internal.h"
 
 namespace lco {
 
-static inline uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) {
+  return a < b ? a : b;
+}
 
-constexpr int kThreads = 256;  // k_pass CTA size (8 warps)
+constexpr int kThreads = 256;  // k_scatter / k_count CTA size (8 warps)
 constexpr int kItems = 16;     // nonzeros per thread per tile
 constexpr int kTile = kThreads * kItems;
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagInc = 1u << 31;
-constexpr uint32_t kValueMask = (1u << 30) - 1;
+constexpr int kChunkTiles = 64;  // tiles per scan chunk
+constexpr int kScanThreads = 256;
 constexpr uint32_t kInvalid = 0xFFFFu;
 
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
 
+// Lanes of the warp holding the same BITS-bit digit (0 for invalid lanes): one ballot
+// per digit bit (ALU pipe), instead of MATCH.ANY (MIO pipe).
+template <int BITS>
+__device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
+  uint32_t m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t v = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? v : ~v;
+  }
+  return valid ? m : 0u;
+}
+
 // ---------------------------------------------------------------------------------
-// Block-wide exclusive scan of `bins` counters (in place into `out`), NT threads.
+// Block-wide exclusive scan of BINS counters from `in` into `out`, NT threads.
 // ---------------------------------------------------------------------------------
 template <int NT, int BINS>
 __device__ __forceinline__ void block_scan_bins(const uint32_t* in, uint32_t* out,
@@ -96,6 +113,38 @@ __device__ __forceinline__ void block_scan_bins(const uint32_t* in, uint32_t* ou
   __syncthreads();
 }
 
+// Destination rank of a new key: number of splitters <= k2 (splitters ascending).
+__device__ __forceinline__ uint32_t rank_of(const uint64_t* __restrict__ spl, int world,
+                                            uint64_t k2) {
+  int lo = 0, hi = world - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(spl + mid) <= k2) lo = mid + 1;
+    else hi = mid;
+  }
+  return (uint32_t)lo;
+}
+
+// ---------------------------------------------------------------------------------
+// Per-pass parameters shared by the pass kernels.
+// ---------------------------------------------------------------------------------
+struct PassParams {
+  KeyPlan kp;
+  int pass;
+  int qshift;               // >= 0: q = K' >> qshift (T a power of two); -1: fast division
+  uint64_t nnz;
+  uint32_t tiles;
+  uint32_t nchunks;
+  const uint64_t* splitters;  // partition mode: digit = destination rank
+  int world;
+};
+
+__device__ __forceinline__ uint32_t digit_new(const PassParams& a, uint64_t k2) {
+  if (a.splitters) return rank_of(a.splitters, a.world, k2);
+  const uint64_t q = a.qshift >= 0 ? (k2 >> a.qshift) : fdiv(a.kp.divT, k2);
+  return digit_of(a.kp, q, a.pass);
+}
+
 // ---------------------------------------------------------------------------------
 // k_copy
 // ---------------------------------------------------------------------------------
@@ -112,287 +161,284 @@ __global__ void k_copy(uint64_t nnz, const uint64_t* __restrict__ keys_in,
 }
 
 // ---------------------------------------------------------------------------------
-// k_hist: digit histograms of q = K' div T for every pass.
+// k_count: one tile per CTA: tile histogram -> thist[t][BINS] (uint16) and added into
+// its chunk's sums csum[t / kChunkTiles][BINS] (zeroed by the launcher).
 // ---------------------------------------------------------------------------------
-struct HistArgs {
-  KeyPlan kp;
-  const uint64_t* keys;
-  uint64_t nnz;
-  uint32_t* ghist;     // [passes][bins], zeroed by the caller
-  uint32_t* bucket;    // [passes][bins] exclusive scan (written by the last CTA)
-  uint32_t* done;      // CTA completion counter, zeroed by the caller
-  uint32_t* zero;      // region zeroed here (status of the first pass)
-  uint64_t zero_words; // in uint32
-  const uint64_t* splitters;  // partition mode: digit = destination rank (else null)
-  int world;
-  uint64_t* counts64;  // partition mode: per-rank counts (uint64), or null
-};
-
-// Destination rank of a new key: number of splitters <= k2 (splitters ascending).
-__device__ __forceinline__ uint32_t rank_of(const uint64_t* __restrict__ spl, int world,
-                                            uint64_t k2) {
-  int lo = 0, hi = world - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(spl + mid) <= k2) lo = mid + 1;
-    else hi = mid;
+template <int RB, bool FIRST>
+__global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ PassParams a,
+                                                    const uint64_t* __restrict__ keys,
+                                                    uint16_t* __restrict__ thist,
+                                                    uint32_t* __restrict__ csum) {
+  constexpr int BINS = 1 << RB;
+  __shared__ uint32_t h[BINS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t t = blockIdx.x;
+  for (int i = tid; i < BINS; i += kThreads) h[i] = 0;
+  const uint64_t base = (uint64_t)t * kTile;
+  const uint32_t n = (uint32_t)umin64(kTile, a.nnz - base);
+  uint64_t k[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+    k[it] = pos < n ? __ldcs(keys + base + pos) : 0ull;
   }
-  return (uint32_t)lo;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+    const bool ok = pos < n;
+    // plain shared atomics: a histogram needs no order (conflicting lanes of a warp are
+    // serialized by the hardware, which only costs on long runs of equal digits)
+    if (ok) atomicAdd(&h[digit_new(a, FIRST ? reencode(a.kp, k[it]) : k[it])], 1u);
+  }
+  __syncthreads();
+  uint16_t* row = thist + (size_t)t * BINS;
+  uint32_t* cs = csum + (size_t)(t / kChunkTiles) * BINS;
+  for (int d = tid; d < BINS; d += kThreads) {
+    const uint32_t v = h[d];
+    row[d] = (uint16_t)v;
+    if (v) atomicAdd(cs + d, v);
+  }
 }
 
-constexpr int kHistThreads = 512;
-
+// ---------------------------------------------------------------------------------
+// k_scan: csum[c][d] <- sum_{c' < c} csum[c'][d] (in place); totals; the last CTA
+// turns the totals into bucket starts (and an optional uint64 copy of the totals).
+// ---------------------------------------------------------------------------------
 template <int RB>
-__global__ void __launch_bounds__(kHistThreads) k_hist(const __grid_constant__ HistArgs a) {
+__global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ csum,
+                                                       uint32_t nchunks,
+                                                       uint32_t* __restrict__ totals,
+                                                       uint32_t* __restrict__ bucket,
+                                                       uint32_t* __restrict__ done,
+                                                       uint64_t* __restrict__ counts64,
+                                                       int ncounts) {
   constexpr int BINS = 1 << RB;
-  extern __shared__ __align__(16) uint32_t sh[];  // [passes][BINS]
+  constexpr int LANES = BINS >= 64 ? 64 : BINS;  // bins per CTA
+  constexpr int SPLIT = kScanThreads / LANES;    // chunk groups per bin
+  __shared__ uint32_t part[kScanThreads];
   __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t sh[BINS];
   __shared__ bool s_last;
-  const int P = a.kp.passes;
   const int tid = threadIdx.x;
-  for (int i = tid; i < P * BINS; i += kHistThreads) sh[i] = 0;
-  {  // zero the first pass's look-back status (overlaps with the histogram)
-    const uint64_t stride = (uint64_t)gridDim.x * kHistThreads;
-    for (uint64_t i = (uint64_t)blockIdx.x * kHistThreads + tid; i < a.zero_words; i += stride)
-      a.zero[i] = 0;
-  }
+  const int d = blockIdx.x * LANES + tid % LANES;
+  const int g = tid / LANES;
+  const uint32_t per = (nchunks + SPLIT - 1) / SPLIT;
+  const uint32_t c0 = min(nchunks, g * per), c1 = min(nchunks, c0 + per);
+  uint32_t sum = 0;
+#pragma unroll 8
+  for (uint32_t c = c0; c < c1; ++c) sum += __ldcg(csum + (size_t)c * BINS + d);
+  part[tid] = sum;
   __syncthreads();
-  const uint64_t stride = (uint64_t)gridDim.x * kHistThreads;
-  constexpr int U = 4;
-  for (uint64_t i0 = (uint64_t)blockIdx.x * kHistThreads * U + tid; i0 < a.nnz;
-       i0 += stride * U) {
-    uint64_t k[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      uint64_t i = i0 + (uint64_t)u * kHistThreads;
-      k[u] = i < a.nnz ? __ldcs(a.keys + i) : 0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      uint64_t i = i0 + (uint64_t)u * kHistThreads;
-      if (i < a.nnz) {
-        const uint64_t k2 = reencode(a.kp, k[u]);
-        if (a.splitters) {
-          atomicAdd(&sh[rank_of(a.splitters, a.world, k2)], 1u);
-        } else {
-          const uint64_t q = fdiv(a.kp.divT, k2);
-          for (int j = 0; j < P; ++j) atomicAdd(&sh[j * BINS + digit_of(a.kp, q, j)], 1u);
-        }
-      }
-    }
+  uint32_t run = 0;
+  for (int g2 = 0; g2 < g; ++g2) run += part[g2 * LANES + tid % LANES];
+  for (uint32_t c = c0; c < c1; ++c) {
+    const size_t o = (size_t)c * BINS + d;
+    const uint32_t v = __ldcg(csum + o);
+    csum[o] = run;
+    run += v;
   }
-  __syncthreads();
-  for (int i = tid; i < P * BINS; i += kHistThreads) {
-    uint32_t v = sh[i];
-    if (v) atomicAdd(&a.ghist[i], v);
-  }
+  if (g == SPLIT - 1) totals[d] = run;
   __threadfence();
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  for (int j = 0; j < P; ++j) {
-    for (int i = tid; i < BINS; i += kHistThreads) {
-      sh[i] = __ldcg(a.ghist + j * BINS + i);
-      if (a.counts64 && i < a.world) a.counts64[i] = sh[i];
+  for (int i = tid; i < BINS; i += kScanThreads) {
+    sh[i] = __ldcg(totals + i);
+    if (counts64 && i < ncounts) counts64[i] = sh[i];
+  }
+  __syncthreads();
+  block_scan_bins<kScanThreads, BINS>(sh, bucket, s_warp);
+}
+
+// ---------------------------------------------------------------------------------
+// k_offsets: toff[t][d] = bucket[d] + csum[c][d] + sum of thist rows before t in c.
+// ---------------------------------------------------------------------------------
+template <int RB>
+__global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ PassParams a,
+                                                      const uint16_t* __restrict__ thist,
+                                                      const uint32_t* __restrict__ csum,
+                                                      const uint32_t* __restrict__ bucket,
+                                                      uint32_t* __restrict__ toff) {
+  constexpr int BINS = 1 << RB;
+  const uint32_t c = blockIdx.x;
+  const uint32_t t0 = c * kChunkTiles, t1 = min(a.tiles, t0 + kChunkTiles);
+  for (int d = threadIdx.x; d < BINS; d += kThreads) {
+    uint32_t run = __ldg(bucket + d) + __ldcg(csum + (size_t)c * BINS + d);
+    for (uint32_t t = t0; t < t1; ++t) {
+      toff[(size_t)t * BINS + d] = run;
+      run += __ldcg(thist + (size_t)t * BINS + d);
     }
-    __syncthreads();
-    block_scan_bins<kHistThreads, BINS>(sh, a.bucket + j * BINS, s_warp);
   }
 }
 
 // ---------------------------------------------------------------------------------
-// k_pass: one stable LSD pass (onesweep-style decoupled look-back).
-// VMODE: 0 no values, 1 carry values through shared memory (single pass),
-//        2 gather vals_in[position] in the last pass (multi-pass).
+// k_scatter: one tile per CTA.
 // ---------------------------------------------------------------------------------
-struct PassArgs {
-  KeyPlan kp;
-  int pass;
-  uint64_t nnz;
-  // FIRST-pass inputs
-  const uint64_t* keys_in;
+struct ScatterIO {
+  const uint64_t* keys_in;  // FIRST pass inputs
   const double* vals_in;
   const uint32_t* idx_in;
-  // later-pass inputs (carried new keys and source positions)
-  const uint64_t* kin;
+  const uint64_t* kin;      // later-pass inputs (carried K', V, source position)
+  const double* vin;
   const uint32_t* pin;
-  // outputs: intermediate (kout, pout) or final (keys_out, perm_out, vals_out)
-  uint64_t* kout;
+  uint64_t* kout;           // outputs (final arrays on the last pass)
+  double* vout;
   uint32_t* pout;
-  double* vals_out;
-  const uint32_t* bucket;  // [bins] exclusive digit starts of this pass
-  uint32_t* status;        // [tiles][bins] look-back words of this pass (zeroed)
-  uint32_t* status_next;   // [tiles][bins] to zero for the next pass, or null
-  uint32_t* tile_counter;  // dynamic tile id (zeroed)
-  const uint64_t* splitters;  // partition mode (single pass): digit = destination rank
-  int world;
-  int keep_old_key;        // partition mode: scatter the old key, not K'
-  uint32_t idx_base;       // added to the source position in single-pass payloads
+  const uint32_t* toff;     // [tiles][BINS] from k_offsets
+  int keep_old_key;         // partition: scatter the old key
+  uint32_t idx_base;        // partition: added to single-pass source positions
 };
 
 template <int RB>
-constexpr size_t pass_smem_bytes() {
+constexpr size_t scatter_smem_bytes() {
   return (size_t)kTile * 8 + (size_t)(kThreads / 32) * (1 << RB) * 2 + (size_t)(1 << RB) * 8 +
          (size_t)kTile * 2;
 }
 
-template <int RB, bool FIRST, bool LAST, int VMODE>
-__global__ void __launch_bounds__(kThreads) k_pass(const __grid_constant__ PassArgs a) {
+template <int RB, bool FIRST, bool LAST, bool VALS>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_scatter(const __grid_constant__ PassParams a, const __grid_constant__ ScatterIO io) {
   constexpr int BINS = 1 << RB;
   constexpr int W = kThreads / 32;
+  constexpr int NB = BINS >= kThreads ? BINS / kThreads : 1;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* stage = reinterpret_cast<uint64_t*>(smem);              // [kTile]
   uint16_t* whist = reinterpret_cast<uint16_t*>(stage + kTile);     // [W][BINS]
-  uint32_t* tcount = reinterpret_cast<uint32_t*>(whist + W * BINS); // [BINS] -> global base
-  uint32_t* toff = tcount + BINS;                                   // [BINS]
-  uint16_t* sdig = reinterpret_cast<uint16_t*>(toff + BINS);        // [kTile]
-  __shared__ uint32_t s_tile;
+  uint32_t* gbase = reinterpret_cast<uint32_t*>(whist + W * BINS);  // [BINS]
+  uint32_t* loff = gbase + BINS;                                    // [BINS]
+  uint16_t* sdig = reinterpret_cast<uint16_t*>(loff + BINS);        // [kTile]
   __shared__ uint32_t s_warp[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(a.tile_counter, 1u);
+  const uint32_t t = blockIdx.x;
+  const uint64_t base = (uint64_t)t * kTile;
+  const uint32_t n = (uint32_t)umin64(kTile, a.nnz - base);
   for (int i = tid; i < W * BINS / 2; i += kThreads) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t base = (uint64_t)tile * kTile;
-  const uint32_t n = (uint32_t)min((uint64_t)kTile, a.nnz - base);
-  if (a.status_next)
-    for (int i = tid; i < BINS; i += kThreads) a.status_next[(size_t)tile * BINS + i] = 0u;
-
-  // ---- load the tile (warp w owns a contiguous slice; lane-consecutive elements) ----
+  // ---- load keys; warp w owns a contiguous slice, lanes consecutive ----
   uint64_t key[kItems];
-  uint32_t pay[kItems];  // payload: source position, or idx_in value (single pass)
-  double val[VMODE == 1 ? kItems : 1];
   uint32_t meta[kItems];
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
-    const uint64_t i = base + pos;
-    key[it] = 0;
-    pay[it] = 0;
-    if (pos < n) {
-      if (FIRST) {
-        key[it] = __ldcs(a.keys_in + i);
-        if constexpr (VMODE == 1) val[it] = __ldcs(a.vals_in + i);
-        if (LAST && a.idx_in) pay[it] = __ldcs(a.idx_in + i);
-        else pay[it] = (uint32_t)i + (LAST ? a.idx_base : 0u);
-      } else {
-        key[it] = __ldcs(a.kin + i);
-        pay[it] = __ldcs(a.pin + i);
-      }
-    }
+    key[it] = pos < n ? __ldcs((FIRST ? io.keys_in : io.kin) + base + pos) : 0ull;
+  }
+  // global offsets of this tile's digit runs (from the exclusive scan)
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int d = tid + b * kThreads;
+    if (d < BINS) gbase[d] = __ldcs(io.toff + (size_t)t * BINS + d);
   }
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
     if (pos < n) {
+      uint64_t k2 = key[it];
       if (FIRST) {
-        const uint64_t k2 = reencode(a.kp, key[it]);  // LIV shuffle
-        if (a.splitters) {
-          meta[it] = rank_of(a.splitters, a.world, k2);
-          if (!a.keep_old_key) key[it] = k2;
-        } else {
-          key[it] = k2;
-          meta[it] = digit_of(a.kp, fdiv(a.kp.divT, k2), a.pass);
-        }
-      } else {
-        meta[it] = digit_of(a.kp, fdiv(a.kp.divT, key[it]), a.pass);
+        k2 = reencode(a.kp, k2);  // LIV shuffle
+        if (!io.keep_old_key) key[it] = k2;
       }
+      meta[it] = digit_new(a, k2);
     } else {
       meta[it] = kInvalid;
     }
   }
-  // ---- warp-level stable ranking (match_any) into per-warp digit counters ----
+  __syncthreads();
+  // ---- warp-level stable ranking into per-warp digit counters ----
   uint16_t* wh = whist + warp * BINS;
   const uint32_t ltm = lanemask_lt();
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const uint32_t d = meta[it];
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    const int leader = __ffs(peers) - 1;
+    const bool ok = d != kInvalid;
+    const uint32_t peers = peers_of<RB>(d, ok);
     uint32_t before = 0;
-    if (lane == leader && d != kInvalid) {
+    const bool leader = ok && (peers & ltm) == 0;
+    if (leader) {
       before = wh[d];
       wh[d] = (uint16_t)(before + __popc(peers));
     }
-    before = __shfl_sync(0xffffffffu, before, leader);
+    const int src = ok ? __ffs(peers) - 1 : lane;
+    before = __shfl_sync(0xffffffffu, before, src);
     meta[it] = d | ((before + __popc(peers & ltm)) << 16);
     __syncwarp();
   }
   __syncthreads();
-  // ---- per-digit: exclusive prefix across warps, tile count ----
-  for (int d = tid; d < BINS; d += kThreads) {
-    uint32_t s = 0;
+  // ---- per digit: exclusive prefix across warps, tile count ----
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-      const uint32_t c = whist[w * BINS + d];
-      whist[w * BINS + d] = (uint16_t)s;
-      s += c;
+  for (int b = 0; b < NB; ++b) {
+    const int d = tid + b * kThreads;
+    if (d < BINS) {
+      uint32_t s = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint32_t cw = whist[w * BINS + d];
+        whist[w * BINS + d] = (uint16_t)s;
+        s += cw;
+      }
+      loff[d] = s;
     }
-    tcount[d] = s;
-    st_relaxed(a.status + (size_t)tile * BINS + d, (tile ? kFlagAgg : kFlagInc) | s);
   }
   __syncthreads();
-  block_scan_bins<kThreads, BINS>(tcount, toff, s_warp);
+  block_scan_bins<kThreads, BINS>(loff, loff, s_warp);
   // ---- local (tile-sorted) positions; stage keys ----
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     const uint32_t d = meta[it] & 0xFFFFu;
     if (d != kInvalid) {
-      const uint32_t lp = toff[d] + whist[warp * BINS + d] + (meta[it] >> 16);
+      const uint32_t lp = loff[d] + whist[warp * BINS + d] + (meta[it] >> 16);
       stage[lp] = key[it];
       sdig[lp] = (uint16_t)d;
       meta[it] = d | (lp << 16);
     }
   }
-  // ---- decoupled look-back per digit ----
-  for (int d = tid; d < BINS; d += kThreads) {
-    const uint32_t cnt = tcount[d];
-    uint32_t excl = 0;
-    if (tile > 0) {
-      int64_t j = (int64_t)tile - 1;
-      while (true) {
-        const uint32_t s = ld_relaxed(a.status + (size_t)j * BINS + d);
-        if ((s & (kFlagAgg | kFlagInc)) == 0) continue;
-        excl += s & kValueMask;
-        if (s & kFlagInc) break;
-        --j;
-      }
-      st_relaxed(a.status + (size_t)tile * BINS + d, kFlagInc | (excl + cnt));
-    }
-    tcount[d] = a.bucket[d] + excl - toff[d];  // global position of local position 0 of d
-  }
-  __syncthreads();
-  // ---- scatter keys (runs of equal digit are contiguous in stage) ----
-  for (uint32_t p = tid; p < n; p += kThreads) a.kout[tcount[sdig[p]] + p] = stage[p];
-  __syncthreads();
-  uint32_t* stage32 = reinterpret_cast<uint32_t*>(stage);
+  // ---- values: load now, they fly while the keys are written ----
+  double val[VALS ? kItems : 1];
+  if constexpr (VALS) {
 #pragma unroll
-  for (int it = 0; it < kItems; ++it)
-    if ((meta[it] & 0xFFFFu) != kInvalid) stage32[meta[it] >> 16] = pay[it];
-  __syncthreads();
-  for (uint32_t p = tid; p < n; p += kThreads) {
-    const uint32_t dst = tcount[sdig[p]] + p;
-    const uint32_t v = stage32[p];
-    if (!LAST) {
-      a.pout[dst] = v;
-    } else if (FIRST) {
-      if (a.pout) a.pout[dst] = v;
-    } else {
-      if (a.pout) a.pout[dst] = a.idx_in ? __ldg(a.idx_in + v) : v;
-      if constexpr (VMODE == 2) a.vals_out[dst] = __ldg(a.vals_in + v);
+    for (int it = 0; it < kItems; ++it) {
+      const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+      val[it] = pos < n ? __ldcs((FIRST ? io.vals_in : io.vin) + base + pos) : 0.0;
     }
   }
-  if constexpr (VMODE == 1) {
-    __syncthreads();
-    double* stage64 = reinterpret_cast<double*>(stage);
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int d = tid + b * kThreads;
+    if (d < BINS) gbase[d] -= loff[d];  // global position of local slot 0 of digit d
+  }
+  __syncthreads();
+  for (uint32_t p = tid; p < n; p += kThreads) io.kout[gbase[sdig[p]] + p] = stage[p];
+  __syncthreads();
+  if constexpr (VALS) {
+    double* sv = reinterpret_cast<double*>(stage);
 #pragma unroll
     for (int it = 0; it < kItems; ++it)
-      if ((meta[it] & 0xFFFFu) != kInvalid) stage64[meta[it] >> 16] = val[it];
+      if ((meta[it] & 0xFFFFu) != kInvalid) sv[meta[it] >> 16] = val[it];
     __syncthreads();
-    for (uint32_t p = tid; p < n; p += kThreads) a.vals_out[tcount[sdig[p]] + p] = stage64[p];
+    for (uint32_t p = tid; p < n; p += kThreads) io.vout[gbase[sdig[p]] + p] = sv[p];
+    __syncthreads();
+  }
+  if (io.pout) {
+    uint32_t* s32 = reinterpret_cast<uint32_t*>(stage);
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+      if ((meta[it] & 0xFFFFu) != kInvalid) {
+        uint32_t v;
+        if (FIRST) {
+          v = (LAST && io.idx_in) ? __ldg(io.idx_in + base + pos)
+                                  : (uint32_t)(base + pos) + (LAST ? io.idx_base : 0u);
+        } else {
+          v = __ldcs(io.pin + base + pos);
+          if (LAST && io.idx_in) v = __ldg(io.idx_in + v);
+        }
+        s32[meta[it] >> 16] = v;
+      }
+    }
+    __syncthreads();
+    for (uint32_t p = tid; p < n; p += kThreads) io.pout[gbase[sdig[p]] + p] = s32[p];
   }
 }
 
@@ -438,119 +484,130 @@ template <int RB>
 static cudaError_t set_smem_attrs() {
   static bool done = false;
   if (done) return cudaSuccess;
-  const int bytes = (int)pass_smem_bytes<RB>();
+  const int bytes = (int)scatter_smem_bytes<RB>();
   cudaError_t e = cudaSuccess;
-#define LCO_ATTR(F, L, V)                                                                  \
-  e = cudaFuncSetAttribute(k_pass<RB, F, L, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           bytes);                                                         \
+#define LCO_ATTR(F, L, V)                                                       \
+  e = cudaFuncSetAttribute(k_scatter<RB, F, L, V>,                              \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
   if (e != cudaSuccess) return e;
-  LCO_ATTR(true, true, 0)
-  LCO_ATTR(true, true, 1)
-  LCO_ATTR(true, false, 0)
-  LCO_ATTR(false, false, 0)
-  LCO_ATTR(false, true, 0)
-  LCO_ATTR(false, true, 2)
+  LCO_ATTR(true, true, false)
+  LCO_ATTR(true, true, true)
+  LCO_ATTR(true, false, false)
+  LCO_ATTR(true, false, true)
+  LCO_ATTR(false, false, false)
+  LCO_ATTR(false, false, true)
+  LCO_ATTR(false, true, false)
+  LCO_ATTR(false, true, true)
 #undef LCO_ATTR
-  e = cudaFuncSetAttribute(k_hist<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kMaxPasses * (1 << RB) * 4);
-  if (e != cudaSuccess) return e;
   done = true;
   return cudaSuccess;
 }
 
+uint64_t pass_tiles(uint64_t nnz) { return (nnz + kTile - 1) / kTile; }
+int pass_tile() { return kTile; }
+// control block: thist (uint16 [tiles][bins]) | toff ([tiles][bins]) | csum ([chunks][bins])
+//                | totals | bucket | counter
+size_t pass_ctrl_bytes(int rb, uint64_t nnz) {
+  const uint64_t tiles = pass_tiles(nnz);
+  const uint64_t chunks = (tiles + kChunkTiles - 1) / kChunkTiles;
+  const size_t bins = (size_t)1 << rb;
+  return tiles * bins * 2 + 256 + tiles * bins * 4 + (chunks + 2) * bins * 4 + 512;
+}
+
 template <int RB>
-static cudaError_t run_onesweep_rb(const KeyPlan& kp, const OnesweepIO& io, const Launch& L) {
+static cudaError_t run_passes_rb(const KeyPlan& kp, const PassIO& io, const Launch& L) {
   constexpr int BINS = 1 << RB;
   cudaError_t e = set_smem_attrs<RB>();
   if (e != cudaSuccess) return e;
   const bool part = io.splitters != nullptr;
   const int P = part ? 1 : kp.passes;
   const uint64_t nnz = io.nnz;
-  const uint64_t tiles = (nnz + kTile - 1) / kTile;
-  uint32_t* ghist = io.ctrl;
-  uint32_t* bucket = io.ctrl + kMaxPasses * BINS;
-  uint32_t* counters = bucket + kMaxPasses * BINS;  // [kMaxPasses] tile counters, [done]
-  uint32_t* done = counters + kMaxPasses;
-  const size_t ctrl_bytes = (size_t)(2 * kMaxPasses * BINS + kMaxPasses + 1) * 4;
-  if (L.mark) L.mark(L.ctx, "memset_ctrl");
-  e = cudaMemsetAsync(io.ctrl, 0, ctrl_bytes, L.stream);
-  if (e != cudaSuccess) return e;
-  KeyPlan kpp = kp;
-  if (part) kpp.passes = 1;
-  {
-    HistArgs h;
-    h.kp = kpp;
-    h.keys = io.keys_in;
-    h.nnz = nnz;
-    h.ghist = ghist;
-    h.bucket = bucket;
-    h.done = done;
-    h.zero = io.statusA;
-    h.zero_words = tiles * BINS;
-    h.splitters = io.splitters;
-    h.world = io.world;
-    h.counts64 = io.counts64;
-    int grid = (int)umin64((nnz + kHistThreads * 4 - 1) / (kHistThreads * 4), 148 * 2);
-    if (grid < 1) grid = 1;
-    if (L.mark) L.mark(L.ctx, "k_hist");
-    k_hist<RB><<<grid, kHistThreads, P * BINS * 4, L.stream>>>(h);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  const size_t smem = pass_smem_bytes<RB>();
+  const uint32_t tiles = (uint32_t)pass_tiles(nnz);
+  const uint32_t nchunks = (tiles + kChunkTiles - 1) / kChunkTiles;
+  char* cb = reinterpret_cast<char*>(io.ctrl);
+  uint16_t* thist = reinterpret_cast<uint16_t*>(cb);
+  cb += ((size_t)tiles * BINS * 2 + 255) / 256 * 256;
+  uint32_t* toff = reinterpret_cast<uint32_t*>(cb);
+  cb += (size_t)tiles * BINS * 4;
+  uint32_t* csum = reinterpret_cast<uint32_t*>(cb);
+  uint32_t* totals = csum + (size_t)nchunks * BINS;
+  uint32_t* bucket = totals + BINS;
+  uint32_t* done = bucket + BINS;
+
+  PassParams a;
+  memset(&a, 0, sizeof a);
+  a.kp = kp;
+  if (part) a.kp.passes = 1;
+  a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
+  a.nnz = nnz;
+  a.tiles = tiles;
+  a.nchunks = nchunks;
+  a.splitters = io.splitters;
+  a.world = io.world;
+  const bool vals = io.vals_out != nullptr;
+  const size_t smem = scatter_smem_bytes<RB>();
   for (int j = 0; j < P; ++j) {
-    PassArgs p;
-    p.kp = kpp;
-    p.pass = j;
-    p.nnz = nnz;
-    p.keys_in = io.keys_in;
-    p.vals_in = io.vals_in;
-    p.idx_in = io.idx_in;
-    p.kin = (j % 2 == 1) ? io.kA : io.kB;
-    p.pin = (j % 2 == 1) ? io.pA : io.pB;
-    const bool last = j == P - 1;
-    p.kout = last ? io.keys_out : ((j % 2 == 0) ? io.kA : io.kB);
-    p.pout = last ? io.perm_out : ((j % 2 == 0) ? io.pA : io.pB);
-    p.vals_out = io.vals_out;
-    p.bucket = bucket + j * BINS;
-    p.status = (j % 2 == 0) ? io.statusA : io.statusB;
-    p.status_next = last ? nullptr : ((j % 2 == 0) ? io.statusB : io.statusA);
-    p.tile_counter = counters + j;
-    p.splitters = io.splitters;
-    p.world = io.world;
-    p.keep_old_key = part ? 1 : 0;
-    p.idx_base = io.idx_base;
+    a.pass = j;
+    const bool first = j == 0, last = j == P - 1;
+    const uint64_t* in_keys = first ? io.keys_in : ((j % 2 == 1) ? io.kA : io.kB);
+    if ((e = cudaMemsetAsync(csum, 0, ((size_t)nchunks * BINS + 2 * BINS) * 4 + 4, L.stream)) !=
+        cudaSuccess)
+      return e;  // chunk sums, totals, bucket starts and k_scan's completion counter
+    if (L.mark) L.mark(L.ctx, first ? "k_count_first" : "k_count");
+    if (first) k_count<RB, true><<<tiles, kThreads, 0, L.stream>>>(a, in_keys, thist, csum);
+    else k_count<RB, false><<<tiles, kThreads, 0, L.stream>>>(a, in_keys, thist, csum);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (L.mark) L.mark(L.ctx, "k_scan");
+    const int scan_grid = BINS >= 64 ? BINS / 64 : 1;
+    k_scan<RB><<<scan_grid, kScanThreads, 0, L.stream>>>(csum, nchunks, totals, bucket, done,
+                                                        part ? io.counts64 : nullptr, io.world);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (L.mark) L.mark(L.ctx, "k_offsets");
+    k_offsets<RB><<<nchunks, kThreads, 0, L.stream>>>(a, thist, csum, bucket, toff);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ScatterIO s;
+    memset(&s, 0, sizeof s);
+    s.keys_in = io.keys_in;
+    s.vals_in = io.vals_in;
+    s.idx_in = io.idx_in;
+    // pass j reads buffer set (j-1)%2 and writes set j%2 (A = 0, B = 1)
+    s.kin = (j % 2 == 1) ? io.kA : io.kB;
+    s.vin = (j % 2 == 1) ? io.vA : io.vB;
+    s.pin = (j % 2 == 1) ? io.pA : io.pB;
+    s.kout = last ? io.keys_out : ((j % 2 == 0) ? io.kA : io.kB);
+    s.vout = last ? io.vals_out : ((j % 2 == 0) ? io.vA : io.vB);
+    s.pout = last ? io.perm_out : ((j % 2 == 0) ? io.pA : io.pB);
+    s.toff = toff;
+    s.keep_old_key = part ? 1 : 0;
+    s.idx_base = io.idx_base;
     if (L.mark)
-      L.mark(L.ctx, part ? "k_partition" : (P == 1 ? "k_pass_single" : (j == 0 ? "k_pass_first" : (last ? "k_pass_last" : "k_pass_mid"))));
-    const dim3 grid((unsigned)tiles);
+      L.mark(L.ctx, part ? "k_partition"
+                         : (P == 1 ? "k_scatter_single"
+                                   : (first ? "k_scatter_first"
+                                            : (last ? "k_scatter_last" : "k_scatter_mid"))));
+#define LCO_LAUNCH(F, LST)                                                          \
+  if (vals) k_scatter<RB, F, LST, true><<<tiles, kThreads, smem, L.stream>>>(a, s); \
+  else k_scatter<RB, F, LST, false><<<tiles, kThreads, smem, L.stream>>>(a, s);
     if (P == 1) {
-      if (io.vals_out) k_pass<RB, true, true, 1><<<grid, kThreads, smem, L.stream>>>(p);
-      else k_pass<RB, true, true, 0><<<grid, kThreads, smem, L.stream>>>(p);
-    } else if (j == 0) {
-      k_pass<RB, true, false, 0><<<grid, kThreads, smem, L.stream>>>(p);
+      LCO_LAUNCH(true, true)
+    } else if (first) {
+      LCO_LAUNCH(true, false)
     } else if (!last) {
-      k_pass<RB, false, false, 0><<<grid, kThreads, smem, L.stream>>>(p);
+      LCO_LAUNCH(false, false)
     } else {
-      if (io.vals_out) k_pass<RB, false, true, 2><<<grid, kThreads, smem, L.stream>>>(p);
-      else k_pass<RB, false, true, 0><<<grid, kThreads, smem, L.stream>>>(p);
+      LCO_LAUNCH(false, true)
     }
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+#undef LCO_LAUNCH
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
-size_t onesweep_ctrl_bytes(int rb) {
-  return (size_t)(2 * kMaxPasses * (1 << rb) + kMaxPasses + 1) * 4;
-}
-uint64_t onesweep_tiles(uint64_t nnz) { return (nnz + kTile - 1) / kTile; }
-int onesweep_tile() { return kTile; }
-
-cudaError_t run_onesweep(int rb, const KeyPlan& kp, const OnesweepIO& io, const Launch& L) {
+cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L) {
   switch (rb) {
-    case 8: return run_onesweep_rb<8>(kp, io, L);
-    case 10: return run_onesweep_rb<10>(kp, io, L);
-    case 11: return run_onesweep_rb<11>(kp, io, L);
+    case 8: return run_passes_rb<8>(kp, io, L);
+    case 10: return run_passes_rb<10>(kp, io, L);
+    case 11: return run_passes_rb<11>(kp, io, L);
   }
   return cudaErrorInvalidValue;
 }

@@ -13,8 +13,10 @@ struct Launch {
   void* ctx;
 };
 
-// All buffers of one onesweep run.  Partition mode: splitters != null, single pass.
-struct OnesweepIO {
+constexpr uint32_t kMaxChunks = 1024;  // persistent CTAs (chunks) per pass, upper bound
+
+// All buffers of one multi-pass run.  Partition mode: splitters != null, single pass.
+struct PassIO {
   uint64_t nnz;
   const uint64_t* keys_in;
   const double* vals_in;
@@ -22,12 +24,12 @@ struct OnesweepIO {
   uint64_t* keys_out;
   double* vals_out;
   uint32_t* perm_out;
-  uint32_t* ctrl;
-  uint32_t* statusA;
-  uint32_t* statusB;
-  uint64_t* kA;
+  uint32_t* ctrl;  // pass_ctrl_bytes(): chunk histograms, totals, bucket starts, counter
+  uint64_t* kA;    // ping-pong buffers (K', V, source position)
+  double* vA;
   uint32_t* pA;
   uint64_t* kB;
+  double* vB;
   uint32_t* pB;
   const uint64_t* splitters;
   int world;
@@ -35,10 +37,10 @@ struct OnesweepIO {
   uint64_t* counts64;
 };
 
-size_t onesweep_ctrl_bytes(int rb);
-uint64_t onesweep_tiles(uint64_t nnz);
-int onesweep_tile();
-cudaError_t run_onesweep(int rb, const KeyPlan& kp, const OnesweepIO& io, const Launch& L);
+uint64_t pass_tiles(uint64_t nnz);
+int pass_tile();
+size_t pass_ctrl_bytes(int rb, uint64_t nnz);
+cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
 cudaError_t run_copy(uint64_t nnz, const uint64_t* keys_in, const double* vals_in,
                      const uint32_t* idx_in, uint64_t* keys_out, double* vals_out,
                      uint32_t* perm_out, const Launch& L);

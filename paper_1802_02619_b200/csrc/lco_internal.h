@@ -60,6 +60,10 @@ struct KeyPlan {
   uint64_t dim[kMaxModes];        // n_m
   uint64_t nstride[kMaxModes];    // new-key stride of old mode m
   FastDiv divT;                   // q = K' div T
+  int pow2;                       // 1: every normalized dim is a power of two
+  uint8_t oshift[kMaxModes];      // pow2: bit offset of mode m in the old key
+  uint8_t nshift[kMaxModes];      // pow2: bit offset of mode m in the new key
+  uint8_t width[kMaxModes];       // pow2: log2 n_m
   int passes;                     // P
   int dshift[kMaxPasses];         // digit j = (q >> dshift[j]) & ((1 << dbits[j]) - 1)
   int dbits[kMaxPasses];
@@ -68,6 +72,13 @@ struct KeyPlan {
 // LIV shuffle of one key: decode old coordinates from the last mode
 // with fast division, accumulate the new key with the new strides.
 LCO_HD uint64_t reencode(const KeyPlan& p, uint64_t k) {
+  if (p.pow2) {  // every mode is a bit field: the shuffle is a bit permutation
+    uint64_t out = 0;
+#pragma unroll 1
+    for (int m = 0; m < p.n; ++m)
+      out |= ((k >> p.oshift[m]) & ((1ull << p.width[m]) - 1ull)) << p.nshift[m];
+    return out;
+  }
   uint64_t out = 0;
 #pragma unroll 1
   for (int m = p.n - 1; m > 0; --m) {
@@ -119,11 +130,11 @@ struct lco_plan_s {
   int prof_stages;
   void** prof_events;      // cudaEvent_t[prof_calls_max * (kProfStages + 1)]
   int prof_nstages[64];
-  char prof_names[512];
+  char prof_names[1024];
 };
 
 namespace lco {
-constexpr int kProfStages = 16;
+constexpr int kProfStages = 48;
 // Host planning (plan.cpp)
 lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int32_t* perm);
 void choose_passes(OpPlan* op, int sort_bits);

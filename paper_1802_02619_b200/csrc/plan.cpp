@@ -97,6 +97,18 @@ static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64
   }
   if (n == 0) kp.nstride[0] = 1;
   kp.divT = make_fastdiv(T);
+  kp.pow2 = n >= 1;
+  for (int m = 0; m < n; ++m)
+    if (nd[m] & (nd[m] - 1)) kp.pow2 = 0;
+  if (kp.pow2) {
+    int acc_old = 0;
+    for (int m = n - 1; m >= 0; --m) {
+      kp.width[m] = (uint8_t)__builtin_ctzll(nd[m]);
+      kp.oshift[m] = (uint8_t)acc_old;
+      acc_old += kp.width[m];
+    }
+    for (int m = 0; m < n; ++m) kp.nshift[m] = (uint8_t)__builtin_ctzll(kp.nstride[m]);
+  }
   return kp;
 }
 

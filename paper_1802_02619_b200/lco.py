@@ -307,12 +307,12 @@ class Plan:
     def profile_enable(self, calls: int):
         _check(lib().lco_profile_enable(self._h, int(calls)))
 
-    def profile_read(self, max_calls=64, max_stages=17):
+    def profile_read(self, max_calls=64, max_stages=49):
         ms = (ctypes.c_float * (max_calls * max_stages))()
         nc, ns = ctypes.c_int(), ctypes.c_int()
-        names = ctypes.create_string_buffer(1024)
+        names = ctypes.create_string_buffer(4096)
         _check(lib().lco_profile_read(self._h, max_calls, max_stages, ctypes.cast(ms, _P),
-                                      ctypes.byref(nc), ctypes.byref(ns), names, 1024))
+                                      ctypes.byref(nc), ctypes.byref(ns), names, 4096))
         stage_names = names.value.decode().split(";") if names.value else []
         rows = [[ms[c * max_stages + s] for s in range(ns.value)] for c in range(nc.value)]
         return stage_names, rows

@@ -204,11 +204,12 @@ def test_c4_full_certificate(cuda_device):
         ko, vo, po = lco.permute(w.keys, w.vals, w.dims, perm)
         torch.cuda.synchronize()
         certificate_gpu(w, perm, ko, vo, po)
-        # closed form: 13 nonzeros per grid point, output ordered by (y, x, x', y')
+        # closed form: output ordered by (y, x, x', y'); an interior row y holds 13
+        # nonzeros per interior x, 9 at x in {0, n-1} and 12 at x in {1, n-2}
         n = w.dims[0]
         y = ko // (n ** 3)
         assert torch.equal(torch.bincount(y, minlength=n).cpu()[2:-2],
-                           torch.full((n - 4,), 13 * n - 20, dtype=torch.int64))
+                           torch.full((n - 4,), 13 * n - 10, dtype=torch.int64))
 
 
 def test_c5_full_certificate(cuda_device):

@@ -137,8 +137,8 @@ def test_argument_errors():
 def test_workspace_sizes():
     p = lco.Plan((4096,) * 5, (4, 3, 2, 1, 0))
     ws = p.workspace_size(500_000_000)
-    # two ping-pong (key, position) buffers + two look-back status arrays
-    assert 2 * 12 * 500_000_000 < ws < 2 * 12 * 500_000_000 + 2 * 10 ** 9
+    # two ping-pong (key, value, position) buffers + two look-back status arrays
+    assert 2 * 20 * 500_000_000 < ws < 2 * 20 * 500_000_000 + 2 * 10 ** 9
     assert lco.Plan((4, 4), (0, 1)).workspace_size(100) < 1 << 20
     assert p.host_workspace_size(10) > p.workspace_size(10)
 
