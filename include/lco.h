@@ -172,9 +172,13 @@ typedef struct lco_plan_info {
   int passes;                          /* radix passes over HBM (0 = copy) */
   int digit_bits[8];                   /* bits per pass, least significant first */
   int radix_bits;                      /* bins per pass = 2^radix_bits */
-  int path;                            /* 0 copy, 1 onesweep passes, 2 on-chip local */
+  int path;                            /* 0 copy, 1 LSD passes, 2 one on-chip leaf,
+                                          3 MSD passes + on-chip leaf sorts */
   int launches;                        /* kernels this library launches per call */
   int tile;                            /* nonzeros per tile (CTA) */
+  int msd_levels;                      /* path 3: MSD passes before the leaves */
+  int leaf_bits;                       /* paths 2/3: bits of q the leaf sorts handle */
+  double model_bytes;                  /* modelled HBM bytes per nonzero of the plan */
 } lco_plan_info;
 LCO_API lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* info);
 

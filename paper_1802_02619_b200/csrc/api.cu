@@ -25,16 +25,103 @@ struct WsLayout {
   size_t ctrl, kA, vA, pA, kB, vB, pB, flag, total;
 };
 
+// Per-call schedule.  The host plan fixes the sort key q = K' div T and its width B; the
+// call picks how to sort it for this nnz (results are identical, only the cost differs):
+//   copy     B == 0 (identity after normalization);
+//   leaf     nnz fits one on-chip leaf: one kernel, one read + one write;
+//   lsd      P = ceil(B / 11) stable LSD passes (the north_star's LSD over the disturbed
+//            digits), each a tile-granular reduce-then-scan pass;
+//   msd      1-2 stable MSD passes of 8 (+ up to 11) bits, then on-chip leaf sorts of
+//            the remaining bits (the paper's RP recursion into regions).
+// Model: HBM bytes per nonzero (count read 8 + pass r/w ~40, leaf r/w 40).
+struct CallPlan {
+  int path;     // kPathCopy, kPathOnesweep (LSD), kPathLocal (leaf only), kPathMsd
+  int passes;   // global passes
+  int rb;       // LSD radix instantiation
+  MsdPlan msd;
+  KeyPlan kp;
+  double cost;  // modelled bytes per nonzero
+};
+
+CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
+  CallPlan c;
+  memset(&c, 0, sizeof c);
+  c.kp = op.kp;
+  const int B = op.sort_bits;
+  if (op.path == kPathCopy || B == 0) {
+    c.path = kPathCopy;
+    c.cost = 36;
+    return c;
+  }
+  if (nnz <= leaf_cap()) {
+    c.path = kPathLocal;
+    c.msd.levels = 0;
+    c.msd.rb = B;
+    c.cost = 36;
+    return c;
+  }
+  c.path = kPathOnesweep;
+  c.passes = op.passes;
+  c.rb = op.radix_bits;
+  c.cost = 4 + 48.0 * op.passes;
+  if (B <= 11) return c;
+  // MSD digits: enough bits that the expected leaf is <= leaf_target() nonzeros (one
+  // warp sorts it on chip); level 1 prefers 8 bits (cheapest global pass).
+  MsdPlan m;
+  memset(&m, 0, sizeof m);
+  const uint64_t target = leaf_target();
+  double mcost;
+  if ((nnz >> 8) <= target || (B <= 18 && (nnz >> 10) <= target)) {
+    m.levels = 1;
+    m.b1 = ((nnz >> 8) <= target || B < 10) ? 8 : 10;
+    if (m.b1 > B) m.b1 = B;
+    m.rb = B - m.b1;
+    mcost = 8 + 36 + 40;
+  } else {
+    static const int cands[4][2] = {{8, 8}, {8, 10}, {8, 11}, {10, 11}};
+    int k = 3;
+    for (int i = 0; i < 4; ++i)
+      if ((nnz >> (cands[i][0] + cands[i][1])) <= target) {
+        k = i;
+        break;
+      }
+    m.levels = 2;
+    m.b1 = cands[k][0];
+    m.b2 = cands[k][1];
+    if (m.b1 + m.b2 > B) m.b2 = B - m.b1;  // B >= 12 here, so b2 >= 4
+    m.rb = B - m.b1 - m.b2;
+    mcost = 8 + 36 + 8 + 40 + 40;
+  }
+  // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
+  // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
+  // and with a clear modelled win.
+  if (op.segments == 1 && mcost < 0.75 * c.cost) {
+    c.path = kPathMsd;
+    c.msd = m;
+    c.cost = mcost;
+    c.passes = m.levels;
+    c.kp.passes = m.levels;
+    c.kp.dshift[0] = B - m.b1;
+    c.kp.dbits[0] = m.b1;
+    if (m.levels == 2) {
+      c.kp.dshift[1] = B - m.b1 - m.b2;
+      c.kp.dbits[1] = m.b2;
+    }
+  }
+  return c;
+}
+
 // Ping-pong buffers carry (K', V, position); V only when values are moved and the
 // position only when a permutation vector is requested (sizes assume both).
-WsLayout layout_for(int path, int passes, int rb, uint64_t nnz) {
+WsLayout layout_for(const CallPlan& c, uint64_t nnz) {
   WsLayout w;
   memset(&w, 0, sizeof w);
   size_t off = 0;
-  if (path == kPathOnesweep && nnz > 0) {
+  const bool lsd = c.path == kPathOnesweep, msd = c.path == kPathMsd;
+  if ((lsd || msd) && nnz > 0) {
     w.ctrl = off;
-    off += align_up(pass_ctrl_bytes(rb, nnz));
-    if (passes >= 2) {
+    off += align_up(lsd ? pass_ctrl_bytes(c.rb, nnz) : msd_ctrl_bytes(c.msd.b1, c.msd.b2, nnz));
+    if (msd || c.passes >= 2) {
       w.kA = off;
       off += align_up(nnz * 8);
       w.vA = off;
@@ -42,7 +129,7 @@ WsLayout layout_for(int path, int passes, int rb, uint64_t nnz) {
       w.pA = off;
       off += align_up(nnz * 4);
     }
-    if (passes >= 3) {
+    if (msd || c.passes >= 3) {
       w.kB = off;
       off += align_up(nnz * 8);
       w.vB = off;
@@ -157,7 +244,8 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
         return LCO_ERR_ALIAS;
       }
   }
-  const WsLayout w = layout_for(op.path, op.passes, op.radix_bits, nnz);
+  const CallPlan cp = choose_plan(op, nnz);
+  const WsLayout w = layout_for(cp, nnz);
   if (!workspace || ws_bytes < w.total || (reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
     set_error("workspace needs %zu bytes, 256-byte aligned (got %zu at %p)", w.total, ws_bytes,
               workspace);
@@ -192,7 +280,7 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
   ProfCtx pc;
   const bool prof = prof_begin(h, s, &pc, &L);
   cudaError_t e;
-  if (op.path == kPathCopy) {
+  if (cp.path == kPathCopy) {
     e = run_copy(nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, L);
   } else {
     PassIO io;
@@ -206,13 +294,16 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
     io.perm_out = perm_out;
     io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
     const bool mv = vals_out != nullptr, mp = perm_out != nullptr;
-    io.kA = op.passes >= 2 ? reinterpret_cast<uint64_t*>(ws + w.kA) : nullptr;
-    io.vA = op.passes >= 2 && mv ? reinterpret_cast<double*>(ws + w.vA) : nullptr;
-    io.pA = op.passes >= 2 && mp ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
-    io.kB = op.passes >= 3 ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
-    io.vB = op.passes >= 3 && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
-    io.pB = op.passes >= 3 && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
-    e = run_passes(op.radix_bits, op.kp, io, L);
+    const bool hasA = cp.path == kPathMsd || cp.passes >= 2;
+    const bool hasB = cp.path == kPathMsd || cp.passes >= 3;
+    io.kA = hasA ? reinterpret_cast<uint64_t*>(ws + w.kA) : nullptr;
+    io.vA = hasA && mv ? reinterpret_cast<double*>(ws + w.vA) : nullptr;
+    io.pA = hasA && mp ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
+    io.kB = hasB ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
+    io.vB = hasB && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
+    io.pB = hasB && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
+    if (cp.path == kPathOnesweep) e = run_passes(cp.rb, cp.kp, io, L);
+    else e = run_msd(cp.msd, cp.kp, io, L);
   }
   if (prof) prof_end(&pc);
   if (e != cudaSuccess) return cuda_fail(e, sort ? "lco_sort" : "lco_permute");
@@ -279,10 +370,15 @@ lco_status lco_workspace_size(lco_handle h, uint64_t nnz, size_t* bytes) {
   }
   const OpPlan& a = h->op_permute;
   const OpPlan& b = h->op_sort;
-  size_t x = layout_for(a.path, a.passes, a.radix_bits, nnz).total;
-  size_t y = layout_for(b.path, b.passes, b.radix_bits, nnz).total;
+  size_t x = layout_for(choose_plan(a, nnz), nnz).total;
+  size_t y = layout_for(choose_plan(b, nnz), nnz).total;
   // partition (up to 2048 ranks) uses at most a single 11-bit pass
-  size_t z = layout_for(kPathOnesweep, 1, 11, nnz).total;
+  CallPlan part;
+  memset(&part, 0, sizeof part);
+  part.path = kPathOnesweep;
+  part.passes = 1;
+  part.rb = 11;
+  size_t z = layout_for(part, nnz).total;
   size_t m = x > y ? x : y;
   *bytes = m > z ? m : z;
   return LCO_OK;
@@ -389,7 +485,12 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
     return LCO_ERR_ARG;
   }
   const int rb = partition_rb(world);
-  const WsLayout w = layout_for(kPathOnesweep, 1, rb, nnz);
+  CallPlan pp;
+  memset(&pp, 0, sizeof pp);
+  pp.path = kPathOnesweep;
+  pp.passes = 1;
+  pp.rb = rb;
+  const WsLayout w = layout_for(pp, nnz);
   if (!workspace || workspace_bytes < w.total || reinterpret_cast<uintptr_t>(workspace) % kAlign) {
     set_error("workspace needs %zu bytes, 256-byte aligned", w.total);
     return LCO_ERR_WORKSPACE;
@@ -463,12 +564,23 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   info->middle_size = op.middle;
   info->num_segments = op.segments;
   info->sort_bits = op.sort_bits;
-  info->passes = op.passes;
-  for (int j = 0; j < op.passes && j < 8; ++j) info->digit_bits[j] = op.kp.dbits[j];
-  info->radix_bits = op.radix_bits;
-  info->path = op.path;
-  info->tile = op.path == kPathOnesweep ? pass_tile() : 0;
-  info->launches = nnz == 0 ? 0 : (op.path == kPathCopy ? 1 : 3 * op.passes);
+  const CallPlan cp = choose_plan(op, nnz);
+  info->passes = cp.passes;
+  for (int j = 0; j < cp.passes && j < 8; ++j) info->digit_bits[j] = cp.kp.dbits[j];
+  info->radix_bits = cp.path == kPathOnesweep ? cp.rb : (cp.path == kPathMsd ? 8 : 0);
+  info->path = cp.path;
+  info->tile = cp.path == kPathOnesweep || cp.path == kPathMsd ? pass_tile() : 0;
+  info->msd_levels = cp.msd.levels;
+  info->leaf_bits = cp.path == kPathMsd || cp.path == kPathLocal ? cp.msd.rb : 0;
+  info->model_bytes = cp.cost;
+  // kernels of this library per call (cudaMemsetAsync not counted)
+  int launches = 0;
+  if (nnz > 0) {
+    if (cp.path == kPathCopy || cp.path == kPathLocal) launches = 1;
+    else if (cp.path == kPathOnesweep) launches = 4 * cp.passes;
+    else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 1;
+  }
+  info->launches = launches;
   return LCO_OK;
 }
 

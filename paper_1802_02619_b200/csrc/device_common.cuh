@@ -1,0 +1,169 @@
+// device_common.cuh — device helpers shared by kernels.cu and msd.cu (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "lco_internal.h"
+
+namespace lco {
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) {
+  return a < b ? a : b;
+}
+
+constexpr int kThreads = 256;  // k_scatter / k_count CTA size (8 warps)
+constexpr int kItems = 16;     // nonzeros per thread per tile
+constexpr int kTile = kThreads * kItems;
+constexpr int kChunkTiles = 64;  // tiles per scan chunk
+constexpr int kScanThreads = 256;
+constexpr uint32_t kInvalid = 0xFFFFu;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Lanes of the warp holding the same BITS-bit digit (0 for invalid lanes): one ballot
+// per digit bit (ALU pipe), instead of MATCH.ANY (MIO pipe).
+template <int BITS>
+__device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
+  uint32_t m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t v = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? v : ~v;
+  }
+  return valid ? m : 0u;
+}
+
+// ---------------------------------------------------------------------------------
+// Block-wide exclusive scan of BINS counters from `in` into `out`, NT threads.
+// ---------------------------------------------------------------------------------
+template <int NT, int BINS>
+__device__ __forceinline__ void block_scan_bins(const uint32_t* in, uint32_t* out,
+                                                uint32_t* s_warp) {
+  constexpr int PER = BINS >= NT ? BINS / NT : 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t v[PER];
+  uint32_t sum = 0;
+  const bool active = tid * PER < BINS;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    v[i] = active ? in[tid * PER + i] : 0u;
+    sum += v[i];
+  }
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < NT / 32 ? s_warp[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < NT / 32) s_warp[lane] = wi - w;
+  }
+  __syncthreads();
+  uint32_t run = s_warp[warp] + incl - sum;
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      out[tid * PER + i] = run;
+      run += v[i];
+    }
+  }
+  __syncthreads();
+}
+
+// Destination rank of a new key: number of splitters <= k2 (splitters ascending).
+__device__ __forceinline__ uint32_t rank_of(const uint64_t* __restrict__ spl, int world,
+                                            uint64_t k2) {
+  int lo = 0, hi = world - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(spl + mid) <= k2) lo = mid + 1;
+    else hi = mid;
+  }
+  return (uint32_t)lo;
+}
+
+// ---------------------------------------------------------------------------------
+// Per-pass parameters shared by the pass kernels.
+// ---------------------------------------------------------------------------------
+// Segmented passes (MSD level 2): tiles never straddle a segment; the tile table lists
+// every tile's element range and segment.
+struct TileEntry {
+  uint32_t start;
+  uint32_t n;
+  uint32_t seg;
+  uint32_t pad;
+};
+
+struct PassParams {
+  KeyPlan kp;
+  int pass;
+  int qshift;               // >= 0: q = K' >> qshift (T a power of two); -1: fast division
+  uint64_t nnz;
+  uint32_t tiles;
+  uint32_t nchunks;
+  const uint64_t* splitters;  // partition mode: digit = destination rank
+  int world;
+  const TileEntry* ttab;      // segmented mode: tile table (else tiles are t * kTile)
+  const uint32_t* ntiles;     // segmented mode: number of valid table entries
+};
+
+// Shaved key q = K' div T.
+__device__ __forceinline__ uint64_t q_of(const PassParams& a, uint64_t k2) {
+  return a.qshift >= 0 ? (k2 >> a.qshift) : fdiv(a.kp.divT, k2);
+}
+
+__device__ __forceinline__ uint32_t digit_new(const PassParams& a, uint64_t k2) {
+  if (a.splitters) return rank_of(a.splitters, a.world, k2);
+  return digit_of(a.kp, q_of(a, k2), a.pass);
+}
+
+// Element range of tile t; false if t is past the end of a segmented table.
+__device__ __forceinline__ bool tile_range(const PassParams& a, uint32_t t, uint64_t* base,
+                                           uint32_t* n, uint32_t* seg) {
+  if (a.ttab) {
+    if (t >= *a.ntiles) return false;
+    const TileEntry e = a.ttab[t];
+    *base = e.start;
+    *n = e.n;
+    *seg = e.seg;
+    return true;
+  }
+  *base = (uint64_t)t * kTile;
+  *n = (uint32_t)umin64(kTile, a.nnz - *base);
+  *seg = t / kChunkTiles;
+  return true;
+}
+
+// Inputs / outputs of one k_scatter launch.
+struct ScatterIO {
+  const uint64_t* keys_in;  // FIRST pass inputs
+  const double* vals_in;
+  const uint32_t* idx_in;
+  const uint64_t* kin;      // later-pass inputs (carried K', V, source position)
+  const double* vin;
+  const uint32_t* pin;
+  uint64_t* kout;           // outputs (final arrays on the last pass)
+  double* vout;
+  uint32_t* pout;
+  const uint32_t* toff;     // [tiles][BINS] from k_offsets
+  int keep_old_key;         // partition: scatter the old key
+  uint32_t idx_base;        // partition: added to single-pass source positions
+};
+
+}  // namespace lco

@@ -31,119 +31,11 @@
 #include <cstdint>
 #include <cstring>
 
+#include "device_common.cuh"
 #include "launch.h"
 #include "lco_internal.h"
 
 namespace lco {
-
-__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) {
-  return a < b ? a : b;
-}
-
-constexpr int kThreads = 256;  // k_scatter / k_count CTA size (8 warps)
-constexpr int kItems = 16;     // nonzeros per thread per tile
-constexpr int kTile = kThreads * kItems;
-constexpr int kChunkTiles = 64;  // tiles per scan chunk
-constexpr int kScanThreads = 256;
-constexpr uint32_t kInvalid = 0xFFFFu;
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// Lanes of the warp holding the same BITS-bit digit (0 for invalid lanes): one ballot
-// per digit bit (ALU pipe), instead of MATCH.ANY (MIO pipe).
-template <int BITS>
-__device__ __forceinline__ uint32_t peers_of(uint32_t d, bool valid) {
-  uint32_t m = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-  for (int b = 0; b < BITS; ++b) {
-    const bool bit = (d >> b) & 1u;
-    const uint32_t v = __ballot_sync(0xffffffffu, bit);
-    m &= bit ? v : ~v;
-  }
-  return valid ? m : 0u;
-}
-
-// ---------------------------------------------------------------------------------
-// Block-wide exclusive scan of BINS counters from `in` into `out`, NT threads.
-// ---------------------------------------------------------------------------------
-template <int NT, int BINS>
-__device__ __forceinline__ void block_scan_bins(const uint32_t* in, uint32_t* out,
-                                                uint32_t* s_warp) {
-  constexpr int PER = BINS >= NT ? BINS / NT : 1;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint32_t v[PER];
-  uint32_t sum = 0;
-  const bool active = tid * PER < BINS;
-#pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    v[i] = active ? in[tid * PER + i] : 0u;
-    sum += v[i];
-  }
-  uint32_t incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t w = lane < NT / 32 ? s_warp[lane] : 0u;
-    uint32_t wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
-    }
-    if (lane < NT / 32) s_warp[lane] = wi - w;
-  }
-  __syncthreads();
-  uint32_t run = s_warp[warp] + incl - sum;
-  if (active) {
-#pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      out[tid * PER + i] = run;
-      run += v[i];
-    }
-  }
-  __syncthreads();
-}
-
-// Destination rank of a new key: number of splitters <= k2 (splitters ascending).
-__device__ __forceinline__ uint32_t rank_of(const uint64_t* __restrict__ spl, int world,
-                                            uint64_t k2) {
-  int lo = 0, hi = world - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(spl + mid) <= k2) lo = mid + 1;
-    else hi = mid;
-  }
-  return (uint32_t)lo;
-}
-
-// ---------------------------------------------------------------------------------
-// Per-pass parameters shared by the pass kernels.
-// ---------------------------------------------------------------------------------
-struct PassParams {
-  KeyPlan kp;
-  int pass;
-  int qshift;               // >= 0: q = K' >> qshift (T a power of two); -1: fast division
-  uint64_t nnz;
-  uint32_t tiles;
-  uint32_t nchunks;
-  const uint64_t* splitters;  // partition mode: digit = destination rank
-  int world;
-};
-
-__device__ __forceinline__ uint32_t digit_new(const PassParams& a, uint64_t k2) {
-  if (a.splitters) return rank_of(a.splitters, a.world, k2);
-  const uint64_t q = a.qshift >= 0 ? (k2 >> a.qshift) : fdiv(a.kp.divT, k2);
-  return digit_of(a.kp, q, a.pass);
-}
 
 // ---------------------------------------------------------------------------------
 // k_copy
@@ -162,7 +54,8 @@ __global__ void k_copy(uint64_t nnz, const uint64_t* __restrict__ keys_in,
 
 // ---------------------------------------------------------------------------------
 // k_count: one tile per CTA: tile histogram -> thist[t][BINS] (uint16) and added into
-// its chunk's sums csum[t / kChunkTiles][BINS] (zeroed by the launcher).
+// its chunk's sums csum[t / kChunkTiles][BINS] (segmented mode: into its segment's
+// totals csum[seg][BINS]); csum is zeroed by the launcher.
 // ---------------------------------------------------------------------------------
 template <int RB, bool FIRST>
 __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ PassParams a,
@@ -173,9 +66,10 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   __shared__ uint32_t h[BINS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t t = blockIdx.x;
+  uint64_t base;
+  uint32_t n, seg;
+  if (!tile_range(a, t, &base, &n, &seg)) return;
   for (int i = tid; i < BINS; i += kThreads) h[i] = 0;
-  const uint64_t base = (uint64_t)t * kTile;
-  const uint32_t n = (uint32_t)umin64(kTile, a.nnz - base);
   uint64_t k[kItems];
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
@@ -193,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   }
   __syncthreads();
   uint16_t* row = thist + (size_t)t * BINS;
-  uint32_t* cs = csum + (size_t)(t / kChunkTiles) * BINS;
+  uint32_t* cs = csum + (size_t)seg * BINS;  // chunk sums, or segment totals (segmented)
   for (int d = tid; d < BINS; d += kThreads) {
     const uint32_t v = h[d];
     row[d] = (uint16_t)v;
@@ -277,21 +171,6 @@ __global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ Pa
 // ---------------------------------------------------------------------------------
 // k_scatter: one tile per CTA.
 // ---------------------------------------------------------------------------------
-struct ScatterIO {
-  const uint64_t* keys_in;  // FIRST pass inputs
-  const double* vals_in;
-  const uint32_t* idx_in;
-  const uint64_t* kin;      // later-pass inputs (carried K', V, source position)
-  const double* vin;
-  const uint32_t* pin;
-  uint64_t* kout;           // outputs (final arrays on the last pass)
-  double* vout;
-  uint32_t* pout;
-  const uint32_t* toff;     // [tiles][BINS] from k_offsets
-  int keep_old_key;         // partition: scatter the old key
-  uint32_t idx_base;        // partition: added to single-pass source positions
-};
-
 template <int RB>
 constexpr size_t scatter_smem_bytes() {
   return (size_t)kTile * 8 + (size_t)(kThreads / 32) * (1 << RB) * 2 + (size_t)(1 << RB) * 8 +
@@ -314,8 +193,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t t = blockIdx.x;
-  const uint64_t base = (uint64_t)t * kTile;
-  const uint32_t n = (uint32_t)umin64(kTile, a.nnz - base);
+  uint64_t base;
+  uint32_t n, seg;
+  if (!tile_range(a, t, &base, &n, &seg)) return;
   for (int i = tid; i < W * BINS / 2; i += kThreads) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
   // ---- load keys; warp w owns a contiguous slice, lanes consecutive ----
   uint64_t key[kItems];
@@ -505,111 +385,177 @@ static cudaError_t set_smem_attrs() {
 
 uint64_t pass_tiles(uint64_t nnz) { return (nnz + kTile - 1) / kTile; }
 int pass_tile() { return kTile; }
+int pass_rb(int bits) { return bits <= 8 ? 8 : (bits <= 10 ? 10 : 11); }
+
 // control block: thist (uint16 [tiles][bins]) | toff ([tiles][bins]) | csum ([chunks][bins])
 //                | totals | bucket | counter
 size_t pass_ctrl_bytes(int rb, uint64_t nnz) {
   const uint64_t tiles = pass_tiles(nnz);
   const uint64_t chunks = (tiles + kChunkTiles - 1) / kChunkTiles;
   const size_t bins = (size_t)1 << rb;
-  return tiles * bins * 2 + 256 + tiles * bins * 4 + (chunks + 2) * bins * 4 + 512;
+  return (tiles * bins * 2 + 255) / 256 * 256 + tiles * bins * 4 + (chunks + 2) * bins * 4 + 512;
+}
+
+PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl) {
+  PassCtrl c;
+  const uint32_t tiles = (uint32_t)pass_tiles(nnz);
+  const uint32_t nchunks = (tiles + kChunkTiles - 1) / kChunkTiles;
+  const size_t bins = (size_t)1 << rb;
+  char* cb = reinterpret_cast<char*>(ctrl);
+  c.thist = reinterpret_cast<uint16_t*>(cb);
+  cb += ((size_t)tiles * bins * 2 + 255) / 256 * 256;
+  c.toff = reinterpret_cast<uint32_t*>(cb);
+  cb += (size_t)tiles * bins * 4;
+  c.csum = reinterpret_cast<uint32_t*>(cb);
+  c.totals = c.csum + (size_t)nchunks * bins;
+  c.bucket = c.totals + bins;
+  c.done = c.bucket + bins;
+  c.tiles = tiles;
+  c.nchunks = nchunks;
+  return c;
 }
 
 template <int RB>
-static cudaError_t run_passes_rb(const KeyPlan& kp, const PassIO& io, const Launch& L) {
-  constexpr int BINS = 1 << RB;
+static cudaError_t launch_count_rb(bool first, const PassParams& a, const uint64_t* keys,
+                                   uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s) {
+  if (first) k_count<RB, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  else k_count<RB, false><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count(int rb, bool first, const PassParams& a, const uint64_t* keys,
+                         uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s) {
+  switch (rb) {
+    case 8: return launch_count_rb<8>(first, a, keys, thist, csum, grid, s);
+    case 10: return launch_count_rb<10>(first, a, keys, thist, csum, grid, s);
+    case 11: return launch_count_rb<11>(first, a, keys, thist, csum, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int RB>
+static cudaError_t launch_scatter_rb(bool first, bool last, bool vals, const PassParams& a,
+                                     const ScatterIO& io, uint32_t grid, cudaStream_t s) {
   cudaError_t e = set_smem_attrs<RB>();
   if (e != cudaSuccess) return e;
+  const size_t smem = scatter_smem_bytes<RB>();
+#define LCO_LAUNCH(F, LST)                                                      \
+  if (vals) k_scatter<RB, F, LST, true><<<grid, kThreads, smem, s>>>(a, io);   \
+  else k_scatter<RB, F, LST, false><<<grid, kThreads, smem, s>>>(a, io);
+  if (first && last) {
+    LCO_LAUNCH(true, true)
+  } else if (first) {
+    LCO_LAUNCH(true, false)
+  } else if (!last) {
+    LCO_LAUNCH(false, false)
+  } else {
+    LCO_LAUNCH(false, true)
+  }
+#undef LCO_LAUNCH
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(int rb, bool first, bool last, bool vals, const PassParams& a,
+                           const ScatterIO& io, uint32_t grid, cudaStream_t s) {
+  switch (rb) {
+    case 8: return launch_scatter_rb<8>(first, last, vals, a, io, grid, s);
+    case 10: return launch_scatter_rb<10>(first, last, vals, a, io, grid, s);
+    case 11: return launch_scatter_rb<11>(first, last, vals, a, io, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// Buffers of pass j: read set (j-1)%2, write set j%2 (A = 0, B = 1); the first pass reads
+// the inputs, the last writes the outputs.
+ScatterIO pass_buffers(const PassIO& io, int j, bool last, const uint32_t* toff) {
+  ScatterIO s;
+  memset(&s, 0, sizeof s);
+  s.keys_in = io.keys_in;
+  s.vals_in = io.vals_in;
+  s.idx_in = io.idx_in;
+  s.kin = (j % 2 == 1) ? io.kA : io.kB;
+  s.vin = (j % 2 == 1) ? io.vA : io.vB;
+  s.pin = (j % 2 == 1) ? io.pA : io.pB;
+  s.kout = last ? io.keys_out : ((j % 2 == 0) ? io.kA : io.kB);
+  s.vout = last ? io.vals_out : ((j % 2 == 0) ? io.vA : io.vB);
+  s.pout = last ? io.perm_out : ((j % 2 == 0) ? io.pA : io.pB);
+  s.toff = toff;
+  s.keep_old_key = io.splitters ? 1 : 0;
+  s.idx_base = io.idx_base;
+  return s;
+}
+
+// One unsegmented pass: count -> scan -> offsets -> scatter.
+cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool first,
+                     bool last, const Launch& L) {
+  const int BINS = 1 << rb;
+  const PassCtrl c = pass_ctrl_layout(rb, io.nnz, io.ctrl);
+  PassParams a = a0;
+  a.pass = j;
+  a.tiles = c.tiles;
+  a.nchunks = c.nchunks;
+  cudaError_t e;
+  const bool part = io.splitters != nullptr;
+  if ((e = cudaMemsetAsync(c.csum, 0, ((size_t)c.nchunks * BINS + 2 * BINS) * 4 + 4, L.stream)) !=
+      cudaSuccess)
+    return e;  // chunk sums, totals, bucket starts and k_scan's completion counter
+  const uint64_t* in_keys = first ? io.keys_in : ((j % 2 == 1) ? io.kA : io.kB);
+  if (L.mark) L.mark(L.ctx, first ? "k_count_first" : "k_count");
+  if ((e = launch_count(rb, first, a, in_keys, c.thist, c.csum, c.tiles, L.stream)) != cudaSuccess)
+    return e;
+  if (L.mark) L.mark(L.ctx, "k_scan");
+  const int scan_grid = BINS >= 64 ? BINS / 64 : 1;
+  switch (rb) {
+    case 8:
+      k_scan<8><<<scan_grid, kScanThreads, 0, L.stream>>>(c.csum, c.nchunks, c.totals, c.bucket,
+                                                          c.done, part ? io.counts64 : nullptr,
+                                                          io.world);
+      break;
+    case 10:
+      k_scan<10><<<scan_grid, kScanThreads, 0, L.stream>>>(c.csum, c.nchunks, c.totals, c.bucket,
+                                                           c.done, part ? io.counts64 : nullptr,
+                                                           io.world);
+      break;
+    case 11:
+      k_scan<11><<<scan_grid, kScanThreads, 0, L.stream>>>(c.csum, c.nchunks, c.totals, c.bucket,
+                                                           c.done, part ? io.counts64 : nullptr,
+                                                           io.world);
+      break;
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (L.mark) L.mark(L.ctx, "k_offsets");
+  switch (rb) {
+    case 8: k_offsets<8><<<c.nchunks, kThreads, 0, L.stream>>>(a, c.thist, c.csum, c.bucket, c.toff); break;
+    case 10: k_offsets<10><<<c.nchunks, kThreads, 0, L.stream>>>(a, c.thist, c.csum, c.bucket, c.toff); break;
+    case 11: k_offsets<11><<<c.nchunks, kThreads, 0, L.stream>>>(a, c.thist, c.csum, c.bucket, c.toff); break;
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const ScatterIO s = pass_buffers(io, j, last, c.toff);
+  if (L.mark)
+    L.mark(L.ctx, part ? "k_partition"
+                       : (first && last ? "k_scatter_single"
+                                        : (first ? "k_scatter_first"
+                                                 : (last ? "k_scatter_last" : "k_scatter_mid"))));
+  return launch_scatter(rb, first, last, io.vals_out != nullptr, a, s, c.tiles, L.stream);
+}
+
+// Stable LSD radix sort over all passes of the key plan (or one partition pass).
+cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L) {
   const bool part = io.splitters != nullptr;
   const int P = part ? 1 : kp.passes;
-  const uint64_t nnz = io.nnz;
-  const uint32_t tiles = (uint32_t)pass_tiles(nnz);
-  const uint32_t nchunks = (tiles + kChunkTiles - 1) / kChunkTiles;
-  char* cb = reinterpret_cast<char*>(io.ctrl);
-  uint16_t* thist = reinterpret_cast<uint16_t*>(cb);
-  cb += ((size_t)tiles * BINS * 2 + 255) / 256 * 256;
-  uint32_t* toff = reinterpret_cast<uint32_t*>(cb);
-  cb += (size_t)tiles * BINS * 4;
-  uint32_t* csum = reinterpret_cast<uint32_t*>(cb);
-  uint32_t* totals = csum + (size_t)nchunks * BINS;
-  uint32_t* bucket = totals + BINS;
-  uint32_t* done = bucket + BINS;
-
   PassParams a;
   memset(&a, 0, sizeof a);
   a.kp = kp;
   if (part) a.kp.passes = 1;
   a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
-  a.nnz = nnz;
-  a.tiles = tiles;
-  a.nchunks = nchunks;
+  a.nnz = io.nnz;
   a.splitters = io.splitters;
   a.world = io.world;
-  const bool vals = io.vals_out != nullptr;
-  const size_t smem = scatter_smem_bytes<RB>();
   for (int j = 0; j < P; ++j) {
-    a.pass = j;
-    const bool first = j == 0, last = j == P - 1;
-    const uint64_t* in_keys = first ? io.keys_in : ((j % 2 == 1) ? io.kA : io.kB);
-    if ((e = cudaMemsetAsync(csum, 0, ((size_t)nchunks * BINS + 2 * BINS) * 4 + 4, L.stream)) !=
-        cudaSuccess)
-      return e;  // chunk sums, totals, bucket starts and k_scan's completion counter
-    if (L.mark) L.mark(L.ctx, first ? "k_count_first" : "k_count");
-    if (first) k_count<RB, true><<<tiles, kThreads, 0, L.stream>>>(a, in_keys, thist, csum);
-    else k_count<RB, false><<<tiles, kThreads, 0, L.stream>>>(a, in_keys, thist, csum);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (L.mark) L.mark(L.ctx, "k_scan");
-    const int scan_grid = BINS >= 64 ? BINS / 64 : 1;
-    k_scan<RB><<<scan_grid, kScanThreads, 0, L.stream>>>(csum, nchunks, totals, bucket, done,
-                                                        part ? io.counts64 : nullptr, io.world);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    if (L.mark) L.mark(L.ctx, "k_offsets");
-    k_offsets<RB><<<nchunks, kThreads, 0, L.stream>>>(a, thist, csum, bucket, toff);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ScatterIO s;
-    memset(&s, 0, sizeof s);
-    s.keys_in = io.keys_in;
-    s.vals_in = io.vals_in;
-    s.idx_in = io.idx_in;
-    // pass j reads buffer set (j-1)%2 and writes set j%2 (A = 0, B = 1)
-    s.kin = (j % 2 == 1) ? io.kA : io.kB;
-    s.vin = (j % 2 == 1) ? io.vA : io.vB;
-    s.pin = (j % 2 == 1) ? io.pA : io.pB;
-    s.kout = last ? io.keys_out : ((j % 2 == 0) ? io.kA : io.kB);
-    s.vout = last ? io.vals_out : ((j % 2 == 0) ? io.vA : io.vB);
-    s.pout = last ? io.perm_out : ((j % 2 == 0) ? io.pA : io.pB);
-    s.toff = toff;
-    s.keep_old_key = part ? 1 : 0;
-    s.idx_base = io.idx_base;
-    if (L.mark)
-      L.mark(L.ctx, part ? "k_partition"
-                         : (P == 1 ? "k_scatter_single"
-                                   : (first ? "k_scatter_first"
-                                            : (last ? "k_scatter_last" : "k_scatter_mid"))));
-#define LCO_LAUNCH(F, LST)                                                          \
-  if (vals) k_scatter<RB, F, LST, true><<<tiles, kThreads, smem, L.stream>>>(a, s); \
-  else k_scatter<RB, F, LST, false><<<tiles, kThreads, smem, L.stream>>>(a, s);
-    if (P == 1) {
-      LCO_LAUNCH(true, true)
-    } else if (first) {
-      LCO_LAUNCH(true, false)
-    } else if (!last) {
-      LCO_LAUNCH(false, false)
-    } else {
-      LCO_LAUNCH(false, true)
-    }
-#undef LCO_LAUNCH
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    cudaError_t e = run_pass(rb, a, io, j, j == 0, j == P - 1, L);
+    if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
-}
-
-cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L) {
-  switch (rb) {
-    case 8: return run_passes_rb<8>(kp, io, L);
-    case 10: return run_passes_rb<10>(kp, io, L);
-    case 11: return run_passes_rb<11>(kp, io, L);
-  }
-  return cudaErrorInvalidValue;
 }
 
 cudaError_t run_copy(uint64_t nnz, const uint64_t* keys_in, const double* vals_in,

@@ -37,10 +37,46 @@ struct PassIO {
   uint64_t* counts64;
 };
 
+// Pointers into a pass control block (pass_ctrl_bytes()).
+struct PassCtrl {
+  uint16_t* thist;  // [tiles][bins] tile histograms
+  uint32_t* toff;   // [tiles][bins] global position of each tile's digit runs
+  uint32_t* csum;   // [chunks][bins] chunk sums -> exclusive prefix over chunks
+  uint32_t* totals; // [bins] digit totals
+  uint32_t* bucket; // [bins] digit bucket starts
+  uint32_t* done;   // k_scan completion counter
+  uint32_t tiles, nchunks;
+};
+
+// MSD-hybrid schedule (msd.cu): `levels` stable MSD passes of b1 (and b2) bits, then
+// on-chip leaf sorts of the remaining rb bits of q.  levels == 0: the whole input is
+// one leaf.
+struct MsdPlan {
+  int levels;
+  int b1, b2;
+  int rb;
+};
+
+struct PassParams;
+struct ScatterIO;
+
 uint64_t pass_tiles(uint64_t nnz);
 int pass_tile();
+int pass_rb(int bits);
 size_t pass_ctrl_bytes(int rb, uint64_t nnz);
+PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl);
+cudaError_t launch_count(int rb, bool first, const PassParams& a, const uint64_t* keys,
+                         uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s);
+cudaError_t launch_scatter(int rb, bool first, bool last, bool vals, const PassParams& a,
+                           const ScatterIO& io, uint32_t grid, cudaStream_t s);
+ScatterIO pass_buffers(const PassIO& io, int j, bool last, const uint32_t* toff);
+cudaError_t run_pass(int rb, const PassParams& a, const PassIO& io, int j, bool first, bool last,
+                     const Launch& L);
 cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
+uint32_t leaf_cap();      // largest leaf one CTA sorts in shared memory
+uint32_t leaf_target();   // expected leaf size the MSD digits aim for (warp leaves)
+size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
+cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
 cudaError_t run_copy(uint64_t nnz, const uint64_t* keys_in, const double* vals_in,
                      const uint32_t* idx_in, uint64_t* keys_out, double* vals_out,
                      uint32_t* perm_out, const Launch& L);

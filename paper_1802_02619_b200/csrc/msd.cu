@@ -1,0 +1,831 @@
+// msd.cu — the MSD-hybrid schedule for wide sort keys.
+//
+// The paper's RP routine sorts the shaved keys with a stable, out-of-place MSD radix
+// sort that recurses into the regions it creates (§4.1), and LibNT's
+// radix sorts are hybrids that finish small regions with a different sort
+// (PAPER.md:594 suppl.).  On B200 that becomes:
+//   level 1   one stable global pass on the top b1 bits of q (kernels.cu pass kernels);
+//   level 2   for level-1 buckets larger than a leaf, one stable segmented pass on the
+//             next b2 bits (tiles never straddle a bucket: k_msd_tiles builds the tile
+//             table, k_count in segmented mode, k_offsets_seg, k_scatter in segmented
+//             mode);
+//   leaves    every bucket that fits on chip (<= kLeafCap nonzeros) is sorted on its
+//             remaining bits by one CTA in shared memory (k_leaf): stable LSD passes with
+//             ballot ranking over an (key, index) pair, then one gather of (K', V,
+//             position) from L2 and coalesced writes of the final outputs.  Leaves that
+//             do not fit (skewed data) are sorted by the same CTA streaming sub-tiles
+//             through global scratch.
+// Buckets keep their position ranges from level to level (the paper's "regions"), so
+// every leaf writes its final outputs in place.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "device_common.cuh"
+#include "launch.h"
+#include "lco_internal.h"
+
+namespace lco {
+
+constexpr int kLeafCap = 2048;      // largest leaf sorted in shared memory
+constexpr int kLeafBucketBits = 11;  // bucket pass of the on-chip leaf sort: <= 2^11 bins
+constexpr int kSmallBucket = 16;     // buckets up to this size are finished by insertion
+constexpr int kLeafThreads = 256;
+constexpr int kLeafWarps = kLeafThreads / 32;
+
+// ---------------------------------------------------------------------------------
+// k_msd_tiles: one CTA, thread b = level-1 bucket (<= 1024).  Buckets larger than `cap` get tiles
+// in the level-2 tile table; the rest are leaves.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__ totals1,
+                                                   const uint32_t* __restrict__ bucket1,
+                                                   int nb1, uint32_t cap,
+                                                   TileEntry* __restrict__ ttab,
+                                                   uint32_t* __restrict__ tfirst,
+                                                   uint32_t* __restrict__ tcnt,
+                                                   uint32_t* __restrict__ ntiles) {
+  __shared__ uint32_t cnt[1024];
+  __shared__ uint32_t off[1024];
+  __shared__ uint32_t s_warp[32];
+  const int b = threadIdx.x;
+  const uint32_t size = b < nb1 ? totals1[b] : 0u;
+  const uint32_t nt = size > cap ? (size + kTile - 1) / kTile : 0u;
+  cnt[b] = nt;
+  __syncthreads();
+  block_scan_bins<1024, 1024>(cnt, off, s_warp);
+  if (b < nb1) {
+    tfirst[b] = off[b];
+    tcnt[b] = nt;
+  }
+  if (b == 1023) *ntiles = off[1023] + nt;
+  const uint32_t start = b < nb1 ? bucket1[b] : 0u;
+  for (uint32_t j = 0; j < nt; ++j) {
+    TileEntry e;
+    e.start = start + j * kTile;
+    e.n = min((uint32_t)kTile, size - j * kTile);
+    e.seg = b;
+    e.pad = 0;
+    ttab[off[b] + j] = e;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_offsets_seg: CTA per level-1 bucket with tiles.  base2[b][d] = bucket start of
+// sub-bucket (b, d); toff[t][d] = running position over the bucket's tiles.
+// ---------------------------------------------------------------------------------
+template <int RB>
+__global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __restrict__ bucket1,
+                                                          const uint32_t* __restrict__ tfirst,
+                                                          const uint32_t* __restrict__ tcnt,
+                                                          const uint32_t* __restrict__ btot,
+                                                          const uint16_t* __restrict__ thist,
+                                                          uint32_t* __restrict__ base2,
+                                                          uint32_t* __restrict__ toff) {
+  constexpr int BINS = 1 << RB;
+  __shared__ uint32_t tot[BINS];
+  __shared__ uint32_t ex[BINS];
+  __shared__ uint32_t s_warp[32];
+  const int b = blockIdx.x;
+  const uint32_t nt = tcnt[b];
+  if (nt == 0) return;
+  for (int d = threadIdx.x; d < BINS; d += kThreads) tot[d] = btot[(size_t)b * BINS + d];
+  __syncthreads();
+  block_scan_bins<kThreads, BINS>(tot, ex, s_warp);
+  const uint32_t t0 = tfirst[b], start = bucket1[b];
+  for (int d = threadIdx.x; d < BINS; d += kThreads) {
+    uint32_t run = start + ex[d];
+    base2[(size_t)b * BINS + d] = run;
+    for (uint32_t j = 0; j < nt; ++j) {
+      const size_t o = (size_t)(t0 + j) * BINS + d;
+      toff[o] = run;
+      run += thist[o];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Leaf sort.
+// ---------------------------------------------------------------------------------
+struct LeafArgs {
+  PassParams a;            // q = K' div T (qshift / divT)
+  int levels;              // 0: one leaf = the whole input; 1 or 2 MSD levels before
+  int b1, b2;              // level-1 digit bits; level-2 bucket row stride (bits)
+  int rb;                  // remaining bits of q the leaves of this launch sort on
+  int rb1;                 // deferred list: remaining bits of level-1 leaves
+  int only_level;          // 1: this launch sorts the level-1 leaves, 2: level-2 leaves
+  uint32_t cap;            // largest leaf sorted in shared memory
+  const uint32_t* totals1; // level-1 bucket sizes / starts
+  const uint32_t* bucket1;
+  const uint32_t* tcnt;    // level-2 tiles per level-1 bucket (0: bucket is a leaf)
+  const uint32_t* btot;    // level-2 sub-bucket sizes / starts
+  const uint32_t* base2;
+  // data: the original input (levels == 0), buffer A (level-1 output), B (level-2)
+  const uint64_t* keys_in;
+  const double* vals_in;
+  const uint32_t* idx_in;
+  uint64_t* kA;
+  double* vA;
+  uint32_t* pA;
+  uint64_t* kB;
+  double* vB;
+  uint32_t* pB;
+  uint64_t* keys_out;
+  double* vals_out;
+  uint32_t* perm_out;
+  // leaves a warp could not sort (too large, or skewed buckets) go to a list that the
+  // block-level kernel drains: entry = level << 30 | slot
+  uint32_t* defer;
+  uint32_t* ndefer;
+  const uint32_t* dlist;   // block kernel: deferred list to drain (null: slot mode)
+  const uint32_t* dcount;
+};
+
+// A readable (K', V, position) array set.
+struct Rec {
+  const uint64_t* k;
+  const double* v;
+  const uint32_t* p;
+  bool raw;  // k holds input keys (re-encode on read), positions are implicit
+};
+
+// Shared-memory layout of a (persistent) leaf CTA: two stages of records (K', V,
+// position) of up to kLeafCap nonzeros — the next leaf streams in with cp.async while
+// the current one is sorted — plus two index arrays, the bucket table and the rank
+// counters of the radix fallback.
+constexpr size_t kLeafStageBytes = (size_t)kLeafCap * (8 + 8 + 4);
+constexpr size_t leaf_smem_bytes(int lb) {
+  return 2 * kLeafStageBytes + (size_t)kLeafCap * 4 + ((size_t)1 << kLeafBucketBits) * 4 +
+         (size_t)kLeafWarps * ((size_t)1 << lb) * 4 + ((size_t)1 << lb) * 12 + 64;
+}
+
+struct LeafDesc {
+  uint32_t start, n;
+  int src;  // 0: raw input (re-encode), 1: buffer A, 2: buffer B  (== MSD level)
+};
+
+__device__ __forceinline__ uint32_t leaf_slots(const LeafArgs& L, int level) {
+  return level == 0 ? 1u : (level == 1 ? (1u << L.b1) : (1u << (L.b1 + L.b2)));
+}
+
+// Leaf `slot` of MSD level `level` (0: the raw input as one leaf); false if empty or
+// split further.
+__device__ __forceinline__ bool leaf_at(const LeafArgs& L, int level, uint32_t slot,
+                                        LeafDesc* d) {
+  if (slot >= leaf_slots(L, level)) return false;
+  if (level == 0) {
+    *d = LeafDesc{0u, (uint32_t)L.a.nnz, 0};
+  } else if (level == 1) {
+    if (L.levels == 2 && L.tcnt[slot] > 0) return false;  // split again at level 2
+    *d = LeafDesc{L.bucket1[slot], L.totals1[slot], 1};
+  } else {
+    if (L.tcnt[slot >> L.b2] == 0) return false;
+    *d = LeafDesc{L.base2[slot], L.btot[slot], 2};
+  }
+  return d->n > 0;
+}
+
+// Next leaf of this CTA at or after position `k` (stride gridDim.x) of its work list:
+// the deferred list (entries level << 30 | slot) or, without one, the slots of
+// L.only_level.
+__device__ __forceinline__ bool next_leaf(const LeafArgs& L, uint32_t& k, LeafDesc* d) {
+  if (L.dlist) {
+    const uint32_t cnt = *L.dcount;
+    for (; k < cnt; k += gridDim.x) {
+      const uint32_t e = L.dlist[k];
+      if (leaf_at(L, (int)(e >> 30), e & ((1u << 30) - 1), d)) return true;
+    }
+    return false;
+  }
+  const uint32_t nslots = leaf_slots(L, L.only_level);
+  for (; k < nslots; k += gridDim.x)
+    if (leaf_at(L, L.only_level, k, d)) return true;
+  return false;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Sort key of a staged record: the leaf's remaining bits of q = K' div T.
+__device__ __forceinline__ uint64_t leaf_key(const LeafArgs& L, uint64_t k2, uint64_t mask) {
+  return q_of(L.a, k2) & mask;
+}
+
+// Block-wide stable counting sort of m <= kLeafCap indices by the LB-bit digit at
+// `shift` of the staged keys: per-warp contiguous slices, counts, then an in-order
+// ballot ranking sweep.  On return io holds the sorted indices, loff[d] the first slot
+// of digit d and cnt[d] its count.
+template <int LB>
+__device__ __forceinline__ void leaf_rank_pass(const LeafArgs& L, const uint64_t* Kp,
+                                               uint64_t mask, const uint16_t* ii, uint16_t* io,
+                                               uint32_t m, int shift, uint32_t* whist,
+                                               uint32_t* loff, uint32_t* cnt, uint32_t* s_warp) {
+  constexpr int BINS = 1 << LB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t slice = ((m + kLeafWarps - 1) / kLeafWarps + 31) / 32 * 32;
+  const uint32_t s0 = min(m, warp * slice), s1 = min(m, s0 + slice);
+  uint32_t* wh = whist + warp * BINS;
+  for (int i = tid; i < kLeafWarps * BINS; i += kLeafThreads) whist[i] = 0;
+  __syncthreads();
+  for (uint32_t i = s0 + lane; i < s1; i += 32)
+    atomicAdd(&wh[(uint32_t)(leaf_key(L, Kp[ii[i]], mask) >> shift) & (BINS - 1)], 1u);
+  __syncthreads();
+  for (int d = tid; d < BINS; d += kLeafThreads) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int w = 0; w < kLeafWarps; ++w) {
+      const uint32_t c = whist[w * BINS + d];
+      whist[w * BINS + d] = s;
+      s += c;
+    }
+    cnt[d] = s;
+  }
+  __syncthreads();
+  block_scan_bins<kLeafThreads, BINS>(cnt, loff, s_warp);
+  for (int i = tid; i < kLeafWarps * BINS; i += kLeafThreads) whist[i] += loff[i % BINS];
+  __syncthreads();
+  const uint32_t ltm = lanemask_lt();
+  const uint32_t rounds = (s1 - s0 + 31) / 32;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    const uint32_t i = s0 + r * 32 + lane;
+    const bool ok = i < s1;
+    const uint16_t x = ok ? ii[i] : (uint16_t)0;
+    const uint32_t d = ok ? (uint32_t)(leaf_key(L, Kp[x], mask) >> shift) & (BINS - 1) : 0u;
+    const uint32_t peers = peers_of<LB>(d, ok);
+    const bool leader = ok && (peers & ltm) == 0;
+    uint32_t before = 0;
+    if (leader) {
+      before = wh[d];
+      wh[d] = before + __popc(peers);
+    }
+    before = __shfl_sync(0xffffffffu, before, ok ? __ffs(peers) - 1 : lane);
+    if (ok) io[before + __popc(peers & ltm)] = x;
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+template <bool VALS>
+__device__ __forceinline__ void store_rec(const LeafArgs& L, uint64_t g, uint64_t k2, double v,
+                                          uint32_t pos) {
+  L.keys_out[g] = k2;
+  if (VALS) L.vals_out[g] = v;
+  if (L.perm_out) L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pos) : pos;
+}
+
+template <int LB, bool VALS>
+__global__ void __launch_bounds__(kLeafThreads) k_leaf(const __grid_constant__ LeafArgs L) {
+  constexpr int BINS = 1 << LB;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* Kst[2];
+  double* Vst[2];
+  uint32_t* Pst[2];
+  {
+    unsigned char* p = smem;
+    for (int s = 0; s < 2; ++s) {
+      Kst[s] = reinterpret_cast<uint64_t*>(p);
+      Vst[s] = reinterpret_cast<double*>(p + kLeafCap * 8);
+      Pst[s] = reinterpret_cast<uint32_t*>(p + kLeafCap * 16);
+      p += kLeafStageBytes;
+    }
+  }
+  unsigned char* q = smem + 2 * kLeafStageBytes;
+  uint16_t* ia = reinterpret_cast<uint16_t*>(q);                          // [cap]
+  uint16_t* ib = ia + kLeafCap;                                           // [cap]
+  uint32_t* bkt = reinterpret_cast<uint32_t*>(ib + kLeafCap);             // [2^bits]
+  uint32_t* whist = bkt + (1 << kLeafBucketBits);                         // [warps][BINS]
+  uint32_t* loff = whist + kLeafWarps * BINS;                             // [BINS]
+  uint32_t* cnt = loff + BINS;                                            // [BINS]
+  uint32_t* run = cnt + BINS;                                             // [BINS]
+  __shared__ uint32_t s_warp[32];
+  __shared__ int s_big;
+
+  const int tid = threadIdx.x;
+  const bool want_pos = L.perm_out != nullptr;
+
+  auto srcrec = [&](int src) -> Rec {
+    if (src == 0) return Rec{L.keys_in, L.vals_in, nullptr, true};
+    if (src == 1) return Rec{L.kA, L.vA, L.pA, false};
+    return Rec{L.kB, L.vB, L.pB, false};
+  };
+  // Synchronous staging of records [e0, e0 + m) of leaf d (raw input / fallback).
+  auto load_sync = [&](const LeafDesc& d, int st, uint32_t e0, uint32_t m, const Rec& r) {
+    for (uint32_t i = tid; i < m; i += kLeafThreads) {
+      const uint64_t gi = (uint64_t)d.start + e0 + i;
+      const uint64_t k = __ldcs(r.k + gi);
+      Kst[st][i] = r.raw ? reencode(L.a.kp, k) : k;
+      if (VALS) Vst[st][i] = __ldcs(r.v + gi);
+      if (want_pos) Pst[st][i] = r.raw ? (uint32_t)gi : __ldcs(r.p + gi);
+    }
+  };
+  // Asynchronous staging of a whole leaf (buffers A / B only).
+  auto prefetch = [&](const LeafDesc& d, int st) {
+    const Rec r = srcrec(d.src);
+    for (uint32_t i = tid; i < d.n; i += kLeafThreads) {
+      const uint64_t gi = (uint64_t)d.start + i;
+      cp_async8(Kst[st] + i, r.k + gi);
+      if (VALS) cp_async8(Vst[st] + i, r.v + gi);
+      if (want_pos) cp_async4(Pst[st] + i, r.p + gi);
+    }
+  };
+  auto async_ok = [&](const LeafDesc& d) { return d.src != 0 && d.n <= L.cap; };
+
+  uint32_t slot = blockIdx.x;
+  LeafDesc cur;
+  bool has = next_leaf(L, slot, &cur);
+  if (has && async_ok(cur)) prefetch(cur, 0);
+  cp_async_commit();
+  int st = 0;
+  while (has) {
+    uint32_t nslot = slot + gridDim.x;
+    LeafDesc nxt;
+    const bool hasn = next_leaf(L, nslot, &nxt);
+    if (hasn && async_ok(nxt)) prefetch(nxt, st ^ 1);
+    cp_async_commit();
+    uint64_t* Kp = Kst[st];
+    double* Vs = Vst[st];
+    uint32_t* Ps = Pst[st];
+    const uint32_t n = cur.n, start = cur.start;
+    // level-1 leaves of a two-level plan sort more bits than level-2 leaves
+    const int rb = (L.dlist && cur.src == 1) ? L.rb1 : L.rb;
+    const uint64_t mask = rb >= 64 ? ~0ull : ((1ull << rb) - 1ull);
+    const int npass = (rb + LB - 1) / LB;
+    if (n <= L.cap) {
+      if (cur.src == 0) load_sync(cur, st, 0, n, srcrec(0));
+      cp_async_wait<1>();  // this thread's copies of the current leaf have landed
+      for (uint32_t i = tid; i < n; i += kLeafThreads) ia[i] = (uint16_t)i;
+      // Bucket pass on the top tb bits (about one bucket per nonzero): unordered slots
+      // from shared atomics, then each bucket is finished by insertion on (key, index);
+      // the index tie-break makes the result exactly the stable order.  A bucket larger
+      // than kSmallBucket (skewed or duplicate keys) sends the leaf to stable radix
+      // passes.
+      int lg = 0;
+      while ((1u << lg) < n) ++lg;
+      const int tb = min(min(rb, max(lg, 1)), kLeafBucketBits);
+      const int bshift = rb - tb;
+      const uint32_t nbk = 1u << tb;
+      for (uint32_t b = tid; b < nbk; b += kLeafThreads) bkt[b] = 0;
+      if (tid == 0) s_big = 0;
+      __syncthreads();  // staged records, bucket table zeroed
+      for (uint32_t i = tid; i < n; i += kLeafThreads)
+        atomicAdd(&bkt[(uint32_t)(leaf_key(L, Kp[i], mask) >> bshift)], 1u);
+      __syncthreads();
+      {  // exclusive scan of the bucket counts
+        const uint32_t per = (nbk + kLeafThreads - 1) / kLeafThreads;
+        const uint32_t b0 = min(nbk, tid * per), b1 = min(nbk, b0 + per);
+        uint32_t sum = 0;
+        for (uint32_t b = b0; b < b1; ++b) sum += bkt[b];
+        cnt[tid] = sum;
+        __syncthreads();
+        block_scan_bins<kLeafThreads, kLeafThreads>(cnt, loff, s_warp);
+        uint32_t r = loff[tid];
+        for (uint32_t b = b0; b < b1; ++b) {
+          const uint32_t c = bkt[b];
+          bkt[b] = r;
+          r += c;
+        }
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < n; i += kLeafThreads)
+        ib[atomicAdd(&bkt[(uint32_t)(leaf_key(L, Kp[i], mask) >> bshift)], 1u)] = (uint16_t)i;
+      __syncthreads();
+      for (uint32_t b = tid; b < nbk; b += kLeafThreads) {  // bkt[b] = end of bucket b
+        const uint32_t lo = b ? bkt[b - 1] : 0u, hi = bkt[b];
+        if (hi - lo > (uint32_t)kSmallBucket) {
+          s_big = 1;
+        } else {
+          for (uint32_t i = lo + 1; i < hi; ++i) {
+            const uint16_t x = ib[i];
+            const uint64_t k = leaf_key(L, Kp[x], mask);
+            uint32_t j = i;
+            while (j > lo) {
+              const uint16_t y = ib[j - 1];
+              const uint64_t ky = leaf_key(L, Kp[y], mask);
+              if (ky < k || (ky == k && y < x)) break;
+              ib[j] = y;
+              --j;
+            }
+            ib[j] = x;
+          }
+        }
+      }
+      __syncthreads();
+      const uint16_t* order = ib;
+      if (s_big) {  // stable LSD radix passes on the original order
+        uint16_t* xa = ia;
+        uint16_t* xb = ib;
+        for (int p = 0; p < npass; ++p) {
+          leaf_rank_pass<LB>(L, Kp, mask, xa, xb, n, p * LB, whist, loff, cnt, s_warp);
+          uint16_t* t = xa; xa = xb; xb = t;
+        }
+        order = xa;
+      }
+      for (uint32_t j = tid; j < n; j += kLeafThreads) {
+        const uint16_t e = order[j];
+        store_rec<VALS>(L, (uint64_t)start + j, Kp[e], VALS ? Vs[e] : 0.0, want_pos ? Ps[e] : 0u);
+      }
+    } else {
+      // ---------------- fallback: leaf larger than shared memory -------------------
+      // Stable LSD over the remaining bits; each pass streams sub-tiles of kLeafCap in
+      // order with running per-digit offsets, ping-ponging between the scratch ranges of
+      // the other buffers; the last pass writes the final outputs.
+      uint64_t* sk[2];
+      double* sv[2];
+      uint32_t* sp[2];
+      if (cur.src == 1) {
+        sk[0] = L.kB; sv[0] = L.vB; sp[0] = L.pB;
+        sk[1] = L.kA; sv[1] = L.vA; sp[1] = L.pA;
+      } else {  // level-2 leaves (src B); the raw input never exceeds one leaf
+        sk[0] = L.kA; sv[0] = L.vA; sp[0] = L.pA;
+        sk[1] = L.kB; sv[1] = L.vB; sp[1] = L.pB;
+      }
+      Rec rcur = srcrec(cur.src);
+      int target = 0;
+      for (int p = 0; p < npass; ++p) {
+        const bool last = p == npass - 1;
+        const int shift = p * LB;
+        for (int d = tid; d < BINS; d += kLeafThreads) cnt[d] = 0;
+        __syncthreads();
+        for (uint32_t i = tid; i < n; i += kLeafThreads) {
+          const uint64_t k = __ldcs(rcur.k + (uint64_t)start + i);
+          atomicAdd(&cnt[(uint32_t)(leaf_key(L, k, mask) >> shift) & (BINS - 1)], 1u);
+        }
+        __syncthreads();
+        block_scan_bins<kLeafThreads, BINS>(cnt, run, s_warp);
+        for (uint32_t s0 = 0; s0 < n; s0 += L.cap) {
+          const uint32_t m = min(L.cap, n - s0);
+          load_sync(cur, st, s0, m, rcur);
+          for (uint32_t i = tid; i < m; i += kLeafThreads) ia[i] = (uint16_t)i;
+          __syncthreads();
+          leaf_rank_pass<LB>(L, Kp, mask, ia, ib, m, shift, whist, loff, cnt, s_warp);
+          for (uint32_t j = tid; j < m; j += kLeafThreads) {
+            const uint16_t e = ib[j];
+            const uint32_t d = (uint32_t)(leaf_key(L, Kp[e], mask) >> shift) & (BINS - 1);
+            const uint64_t g = (uint64_t)start + run[d] + (j - loff[d]);
+            if (last) {
+              store_rec<VALS>(L, g, Kp[e], VALS ? Vs[e] : 0.0, want_pos ? Ps[e] : 0u);
+            } else {
+              sk[target][g] = Kp[e];
+              if (VALS) sv[target][g] = Vs[e];
+              if (want_pos) sp[target][g] = Ps[e];
+            }
+          }
+          __syncthreads();
+          for (int d = tid; d < BINS; d += kLeafThreads) run[d] += cnt[d];
+          __syncthreads();
+        }
+        rcur = Rec{sk[target], sv[target], sp[target], false};
+        target ^= 1;
+      }
+    }
+    __syncthreads();  // the stage is free for the prefetch two leaves ahead
+    cur = nxt;
+    has = hasn;
+    slot = nslot;
+    st ^= 1;
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------
+// k_leafw: one warp per leaf of up to kWCap nonzeros (the common case: the MSD digits
+// aim at ~kWCap/2).  Warp-synchronous, no block barriers: cp.async staging of (K', V,
+// position), bucket pass on the top bits with shared atomics, insertion per bucket on
+// (key, index) (exactly the stable order), coalesced writes.  Leaves that are larger, or
+// whose buckets are not small (skewed or duplicate keys), are appended to the deferred
+// list for the block-level k_leaf.  Leaf descriptors are fetched 32 at a time (one per
+// lane).
+// ---------------------------------------------------------------------------------
+constexpr int kWCap = 512;
+constexpr int kWBucketBits = 9;
+constexpr int kWWarps = 8;  // warps per CTA
+constexpr size_t kWWarpBytes = (size_t)kWCap * (8 + 8 + 4 + 2) + ((size_t)1 << kWBucketBits) * 4;
+
+uint32_t leaf_target() { return kWCap / 2; }
+
+template <bool VALS>
+__global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ LeafArgs L) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned char* base = smem + warp * kWWarpBytes;
+  uint64_t* K = reinterpret_cast<uint64_t*>(base);
+  double* V = reinterpret_cast<double*>(base + kWCap * 8);
+  uint32_t* P = reinterpret_cast<uint32_t*>(base + kWCap * 16);
+  uint16_t* X = reinterpret_cast<uint16_t*>(base + kWCap * 20);
+  uint32_t* B = reinterpret_cast<uint32_t*>(base + kWCap * 22);
+  const bool want_pos = L.perm_out != nullptr;
+  const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
+  const int level = L.only_level;
+  const uint32_t nslots = leaf_slots(L, level);
+  const uint32_t W = gridDim.x * kWWarps;
+  const uint32_t gw = blockIdx.x * kWWarps + warp;
+  const uint32_t ltm = lanemask_lt();
+  for (uint64_t b0 = gw; b0 < nslots; b0 += (uint64_t)32 * W) {
+    const uint64_t myslot = b0 + (uint64_t)lane * W;
+    LeafDesc d;
+    bool ok = myslot < nslots && leaf_at(L, level, (uint32_t)myslot, &d);
+    if (ok && d.n > (uint32_t)kWCap) {  // larger than a warp leaf: defer
+      L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)level << 30) | (uint32_t)myslot;
+      ok = false;
+    }
+    uint32_t todo = __ballot_sync(0xffffffffu, ok);
+    while (todo) {
+      const int l = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t start = __shfl_sync(0xffffffffu, d.start, l);
+      const uint32_t n = __shfl_sync(0xffffffffu, d.n, l);
+      const int srcid = __shfl_sync(0xffffffffu, d.src, l);
+      const uint64_t* sk = srcid == 1 ? L.kA : L.kB;
+      const double* sv = srcid == 1 ? L.vA : L.vB;
+      const uint32_t* sp = srcid == 1 ? L.pA : L.pB;
+      for (uint32_t i = lane; i < n; i += 32) {
+        cp_async8(K + i, sk + (uint64_t)start + i);
+        if (VALS) cp_async8(V + i, sv + (uint64_t)start + i);
+        if (want_pos) cp_async4(P + i, sp + (uint64_t)start + i);
+      }
+      cp_async_commit();
+      int lg = 0;
+      while ((1u << lg) < n) ++lg;
+      const int tb = min(min(L.rb, max(lg, 1)), kWBucketBits);
+      const int bshift = L.rb - tb;
+      const uint32_t nbk = 1u << tb;
+      for (uint32_t b = lane; b < nbk; b += 32) B[b] = 0;
+      cp_async_wait<0>();
+      __syncwarp();
+      for (uint32_t i = lane; i < n; i += 32)
+        atomicAdd(&B[(uint32_t)(leaf_key(L, K[i], mask) >> bshift)], 1u);
+      __syncwarp();
+      {  // warp exclusive scan of the bucket counts (contiguous chunk per lane)
+        const uint32_t per = (nbk + 31) / 32;
+        const uint32_t c0 = min(nbk, lane * per), c1 = min(nbk, c0 + per);
+        uint32_t sum = 0;
+        for (uint32_t b = c0; b < c1; ++b) sum += B[b];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        uint32_t r = incl - sum;
+        for (uint32_t b = c0; b < c1; ++b) {
+          const uint32_t c = B[b];
+          B[b] = r;
+          r += c;
+        }
+      }
+      __syncwarp();
+      for (uint32_t i = lane; i < n; i += 32)
+        X[atomicAdd(&B[(uint32_t)(leaf_key(L, K[i], mask) >> bshift)], 1u)] = (uint16_t)i;
+      __syncwarp();
+      bool big = false;
+      for (uint32_t b = lane; b < nbk; b += 32) {  // B[b] = end of bucket b
+        const uint32_t lo = b ? B[b - 1] : 0u, hi = B[b];
+        if (hi - lo > (uint32_t)kSmallBucket) {
+          big = true;
+        } else {
+          for (uint32_t i = lo + 1; i < hi; ++i) {
+            const uint16_t x = X[i];
+            const uint64_t k = leaf_key(L, K[x], mask);
+            uint32_t j = i;
+            while (j > lo) {
+              const uint16_t y = X[j - 1];
+              const uint64_t ky = leaf_key(L, K[y], mask);
+              if (ky < k || (ky == k && y < x)) break;
+              X[j] = y;
+              --j;
+            }
+            X[j] = x;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, big)) {  // skewed leaf: the block kernel sorts it
+        const uint32_t slot = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)myslot, l);
+        if (lane == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)level << 30) | slot;
+        __syncwarp();
+        continue;
+      }
+      __syncwarp();
+      for (uint32_t j = lane; j < n; j += 32) {
+        const uint16_t e = X[j];
+        const uint64_t g = (uint64_t)start + j;
+        L.keys_out[g] = K[e];
+        if (VALS) L.vals_out[g] = V[e];
+        if (want_pos) {
+          const uint32_t pos = P[e];
+          L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pos) : pos;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// Launchers
+// ---------------------------------------------------------------------------------
+template <int LB, bool VALS>
+static cudaError_t launch_leaf(const LeafArgs& L, uint32_t grid, cudaStream_t s) {
+  static bool attr = false;
+  static int per_sm = 1;
+  const size_t smem = leaf_smem_bytes(LB);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_leaf<LB, VALS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leaf<LB, VALS>, kLeafThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t persistent = (uint32_t)(sms * per_sm);
+  k_leaf<LB, VALS><<<grid < persistent ? grid : persistent, kLeafThreads, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+static cudaError_t run_leaf(const LeafArgs& L, uint32_t grid, bool vals, cudaStream_t s) {
+  return vals ? launch_leaf<8, true>(L, grid, s) : launch_leaf<8, false>(L, grid, s);
+}
+
+template <bool VALS>
+static cudaError_t launch_leafw(const LeafArgs& L, cudaStream_t s) {
+  static bool attr = false;
+  static int per_sm = 1;
+  const size_t smem = kWWarpBytes * kWWarps;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_leafw<VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leafw<VALS>, kWWarps * 32, smem);
+    if (per_sm < 1) per_sm = 1;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_leafw<VALS><<<sms * per_sm, kWWarps * 32, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+uint32_t leaf_cap() { return kLeafCap; }
+
+// Workspace of the MSD schedule beyond the ping-pong buffers: the level-1 pass control
+// block, then the level-2 tables.
+size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz) {
+  const size_t nb1 = (size_t)1 << b1;
+  const uint64_t tiles2 = pass_tiles(nnz) + nb1;
+  size_t s = (pass_ctrl_bytes(pass_rb(b1), nnz) + 255) / 256 * 256;
+  if (b2 > 0) {
+    const size_t rbins2 = (size_t)1 << pass_rb(b2);
+    s += (tiles2 * sizeof(TileEntry) + 255) / 256 * 256;
+    s += (nb1 * 12 + 4 + 255) / 256 * 256;          // tfirst, tcnt, ntiles
+    s += (nb1 * rbins2 * 8 + 255) / 256 * 256;      // btot, base2
+    s += (tiles2 * rbins2 * 2 + 255) / 256 * 256;   // thist2
+    s += tiles2 * rbins2 * 4;                       // toff2
+    s = (s + 255) / 256 * 256 + (nb1 * rbins2 + nb1 + 64) * 4;  // deferred leaf list
+  } else {
+    s += (2 * nb1 + 64) * 4;
+  }
+  return s + 256;
+}
+
+cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& Lc) {
+  cudaError_t e;
+  const uint64_t nnz = io.nnz;
+  const bool vals = io.vals_out != nullptr;
+  PassParams a;
+  memset(&a, 0, sizeof a);
+  a.kp = kp;
+  a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
+  a.nnz = nnz;
+  LeafArgs L;
+  memset(&L, 0, sizeof L);
+  L.a = a;
+  L.levels = mp.levels;
+  L.b1 = mp.b1;
+  L.rb = mp.rb;
+  L.cap = kLeafCap;
+  L.keys_in = io.keys_in;
+  L.vals_in = io.vals_in;
+  L.idx_in = io.idx_in;
+  L.kA = io.kA;
+  L.vA = io.vA;
+  L.pA = io.pA;
+  L.kB = io.kB;
+  L.vB = io.vB;
+  L.pB = io.pB;
+  L.keys_out = io.keys_out;
+  L.vals_out = io.vals_out;
+  L.perm_out = io.perm_out;
+  if (mp.levels == 0) {
+    L.only_level = 0;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf");
+    return run_leaf(L, 1, vals, Lc.stream);
+  }
+  // ---- level 1: stable global pass on the top b1 bits of q, into buffer A ----
+  const int rb1 = pass_rb(mp.b1);
+  char* cb = reinterpret_cast<char*>(io.ctrl);
+  PassIO io1 = io;
+  io1.ctrl = reinterpret_cast<uint32_t*>(cb);
+  cb += (pass_ctrl_bytes(rb1, nnz) + 255) / 256 * 256;
+  if ((e = run_pass(rb1, a, io1, 0, true, false, Lc)) != cudaSuccess) return e;
+  const PassCtrl c1 = pass_ctrl_layout(rb1, nnz, io1.ctrl);
+  L.totals1 = c1.totals;
+  L.bucket1 = c1.bucket;
+  const uint32_t nb1 = 1u << mp.b1;
+  if (mp.levels == 2) {
+    // ---- level 2: stable segmented pass on the next b2 bits, A -> B ----
+    const int rb2 = pass_rb(mp.b2);
+    const size_t rbins2 = (size_t)1 << rb2;
+    const uint64_t tiles2 = pass_tiles(nnz) + nb1;
+    TileEntry* ttab = reinterpret_cast<TileEntry*>(cb);
+    cb += (tiles2 * sizeof(TileEntry) + 255) / 256 * 256;
+    uint32_t* tfirst = reinterpret_cast<uint32_t*>(cb);
+    uint32_t* tcnt = tfirst + nb1;
+    uint32_t* ntiles = tcnt + nb1;
+    cb += ((size_t)nb1 * 12 + 4 + 255) / 256 * 256;
+    uint32_t* btot = reinterpret_cast<uint32_t*>(cb);
+    uint32_t* base2 = btot + (size_t)nb1 * rbins2;
+    cb += ((size_t)nb1 * rbins2 * 8 + 255) / 256 * 256;
+    uint16_t* thist2 = reinterpret_cast<uint16_t*>(cb);
+    cb += (tiles2 * rbins2 * 2 + 255) / 256 * 256;
+    uint32_t* toff2 = reinterpret_cast<uint32_t*>(cb);
+    cb += (tiles2 * rbins2 * 4 + 255) / 256 * 256;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
+    k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1, kLeafCap, ttab, tfirst,
+                                          tcnt, ntiles);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess)
+      return e;
+    PassParams a2 = a;
+    a2.pass = 1;
+    a2.ttab = ttab;
+    a2.ntiles = ntiles;
+    a2.tiles = (uint32_t)tiles2;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_count_seg");
+    if ((e = launch_count(rb2, false, a2, io.kA, thist2, btot, (uint32_t)tiles2, Lc.stream)) !=
+        cudaSuccess)
+      return e;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg");
+    switch (rb2) {
+      case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+      case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+      case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const ScatterIO s = pass_buffers(io, 1, false, toff2);
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_scatter_seg");
+    if ((e = launch_scatter(rb2, false, false, vals, a2, s, (uint32_t)tiles2, Lc.stream)) !=
+        cudaSuccess)
+      return e;
+    L.tcnt = tcnt;
+    L.btot = btot;
+    L.base2 = base2;
+    L.b2 = rb2;  // leaf slots are indexed with the bucket row stride
+  }
+  // ---- leaves: warps sort the small ones, the block kernel drains the deferred list ----
+  uint32_t* defer = reinterpret_cast<uint32_t*>(cb);
+  uint32_t* ndefer = defer + ((size_t)1 << (mp.b1 + (mp.levels == 2 ? pass_rb(mp.b2) : 0))) + nb1;
+  if ((e = cudaMemsetAsync(ndefer, 0, 4, Lc.stream)) != cudaSuccess) return e;
+  L.defer = defer;
+  L.ndefer = ndefer;
+  if (mp.levels == 2) {
+    LeafArgs L2 = L;
+    L2.only_level = 2;
+    L2.rb = mp.rb;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_leafw");
+    if ((e = vals ? launch_leafw<true>(L2, Lc.stream) : launch_leafw<false>(L2, Lc.stream)) !=
+        cudaSuccess)
+      return e;
+  }
+  // level-1 buckets that were not split again sort the bits left after level 1
+  LeafArgs L1 = L;
+  L1.only_level = 1;
+  L1.rb = mp.rb + (mp.levels == 2 ? mp.b2 : 0);
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_leafw_l1");
+  if ((e = vals ? launch_leafw<true>(L1, Lc.stream) : launch_leafw<false>(L1, Lc.stream)) !=
+      cudaSuccess)
+    return e;
+  // deferred leaves (both levels share one list; rb depends on the entry's level)
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf_deferred");
+  LeafArgs LD = L;
+  LD.dlist = defer;
+  LD.dcount = ndefer;
+  LD.rb = mp.rb;
+  LD.rb1 = mp.rb + (mp.levels == 2 ? mp.b2 : 0);
+  return run_leaf(LD, 1u << 20, vals, Lc.stream);
+}
+
+}  // namespace lco

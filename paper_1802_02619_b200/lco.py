@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "liblco.so")
 
 FLAG_VALIDATE = 1
 MAX_ORDER = 16
-PATHS = {0: "copy", 1: "onesweep", 2: "local"}
+PATHS = {0: "copy", 1: "lsd", 2: "leaf", 3: "msd"}
 
 _STATUS = {
     0: "LCO_OK", 1: "LCO_ERR_NULL", 2: "LCO_ERR_ORDER", 3: "LCO_ERR_DIM", 4: "LCO_ERR_PERM",
@@ -61,6 +61,9 @@ class PlanInfo(ctypes.Structure):
         ("path", ctypes.c_int),
         ("launches", ctypes.c_int),
         ("tile", ctypes.c_int),
+        ("msd_levels", ctypes.c_int),
+        ("leaf_bits", ctypes.c_int),
+        ("model_bytes", ctypes.c_double),
     ]
 
 
@@ -202,6 +205,9 @@ class Plan:
             "path": PATHS.get(pi.path, pi.path),
             "launches": pi.launches,
             "tile": pi.tile,
+            "msd_levels": pi.msd_levels,
+            "leaf_bits": pi.leaf_bits,
+            "model_bytes": pi.model_bytes,
         }
 
     # ---------------------------------------------------------------- device calls

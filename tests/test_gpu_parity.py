@@ -132,6 +132,47 @@ def test_large_keys_near_limit(cuda_device):
     check(dims, (1, 0), keys, rng.standard_normal(len(keys)))
 
 
+# ------------------------------------------------------------------ MSD schedule
+def test_msd_two_levels_random(cuda_device):
+    """MSD level 1 (8 bits) + segmented level 2 + on-chip leaves (32-bit leaf keys)."""
+    rng = np.random.default_rng(21)
+    dims = (4096,) * 5
+    keys = np.unique(rng.integers(0, 2 ** 60, 2_600_000, dtype=np.int64))[:2_500_000]
+    keys = keys.astype(np.uint64)
+    assert lco.plan(dims, (4, 3, 2, 1, 0)).info(len(keys))["msd_levels"] == 2
+    check(dims, (4, 3, 2, 1, 0), keys, rng.standard_normal(len(keys)))
+    check(dims, (3, 4, 0, 2, 1), keys, rng.standard_normal(len(keys)))
+
+
+def _skewed(rng, n, hot):
+    """Sorted unique keys of 4096^5 whose new-order top modes are nearly constant, so
+    MSD buckets are far larger than a leaf (exercises the streaming leaf fallback)."""
+    c4 = np.full(n, 7)
+    c3 = np.where(rng.random(n) < hot, 9, rng.integers(0, 4096, n))
+    c2 = rng.integers(0, 2, n)
+    c1 = rng.integers(0, 4096, n)
+    c0 = rng.integers(0, 4096, n)
+    k = np.ravel_multi_index((c0, c1, c2, c3, c4), (4096,) * 5)
+    return np.unique(k).astype(np.uint64)
+
+
+@pytest.mark.parametrize("n", [300_000, 3_000_000])
+def test_msd_skewed_oversize_leaves(n, cuda_device):
+    rng = np.random.default_rng(n)
+    keys = _skewed(rng, n, 0.98)
+    vals = rng.standard_normal(len(keys))
+    check((4096,) * 5, (4, 3, 2, 1, 0), keys, vals)
+
+
+def test_sort_msd_with_duplicates(cuda_device):
+    rng = np.random.default_rng(31)
+    dims = (1000, 1000, 1000)
+    keys = rng.integers(0, 10 ** 9, 1_000_000).astype(np.uint64)
+    keys[1::3] = keys[::3][: len(keys[1::3])]  # many duplicates
+    assert lco.plan(dims, (2, 0, 1)).info(len(keys), sort=True)["path"] == "msd"
+    check(dims, (2, 0, 1), keys, rng.standard_normal(len(keys)), sort=True)
+
+
 # ------------------------------------------------------------------ lco_sort
 def test_sort_unsorted_with_duplicates(cuda_device):
     rng = np.random.default_rng(9)

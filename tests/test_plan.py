@@ -89,7 +89,7 @@ def test_plan_stable_sort_on_shaved_key_equals_oracle(order):
             continue
         q = new // np.uint64(info["trailing"])
         assert int(q.max(initial=0)) < 2 ** info["sort_bits"]
-        assert sum(info["digit_bits"]) == info["sort_bits"]
+        assert sum(info["digit_bits"]) + info["leaf_bits"] == info["sort_bits"]
         assert np.array_equal(np.argsort(q, kind="stable"), ep), (dims, perm)
         # the sort plan sorts on every key bit (T = 1)
         si = p.info(nnz, sort=True)
@@ -97,22 +97,36 @@ def test_plan_stable_sort_on_shaved_key_equals_oracle(order):
 
 
 def test_baseline_config_plans():
-    """Key bits the passes sort per BASELINE config (SURVEY.md §8(a) sizes table)."""
+    """Key bits the passes sort per BASELINE config (SURVEY.md §8(a) sizes table) and the
+    schedule chosen at the config's nnz."""
     cases = {
-        ("C1", (64, 48, 32), (2, 0, 1)): (5, 1),
-        ("C2a", (512,) * 4, (2, 3, 0, 1)): (18, 2),
-        ("C2b", (512,) * 4, (0, 2, 1, 3)): (18, 2),
-        ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2)): (21, 2),
-        ("C3b", (128,) * 6, (0, 3, 1, 4, 2, 5)): (28, 3),
-        ("C4", (2048,) * 4, (1, 0, 2, 3)): (11, 1),
-        ("C5", (4096,) * 5, (4, 3, 2, 1, 0)): (48, 5),
+        ("C1", (64, 48, 32), (2, 0, 1), 5000): (5, "lsd"),
+        ("C2a", (512,) * 4, (2, 3, 0, 1), 1308672): (18, "lsd"),
+        ("C2b", (512,) * 4, (0, 2, 1, 3), 1308672): (18, "lsd"),
+        ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2), 14581760): (21, "lsd"),
+        ("C3b", (128,) * 6, (0, 3, 1, 4, 2, 5), 14581760): (28, "lsd"),
+        ("C4", (2048,) * 4, (1, 0, 2, 3), 54484996): (11, "lsd"),
+        ("C5", (4096,) * 5, (4, 3, 2, 1, 0), 500_000_000): (48, "msd"),
     }
-    for (name, dims, perm), (bits, passes) in cases.items():
-        info = lco.Plan(dims, perm).info(1000)
-        assert (info["sort_bits"], info["passes"]) == (bits, passes), (name, info)
-    c4 = lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(10)
+    for (name, dims, perm, nnz), (bits, path) in cases.items():
+        info = lco.Plan(dims, perm).info(nnz)
+        assert (info["sort_bits"], info["path"]) == (bits, path), (name, info)
+        assert sum(info["digit_bits"]) + info["leaf_bits"] == bits
+    c4 = lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54484996)
     assert c4["norm_dims"] == [2048, 2048, 2 ** 22] and c4["norm_perm"] == [1, 0, 2]
-    assert c4["trailing"] == 2048 * 2 ** 22
+    assert c4["trailing"] == 2048 * 2 ** 22 and c4["passes"] == 1
+
+
+def test_call_schedules():
+    """Schedule per nnz: one on-chip leaf when it fits, MSD + leaves for wide keys, LSD
+    otherwise (modelled bytes decide; results are identical)."""
+    p = lco.Plan((4096,) * 5, (4, 3, 2, 1, 0))
+    assert p.info(1000)["path"] == "leaf"
+    i = p.info(500_000_000)
+    assert i["path"] == "msd" and i["msd_levels"] == 2
+    assert sum(i["digit_bits"]) + i["leaf_bits"] == 48
+    assert p.info(200_000)["msd_levels"] == 1
+    assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54_484_996)["path"] == "lsd"
 
 
 def test_identity_and_size1_moves_are_copies():
@@ -138,7 +152,7 @@ def test_workspace_sizes():
     p = lco.Plan((4096,) * 5, (4, 3, 2, 1, 0))
     ws = p.workspace_size(500_000_000)
     # two ping-pong (key, value, position) buffers + two look-back status arrays
-    assert 2 * 20 * 500_000_000 < ws < 2 * 20 * 500_000_000 + 2 * 10 ** 9
+    assert 2 * 20 * 500_000_000 < ws < 2 * 20 * 500_000_000 + 4 * 10 ** 9
     assert lco.Plan((4, 4), (0, 1)).workspace_size(100) < 1 << 20
     assert p.host_workspace_size(10) > p.workspace_size(10)
 
