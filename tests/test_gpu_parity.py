@@ -156,7 +156,7 @@ def _skewed(rng, n, hot):
     return np.unique(k).astype(np.uint64)
 
 
-@pytest.mark.parametrize("n", [300_000, 3_000_000])
+@pytest.mark.parametrize("n", [40_000, 300_000, 3_000_000])
 def test_msd_skewed_oversize_leaves(n, cuda_device):
     rng = np.random.default_rng(n)
     keys = _skewed(rng, n, 0.98)
@@ -195,7 +195,7 @@ def test_sort_equals_permute_on_sorted(cuda_device):
 
 # ------------------------------------------------------------------ BASELINE configs
 @pytest.mark.parametrize("name,scale", [("C1", None), ("C2", 96), ("C3", 20), ("C4", 100),
-                                        ("C5", 300_000)])
+                                        ("C5", 300_000), ("C5", 30_000), ("C5", 1_500)])
 def test_baseline_configs_scaled(name, scale, cuda_device):
     w = workloads.config(name, scale=scale)
     for perm in w.perms:

@@ -1,0 +1,158 @@
+"""Sharded (multi-GPU) orchestration on CPU: world sizes 2 and 3 with the gloo backend.
+
+The device operations are replaced by oracle-backed test doubles (same contracts as
+lco_key_histogram / lco_partition / lco_permute); what is tested is the orchestration of
+paper_1802_02619_b200.sharded: global index bases, splitter choice from the all-reduced
+histogram, count and payload all_to_all, concatenation order, and that the per-rank
+outputs concatenate to the single-device oracle result bit for bit (SURVEY.md §8(e),
+DESIGN.md "Multi-GPU")."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_1802_02619_b200 import sharded
+
+
+class OracleOps:
+    def __init__(self, dims, perm):
+        self.dims, self.perm = tuple(dims), tuple(perm)
+
+    def key_histogram(self, keys, bits):
+        kb = sharded.key_bits(self.dims)
+        new = oracle.shuffle(self.dims, self.perm, keys.numpy().view(np.uint64))
+        b = (new >> np.uint64(max(0, kb - bits))).astype(np.int64)
+        return torch.from_numpy(np.bincount(b, minlength=1 << bits).astype(np.int64))
+
+    def partition(self, keys, vals, idx_base, splitters):
+        spl = np.zeros(0, np.uint64) if splitters is None else splitters.numpy().view(np.uint64)
+        sk, sv, si, cnt = oracle.partition(self.dims, self.perm, keys.numpy().view(np.uint64),
+                                           vals.numpy(), idx_base, spl)
+        return (torch.from_numpy(sk.view(np.int64)), torch.from_numpy(sv),
+                torch.from_numpy(si.view(np.int32)), torch.from_numpy(cnt.astype(np.int64)))
+
+    def permute(self, keys, vals, idx):
+        ko, vo, po = oracle.permute(self.dims, self.perm, keys.numpy().view(np.uint64),
+                                    vals.numpy(), idx.numpy().view(np.uint32))
+        return (torch.from_numpy(ko.view(np.int64)), torch.from_numpy(vo),
+                torch.from_numpy(po.view(np.int32)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, dims, perm, keys, vals, cuts, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = cuts[rank], cuts[rank + 1]
+    k = torch.from_numpy(keys[lo:hi].view(np.int64).copy())
+    v = torch.from_numpy(vals[lo:hi].copy())
+    ko, vo, po = sharded.permute_sharded(k, v, dims, perm, ops=OracleOps(dims, perm), bits=6)
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), k=ko.numpy(), v=vo.numpy(), p=po.numpy())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims,perm,nnz,uneven", [
+    (2, (64, 48, 32), (2, 0, 1), 5000, False),
+    (2, (16, 16, 16, 16), (3, 1, 2, 0), 20000, True),
+    (3, (40, 30, 20), (1, 2, 0), 7000, True),
+])
+def test_sharded_matches_single_device(world, dims, perm, nnz, uneven, tmp_path):
+    rng = np.random.default_rng(nnz)
+    total = int(np.prod(dims))
+    keys = np.sort(rng.choice(total, nnz, replace=False)).astype(np.uint64)
+    vals = rng.standard_normal(nnz)
+    if uneven:  # one rank gets a small slice, another a large one
+        cuts = [0] + sorted(rng.choice(np.arange(1, nnz), world - 1, replace=False).tolist()) + [nnz]
+        cuts[1] = min(cuts[1], 17)
+        cuts = sorted(cuts)
+    else:
+        cuts = [nnz * r // world for r in range(world + 1)]
+    mp.spawn(_worker, args=(world, _free_port(), dims, perm, keys, vals, cuts, str(tmp_path)),
+             nprocs=world, join=True)
+    parts = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
+    ko = np.concatenate([p["k"] for p in parts]).view(np.uint64)
+    vo = np.concatenate([p["v"] for p in parts])
+    po = np.concatenate([p["p"] for p in parts]).view(np.uint32)
+    ek, ev, ep = oracle.permute(dims, perm, keys, vals)
+    assert np.array_equal(ko, ek) and np.array_equal(po, ep)
+    assert np.array_equal(vo.view(np.uint64), ev.view(np.uint64))
+    # every rank owns a contiguous new-key range and the load is spread
+    sizes = [len(p["k"]) for p in parts]
+    assert sum(sizes) == nnz
+
+
+def test_choose_splitters_quantiles():
+    h = torch.tensor([10, 0, 30, 0, 0, 60, 0, 0], dtype=torch.int64)
+    spl = sharded.choose_splitters(h, 2, kbits=6, bits=3)
+    below = int(h[: spl[0] >> 3].sum())
+    assert below == 40  # 40 / 60 is the split closest to the median
+    assert sharded.choose_splitters(h, 1, 6, 3) == []
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_virtual_ranks_cuda(world, cuda_device):
+    """The CUDA kernels of the sharded path, ranks emulated one after another on one GPU
+    (no rank waits on another): key histogram -> splitters -> lco_partition per slice ->
+    per-destination concatenation in source order -> lco_permute(idx_in)."""
+    import paper_1802_02619_b200 as lco
+    import workloads
+    w = workloads.config("C5", scale=400_000, device=cuda_device)
+    dims, perm = w.dims, w.perms[0]
+    p = lco.plan(dims, perm)
+    n = w.keys.numel()
+    cuts = [n * r // world for r in range(world + 1)]
+    kb = sharded.key_bits(dims)
+    hist = sum(p.key_histogram(w.keys[cuts[r]:cuts[r + 1]], 12) for r in range(world))
+    spl = torch.tensor(sharded.choose_splitters(hist, world, kb, 12), dtype=torch.int64,
+                       device=cuda_device)
+    sends = [p.partition(w.keys[cuts[r]:cuts[r + 1]], w.vals[cuts[r]:cuts[r + 1]], cuts[r], spl)
+             for r in range(world)]
+    outs = []
+    for dst in range(world):
+        ks, vs, ix = [], [], []
+        for src in range(world):
+            sk, sv, si, cnt = sends[src]
+            off = int(cnt[:dst].sum())
+            c = int(cnt[dst])
+            ks.append(sk[off:off + c]); vs.append(sv[off:off + c]); ix.append(si[off:off + c])
+        outs.append(p.permute(torch.cat(ks), torch.cat(vs), torch.cat(ix)))
+    torch.cuda.synchronize()
+    ko = torch.cat([o[0] for o in outs]).cpu().numpy().view(np.uint64)
+    vo = torch.cat([o[1] for o in outs]).cpu().numpy()
+    po = torch.cat([o[2] for o in outs]).cpu().numpy().view(np.uint32)
+    ek, ev, ep = oracle.permute(dims, perm, w.keys.cpu().numpy().view(np.uint64), w.vals.cpu().numpy())
+    assert np.array_equal(ko, ek) and np.array_equal(po, ep)
+    assert np.array_equal(vo.view(np.uint64), ev.view(np.uint64))
+    sizes = [o[0].numel() for o in outs]
+    assert max(sizes) < 1.2 * n / world  # splitters balance uniform keys
+
+
+@pytest.mark.gpu
+def test_permute_sharded_world1_nccl(cuda_device, tmp_path):
+    """permute_sharded end to end through NCCL with a single rank."""
+    import workloads
+    w = workloads.config("C5", scale=100_000, device=cuda_device)
+    store = dist.FileStore(str(tmp_path / "store"), 1)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=cuda_device)
+    try:
+        ko, vo, po = sharded.permute_sharded(w.keys, w.vals, w.dims, w.perms[0])
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+    ek, ev, ep = oracle.permute(w.dims, w.perms[0], w.keys.cpu().numpy().view(np.uint64),
+                                w.vals.cpu().numpy())
+    assert np.array_equal(ko.cpu().numpy().view(np.uint64), ek)
+    assert np.array_equal(po.cpu().numpy().view(np.uint32), ep)
