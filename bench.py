@@ -36,12 +36,19 @@ UNIT = "nonzeros/s"
 # Algorithmic bytes per nonzero of each kernel: the bytes the
 # kernel must move at minimum for the work it does (reads + writes, perm included).
 KERNEL_BYTES = {
-    "k_hist": 8,           # read K
-    "k_pass_first": 20,    # read K; write K', position
-    "k_pass_mid": 24,      # read K', position; write K', position
-    "k_pass_last": 40,     # read K', position, V (gather); write K', V, perm
-    "k_pass_single": 36,   # read K, V; write K', V, perm
-    "k_copy": 36,          # read K, V; write K, V, perm
+    "k_count_first": 8,       # read K (LIV shuffle + digit histogram)
+    "k_count": 8,             # read K'
+    "k_count_seg": 8,         # read K'
+    "k_scatter_first": 36,    # read K, V; write K', V, position
+    "k_scatter_single": 36,   # read K, V; write K', V, perm
+    "k_scatter_mid": 40,      # read K', V, position; write them
+    "k_scatter_seg": 40,
+    "k_scatter_last": 40,
+    "k_leafw": 40,            # read K', V, position; write K', V, perm (final)
+    "k_leafw_l1": 40,
+    "k_leaf": 36,
+    "k_leaf_deferred": 40,
+    "k_copy": 36,             # read K, V; write K, V, perm
     "k_partition": 36,
 }
 STEP_BYTES = 36  # read K+V, write K'+V (32) + the uint32 perm (4)

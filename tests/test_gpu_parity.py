@@ -165,12 +165,15 @@ def test_msd_skewed_oversize_leaves(n, cuda_device):
 
 
 def test_sort_msd_with_duplicates(cuda_device):
+    """lco_sort of unsorted keys with many duplicates through the MSD schedule: equal
+    keys keep input order."""
     rng = np.random.default_rng(31)
-    dims = (1000, 1000, 1000)
-    keys = rng.integers(0, 10 ** 9, 1_000_000).astype(np.uint64)
+    dims = (4096,) * 5
+    keys = rng.integers(0, 2 ** 60, 1_000_000, dtype=np.int64).astype(np.uint64)
     keys[1::3] = keys[::3][: len(keys[1::3])]  # many duplicates
-    assert lco.plan(dims, (2, 0, 1)).info(len(keys), sort=True)["path"] == "msd"
-    check(dims, (2, 0, 1), keys, rng.standard_normal(len(keys)), sort=True)
+    perm = (2, 0, 1, 4, 3)
+    assert lco.plan(dims, perm).info(len(keys), sort=True)["path"] == "msd"
+    check(dims, perm, keys, rng.standard_normal(len(keys)), sort=True)
 
 
 # ------------------------------------------------------------------ lco_sort
