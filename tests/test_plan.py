@@ -125,7 +125,7 @@ def test_call_schedules():
     i = p.info(500_000_000)
     assert i["path"] == "msd" and i["msd_levels"] == 2
     assert sum(i["digit_bits"]) + i["leaf_bits"] == 48
-    assert p.info(60_000)["msd_levels"] == 1
+    assert p.info(40_000)["msd_levels"] == 1
     assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54_484_996)["path"] == "lsd"
 
 
