@@ -507,10 +507,11 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(const __grid_constant__ L
 // list for the block-level k_leaf.  Leaf descriptors are fetched 32 at a time (one per
 // lane).
 // ---------------------------------------------------------------------------------
-constexpr int kWCap = 512;
+constexpr int kWCap = 384;
 constexpr int kWBucketBits = 9;
 constexpr int kWWarps = 8;  // warps per CTA
-constexpr size_t kWWarpBytes = (size_t)kWCap * (8 + 8 + 4 + 2) + ((size_t)1 << kWBucketBits) * 4;
+constexpr size_t kWWarpBytes =
+    (size_t)kWCap * (8 + 8 + 4 + 2 + 2 + 8) + ((size_t)1 << kWBucketBits) * 4;
 
 uint32_t leaf_target() { return kWCap / 2; }
 
@@ -522,8 +523,10 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
   uint64_t* K = reinterpret_cast<uint64_t*>(base);
   double* V = reinterpret_cast<double*>(base + kWCap * 8);
   uint32_t* P = reinterpret_cast<uint32_t*>(base + kWCap * 16);
-  uint16_t* X = reinterpret_cast<uint16_t*>(base + kWCap * 20);
-  uint32_t* B = reinterpret_cast<uint32_t*>(base + kWCap * 22);
+  uint16_t* X = reinterpret_cast<uint16_t*>(base + kWCap * 20);   // bucket order
+  uint16_t* F = reinterpret_cast<uint16_t*>(base + kWCap * 22);   // final order
+  uint64_t* RK = reinterpret_cast<uint64_t*>(base + kWCap * 24);  // sort key, bucket order
+  uint32_t* B = reinterpret_cast<uint32_t*>(base + kWCap * 32);
   const bool want_pos = L.perm_out != nullptr;
   const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
   const int level = L.only_level;
@@ -585,29 +588,31 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
         }
       }
       __syncwarp();
-      for (uint32_t i = lane; i < n; i += 32)
-        X[atomicAdd(&B[(uint32_t)(leaf_key(L, K[i], mask) >> bshift)], 1u)] = (uint16_t)i;
+      for (uint32_t i = lane; i < n; i += 32) {
+        const uint64_t k = leaf_key(L, K[i], mask);
+        const uint32_t slot = atomicAdd(&B[(uint32_t)(k >> bshift)], 1u);
+        X[slot] = (uint16_t)i;
+        RK[slot] = k;
+      }
       __syncwarp();
+      // B[b] is now the end of bucket b.  Every lane ranks one element inside its
+      // (small) bucket by counting smaller (key, index) pairs: no divergent insertion.
       bool big = false;
-      for (uint32_t b = lane; b < nbk; b += 32) {  // B[b] = end of bucket b
+      for (uint32_t p = lane; p < n; p += 32) {
+        const uint64_t k = RK[p];
+        const uint16_t x = X[p];
+        const uint32_t b = (uint32_t)(k >> bshift);
         const uint32_t lo = b ? B[b - 1] : 0u, hi = B[b];
         if (hi - lo > (uint32_t)kSmallBucket) {
           big = true;
-        } else {
-          for (uint32_t i = lo + 1; i < hi; ++i) {
-            const uint16_t x = X[i];
-            const uint64_t k = leaf_key(L, K[x], mask);
-            uint32_t j = i;
-            while (j > lo) {
-              const uint16_t y = X[j - 1];
-              const uint64_t ky = leaf_key(L, K[y], mask);
-              if (ky < k || (ky == k && y < x)) break;
-              X[j] = y;
-              --j;
-            }
-            X[j] = x;
-          }
+          continue;
         }
+        uint32_t r = lo;
+        for (uint32_t j = lo; j < hi; ++j) {
+          const uint64_t kj = RK[j];
+          r += (kj < k || (kj == k && X[j] < x)) ? 1u : 0u;
+        }
+        F[r] = x;
       }
       if (__any_sync(0xffffffffu, big)) {  // skewed leaf: the block kernel sorts it
         const uint32_t slot = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)myslot, l);
@@ -617,7 +622,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
       }
       __syncwarp();
       for (uint32_t j = lane; j < n; j += 32) {
-        const uint16_t e = X[j];
+        const uint16_t e = F[j];
         const uint64_t g = (uint64_t)start + j;
         L.keys_out[g] = K[e];
         if (VALS) L.vals_out[g] = V[e];
