@@ -133,6 +133,21 @@ __device__ __forceinline__ uint32_t digit_new(const PassParams& a, uint64_t k2) 
   return digit_of(a.kp, q_of(a, k2), a.pass);
 }
 
+// Digit extraction with the per-pass shift hoisted: for T a power of two the digit is a
+// single shift-and-mask of K'.
+struct DigitFn {
+  int sh;         // >= 0: digit = (K' >> sh) & mask
+  uint32_t mask;
+  __device__ __forceinline__ DigitFn(const PassParams& a) {
+    mask = (1u << a.kp.dbits[a.pass]) - 1u;
+    sh = (a.qshift >= 0 && !a.splitters) ? a.qshift + a.kp.dshift[a.pass] : -1;
+  }
+  __device__ __forceinline__ uint32_t operator()(const PassParams& a, uint64_t k2) const {
+    if (sh >= 0) return (uint32_t)(k2 >> sh) & mask;
+    return digit_new(a, k2);
+  }
+};
+
 // Element range of tile t; false if t is past the end of a segmented table.
 __device__ __forceinline__ bool tile_range(const PassParams& a, uint32_t t, uint64_t* base,
                                            uint32_t* n, uint32_t* seg) {

@@ -70,20 +70,25 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   uint32_t n, seg;
   if (!tile_range(a, t, &base, &n, &seg)) return;
   for (int i = tid; i < BINS; i += kThreads) h[i] = 0;
-  uint64_t k[kItems];
-#pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
-    k[it] = pos < n ? __ldcs(keys + base + pos) : 0ull;
-  }
+  const DigitFn dg(a);
   __syncthreads();
+  constexpr int H = kItems / 2;  // two rounds of 8 keys keep the registers low
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
-    const bool ok = pos < n;
-    // plain shared atomics: a histogram needs no order (conflicting lanes of a warp are
-    // serialized by the hardware, which only costs on long runs of equal digits)
-    if (ok) atomicAdd(&h[digit_new(a, FIRST ? reencode(a.kp, k[it]) : k[it])], 1u);
+  for (int half = 0; half < 2; ++half) {
+    uint64_t k[H];
+#pragma unroll
+    for (int it = 0; it < H; ++it) {
+      const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
+      k[it] = pos < n ? __ldcs(keys + base + pos) : 0ull;
+    }
+    if (FIRST) reencode_n<H>(a.kp, k);  // LIV shuffle
+#pragma unroll
+    for (int it = 0; it < H; ++it) {
+      const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
+      // plain shared atomics: a histogram needs no order (conflicting lanes of a warp
+      // are serialized by the hardware, which only costs on long runs of equal digits)
+      if (pos < n) atomicAdd(&h[dg(a, k[it])], 1u);
+    }
   }
   __syncthreads();
   uint16_t* row = thist + (size_t)t * BINS;
@@ -211,18 +216,31 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int d = tid + b * kThreads;
     if (d < BINS) gbase[d] = __ldcs(io.toff + (size_t)t * BINS + d);
   }
+  {
+    const DigitFn dg(a);
+    if (FIRST && io.keep_old_key) {  // partition: route by K', move the old key
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
-    if (pos < n) {
-      uint64_t k2 = key[it];
-      if (FIRST) {
-        k2 = reencode(a.kp, k2);  // LIV shuffle
-        if (!io.keep_old_key) key[it] = k2;
+      for (int it = 0; it < kItems; ++it) {
+        const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+        meta[it] = pos < n ? dg(a, reencode(a.kp, key[it])) : kInvalid;
       }
-      meta[it] = digit_new(a, k2);
     } else {
-      meta[it] = kInvalid;
+      if (FIRST) {  // LIV shuffle, in place, two rounds of 8 keys
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint64_t kk[kItems / 2];
+#pragma unroll
+          for (int i = 0; i < kItems / 2; ++i) kk[i] = key[half * (kItems / 2) + i];
+          reencode_n<kItems / 2>(a.kp, kk);
+#pragma unroll
+          for (int i = 0; i < kItems / 2; ++i) key[half * (kItems / 2) + i] = kk[i];
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < kItems; ++it) {
+        const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+        meta[it] = pos < n ? dg(a, key[it]) : kInvalid;
+      }
     }
   }
   __syncthreads();

@@ -64,6 +64,7 @@ struct KeyPlan {
   uint8_t oshift[kMaxModes];      // pow2: bit offset of mode m in the old key
   uint8_t nshift[kMaxModes];      // pow2: bit offset of mode m in the new key
   uint8_t width[kMaxModes];       // pow2: log2 n_m
+  uint64_t omask[kMaxModes];      // pow2: n_m - 1
   int passes;                     // P
   int dshift[kMaxPasses];         // digit j = (q >> dshift[j]) & ((1 << dbits[j]) - 1)
   int dbits[kMaxPasses];
@@ -87,6 +88,44 @@ LCO_HD uint64_t reencode(const KeyPlan& p, uint64_t k) {
     k = q;
   }
   return out + k * p.nstride[0];
+}
+
+// LIV shuffle of N keys at once: the loop over modes is outermost so each mode's
+// constants are read once per thread and applied to every item.
+template <int N>
+LCO_HD void reencode_n(const KeyPlan& p, uint64_t (&k)[N]) {
+  if (p.pow2) {
+    uint64_t out[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) out[i] = 0;
+#pragma unroll 1
+    for (int m = 0; m < p.n; ++m) {
+      const int os = p.oshift[m], ns = p.nshift[m];
+      const uint64_t mk = p.omask[m];
+#pragma unroll
+      for (int i = 0; i < N; ++i) out[i] |= ((k[i] >> os) & mk) << ns;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) k[i] = out[i];
+    return;
+  }
+  uint64_t out[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) out[i] = 0;
+#pragma unroll 1
+  for (int m = p.n - 1; m > 0; --m) {
+    const FastDiv f = p.div[m];
+    const uint64_t dm = p.dim[m], st = p.nstride[m];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const uint64_t q = fdiv(f, k[i]);
+      out[i] += (k[i] - q * dm) * st;
+      k[i] = q;
+    }
+  }
+  const uint64_t s0 = p.nstride[0];
+#pragma unroll
+  for (int i = 0; i < N; ++i) k[i] = out[i] + k[i] * s0;
 }
 
 LCO_HD uint32_t digit_of(const KeyPlan& p, uint64_t q, int pass) {

@@ -104,6 +104,7 @@ static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64
     int acc_old = 0;
     for (int m = n - 1; m >= 0; --m) {
       kp.width[m] = (uint8_t)__builtin_ctzll(nd[m]);
+      kp.omask[m] = nd[m] - 1;
       kp.oshift[m] = (uint8_t)acc_old;
       acc_old += kp.width[m];
     }
