@@ -16,7 +16,14 @@ __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) {
 constexpr int kThreads = 256;  // k_scatter / k_count CTA size (8 warps)
 constexpr int kItems = 16;     // nonzeros per thread per tile
 constexpr int kTile = kThreads * kItems;
-constexpr int kChunkTiles = 64;  // tiles per scan chunk
+constexpr int kChunkTiles = 64;  // max tiles per scan chunk
+
+// Tiles per scan chunk: up to 64, fewer for small inputs so that k_offsets' running
+// sums stay short and there are enough chunks to fill the GPU.
+__host__ __device__ __forceinline__ uint32_t chunk_tiles(uint32_t tiles) {
+  uint32_t c = tiles / 512;
+  return c < 4 ? 4u : (c > (uint32_t)kChunkTiles ? (uint32_t)kChunkTiles : c);
+}
 constexpr int kScanThreads = 256;
 constexpr uint32_t kInvalid = 0xFFFFu;
 
@@ -117,6 +124,7 @@ struct PassParams {
   uint64_t nnz;
   uint32_t tiles;
   uint32_t nchunks;
+  uint32_t ctiles;            // tiles per scan chunk
   const uint64_t* splitters;  // partition mode: digit = destination rank
   int world;
   const TileEntry* ttab;      // segmented mode: tile table (else tiles are t * kTile)
@@ -161,7 +169,7 @@ __device__ __forceinline__ bool tile_range(const PassParams& a, uint32_t t, uint
   }
   *base = (uint64_t)t * kTile;
   *n = (uint32_t)umin64(kTile, a.nnz - *base);
-  *seg = t / kChunkTiles;
+  *seg = t / a.ctiles;
   return true;
 }
 

@@ -3,7 +3,7 @@
 // One stable radix pass over a digit of the shaved key q = K' div T is a
 // tile-granular reduce-then-scan:
 //   k_count    per tile (4096 nonzeros): LIV shuffle on the first pass,
-//              digit, tile histogram (row of thist) and, per chunk of kChunkTiles tiles,
+//              digit, tile histogram (row of thist) and, per chunk of tiles,
 //              the chunk sums;
 //   k_scan     per digit, exclusive scan of the chunk sums; the last CTA turns the digit
 //              totals into bucket starts;
@@ -54,7 +54,7 @@ __global__ void k_copy(uint64_t nnz, const uint64_t* __restrict__ keys_in,
 
 // ---------------------------------------------------------------------------------
 // k_count: one tile per CTA: tile histogram -> thist[t][BINS] (uint16) and added into
-// its chunk's sums csum[t / kChunkTiles][BINS] (segmented mode: into its segment's
+// its chunk's sums csum[t / ctiles][BINS] (segmented mode: into its segment's
 // totals csum[seg][BINS]); csum is zeroed by the launcher.
 // ---------------------------------------------------------------------------------
 template <int RB, bool FIRST>
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ Pa
                                                       uint32_t* __restrict__ toff) {
   constexpr int BINS = 1 << RB;
   const uint32_t c = blockIdx.x;
-  const uint32_t t0 = c * kChunkTiles, t1 = min(a.tiles, t0 + kChunkTiles);
+  const uint32_t t0 = c * a.ctiles, t1 = min(a.tiles, t0 + a.ctiles);
   for (int d = threadIdx.x; d < BINS; d += kThreads) {
     uint32_t run = __ldg(bucket + d) + __ldcg(csum + (size_t)c * BINS + d);
     for (uint32_t t = t0; t < t1; ++t) {
@@ -409,7 +409,7 @@ int pass_rb(int bits) { return bits <= 8 ? 8 : (bits <= 10 ? 10 : 11); }
 //                | totals | bucket | counter
 size_t pass_ctrl_bytes(int rb, uint64_t nnz) {
   const uint64_t tiles = pass_tiles(nnz);
-  const uint64_t chunks = (tiles + kChunkTiles - 1) / kChunkTiles;
+  const uint64_t chunks = (tiles + chunk_tiles((uint32_t)tiles) - 1) / chunk_tiles((uint32_t)tiles);
   const size_t bins = (size_t)1 << rb;
   return (tiles * bins * 2 + 255) / 256 * 256 + tiles * bins * 4 + (chunks + 2) * bins * 4 + 512;
 }
@@ -417,7 +417,7 @@ size_t pass_ctrl_bytes(int rb, uint64_t nnz) {
 PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl) {
   PassCtrl c;
   const uint32_t tiles = (uint32_t)pass_tiles(nnz);
-  const uint32_t nchunks = (tiles + kChunkTiles - 1) / kChunkTiles;
+  const uint32_t nchunks = (tiles + chunk_tiles(tiles) - 1) / chunk_tiles(tiles);
   const size_t bins = (size_t)1 << rb;
   char* cb = reinterpret_cast<char*>(ctrl);
   c.thist = reinterpret_cast<uint16_t*>(cb);
@@ -512,6 +512,7 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
   a.pass = j;
   a.tiles = c.tiles;
   a.nchunks = c.nchunks;
+  a.ctiles = chunk_tiles(c.tiles);
   cudaError_t e;
   const bool part = io.splitters != nullptr;
   if ((e = cudaMemsetAsync(c.csum, 0, ((size_t)c.nchunks * BINS + 2 * BINS) * 4 + 4, L.stream)) !=
