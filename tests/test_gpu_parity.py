@@ -330,3 +330,13 @@ def test_alias_rejected(cuda_device):
     k = torch.arange(10, dtype=torch.int64, device=cuda_device)
     with pytest.raises(ValueError, match="ALIAS"):
         p.permute(k, out=(k, None, None))
+
+
+def test_combinatorial_laplacian_all_perms(cuda_device):
+    """PAPER.md Eq (2.3) pattern (non-power-of-two N, as P:207 and P:526 use 2^k - 1),
+    all 23 permutations, permute and sort both against the oracle (Table 2 workload)."""
+    k, v = workloads.combinatorial_laplacian(63)
+    keys, vals = _np_u64(k), v.numpy()
+    for perm in itertools.permutations(range(4)):
+        check((63,) * 4, perm, keys, vals)
+        check((63,) * 4, perm, keys, vals, sort=True)

@@ -156,6 +156,22 @@ def biharmonic_2d13(n, device="cpu"):
     return _stencil(n, 2, offs, device)
 
 
+def combinatorial_laplacian(n, device="cpu"):
+    """Support pattern of the order-4 combinatorial Laplacian of PAPER.md Eq (2.3),
+    a_ijkl = d(y)_ii' delta_jl d(y)_i'k + d(x)_jj' delta_ik d(x)_j'l, with d the
+    central-difference FD matrix of Eq (2.1): d.d couples offsets {-2, 0, +2}, so each
+    (i, j) has the neighbours (i+-2, j), (i, j+-2) and itself (5 N^2 nonzeros in the
+    interior).  Built in sorted order with Dirichlet truncation (the one-sided boundary
+    rows of Eq 2.1 change only the values near the edges; values are only moved)."""
+    offs = [((-2, 0), 0.25), ((0, -2), 0.25), ((0, 0), -1.0), ((0, 2), 0.25), ((2, 0), 0.25)]
+    return _stencil(n, 2, offs, device)
+
+
+def fill_tensor(n, fill, seed, device="cpu"):
+    """Order-4 n^4 tensor with a constant fill factor (PAPER.md:261 '2% fill')."""
+    return random_tensor((n,) * 4, int(round(fill * n ** 4)), seed, "uniform", device)
+
+
 @dataclass
 class Workload:
     name: str
