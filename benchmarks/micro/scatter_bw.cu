@@ -1,0 +1,112 @@
+// Microbenchmark: achieved HBM bandwidth of scatter write patterns on B200 (sm_100a).
+// A (key, value) stream of N records is moved to a bucketed layout: record j of tile t
+// (4096 records) goes to bucket j % B, after the records of earlier tiles in that
+// bucket -- the write pattern of one radix pass with B digits of uniformly spread keys.
+//   copy        out[i] = in[i] (the copy roofline of the same bytes)
+//   direct      each thread stores its record straight to its destination
+//   staged      the tile is reordered in shared memory, then runs are stored
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scatter_bw scatter_bw.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+constexpr int TILE = 4096;
+
+__device__ __forceinline__ uint64_t dest_of(uint64_t i, uint64_t N, int B) {
+  const uint64_t t = i / TILE, j = i % TILE;
+  const uint64_t per = TILE / B;  // records per bucket per tile
+  return (j % B) * (N / B) + t * per + j / B;
+}
+
+__global__ void k_copy(uint64_t N, const uint64_t* __restrict__ k, const double* __restrict__ v,
+                       uint64_t* __restrict__ ko, double* __restrict__ vo) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x) {
+    ko[i] = __ldcs(k + i);
+    vo[i] = __ldcs(v + i);
+  }
+}
+
+template <int IPT>
+__global__ void __launch_bounds__(256) k_direct(uint64_t N, int B, const uint64_t* __restrict__ k,
+                                                const double* __restrict__ v, uint64_t* __restrict__ ko,
+                                                double* __restrict__ vo) {
+  const uint64_t base = (uint64_t)blockIdx.x * 256 * IPT;
+  uint64_t kk[IPT];
+  double vv[IPT];
+#pragma unroll
+  for (int it = 0; it < IPT; ++it) {
+    const uint64_t i = base + it * 256 + threadIdx.x;
+    kk[it] = i < N ? __ldcs(k + i) : 0;
+    vv[it] = i < N ? __ldcs(v + i) : 0;
+  }
+#pragma unroll
+  for (int it = 0; it < IPT; ++it) {
+    const uint64_t i = base + it * 256 + threadIdx.x;
+    if (i < N) {
+      const uint64_t d = dest_of(i, N, B);
+      ko[d] = kk[it];
+      vo[d] = vv[it];
+    }
+  }
+}
+
+// Reads are coalesced tile loads (kept alive through a checksum); writes go to the
+// bucketed destinations in output-slot order (runs of TILE/B records), no shared
+// memory, so only the HBM write pattern differs from a copy.
+__global__ void __launch_bounds__(256, 2) k_pattern(uint64_t N, int B, const uint64_t* __restrict__ k,
+                                                    const double* __restrict__ v, uint64_t* __restrict__ ko,
+                                                    double* __restrict__ vo, uint64_t pad) {
+  const uint64_t tile = blockIdx.x;
+  const uint64_t base = tile * TILE;
+  const int per = TILE / B;
+  uint64_t acc = 0;
+  double vacc = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    acc += __ldcs(k + base + r * 256 + threadIdx.x);
+    vacc += __ldcs(v + base + r * 256 + threadIdx.x);
+  }
+#pragma unroll 4
+  for (int p = threadIdx.x; p < TILE; p += 256) {
+    const uint64_t d = (uint64_t)(p / per) * (N / B + pad) + tile * per + p % per;
+    ko[d] = acc + p;
+    vo[d] = vacc + p;
+  }
+}
+
+int main() {
+  const uint64_t N = 256ull << 20;  // 256 Mi records: 4 GiB in, 4 GiB out
+  uint64_t *k, *ko;
+  double *v, *vo;
+  cudaMalloc(&k, N * 8);
+  cudaMalloc(&v, N * 8);
+  cudaMalloc(&ko, N * 8 + (64ull << 20));
+  cudaMalloc(&vo, N * 8 + (64ull << 20));
+  cudaMemset(k, 1, N * 8);
+  cudaMemset(v, 2, N * 8);
+
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto time = [&](const char* name, int B, auto launch) {
+    for (int w = 0; w < 2; ++w) launch();
+    cudaEventRecord(e0);
+    const int R = 5;
+    for (int r = 0; r < R; ++r) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= R;
+    printf("%-10s B=%6d  %8.3f ms  %7.1f GB/s  err=%s\n", name, B, ms, 32.0 * N / ms / 1e6,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  time("copy", 0, [&] { k_copy<<<148 * 8, 512>>>(N, k, v, ko, vo); });
+  for (uint64_t pad : {0ull, 40ull}) {
+    printf("pad %llu records between buckets\n", (unsigned long long)pad);
+    for (int B : {1, 4, 16, 64, 256, 1024, 2048, 4096}) {
+      time("pattern", B, [&] { k_pattern<<<N / TILE, 256>>>(N, B, k, v, ko, vo, pad); });
+    }
+  }
+  return 0;
+}

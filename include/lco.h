@@ -178,6 +178,8 @@ typedef struct lco_plan_info {
   int tile;                            /* nonzeros per tile (CTA) */
   int msd_levels;                      /* path 3: MSD passes before the leaves */
   int leaf_bits;                       /* paths 2/3: bits of q the leaf sorts handle */
+  int leaf_kind;                       /* paths 2/3: 1 one warp per leaf (<= 384 nonzeros),
+                                          2 one CTA per leaf (<= 8192 nonzeros) */
   double model_bytes;                  /* modelled HBM bytes per nonzero of the plan */
 } lco_plan_info;
 LCO_API lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* info);

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -65,33 +66,34 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   c.rb = op.radix_bits;
   c.cost = 4 + 48.0 * op.passes;
   if (B <= 11) return c;
-  // MSD digits: enough bits that the expected leaf is <= leaf_target() nonzeros (one
-  // warp sorts it on chip); level 1 prefers 8 bits (cheapest global pass).
+  // MSD levels of 8-bit digits (a 4,096-nonzero tile then writes runs of ~16 nonzeros
+  // per digit, which the HBM write path sustains; 10-11-bit digits write runs of 2-4 and
+  // ran at half the bandwidth, benchmarks/micro/scatter_bw.cu), then one on-chip sort per
+  // leaf: by a warp when the expected leaf is <= leaf_target(), else by a CTA (<= 8K).
   MsdPlan m;
   memset(&m, 0, sizeof m);
-  const uint64_t target = leaf_target();
+  const uint64_t wt = leaf_target();
+  const uint64_t ct = cta_leaf_cap() * 15 / 16;  // expected size, ~4 sigma below the cap
   double mcost;
-  if ((nnz >> 8) <= target || (B <= 18 && (nnz >> 10) <= target)) {
+  if ((nnz >> 8) <= ct) {
     m.levels = 1;
-    m.b1 = ((nnz >> 8) <= target || B < 10) ? 8 : 10;
-    if (m.b1 > B) m.b1 = B;
-    m.rb = B - m.b1;
+    m.b1 = B < 8 ? B : 8;
+    m.b2 = 0;
+    m.cta = (nnz >> m.b1) > wt;
     mcost = 8 + 36 + 40;
   } else {
-    static const int cands[4][2] = {{8, 8}, {8, 10}, {8, 11}, {10, 11}};
-    int k = 3;
-    for (int i = 0; i < 4; ++i)
-      if ((nnz >> (cands[i][0] + cands[i][1])) <= target) {
-        k = i;
-        break;
-      }
     m.levels = 2;
-    m.b1 = cands[k][0];
-    m.b2 = cands[k][1];
+    m.b1 = 8;
+    m.b2 = 8;
+    while (m.b2 < 11 && (nnz >> (m.b1 + m.b2)) > ct) ++m.b2;
     if (m.b1 + m.b2 > B) m.b2 = B - m.b1;  // B >= 12 here, so b2 >= 4
-    m.rb = B - m.b1 - m.b2;
+    m.cta = (nnz >> (m.b1 + m.b2)) > wt;
     mcost = 8 + 36 + 8 + 40 + 40;
   }
+  if (getenv("LCO_MSD_B1")) m.b1 = atoi(getenv("LCO_MSD_B1"));  // experiment hooks
+  if (getenv("LCO_MSD_B2")) m.b2 = atoi(getenv("LCO_MSD_B2"));
+  if (getenv("LCO_MSD_CTA")) m.cta = atoi(getenv("LCO_MSD_CTA"));
+  m.rb = B - m.b1 - m.b2;
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
   // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
   // and with a clear modelled win.
@@ -107,6 +109,7 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
       c.kp.dshift[1] = B - m.b1 - m.b2;
       c.kp.dbits[1] = m.b2;
     }
+    build_digit_moves(&c.kp);
   }
   return c;
 }
@@ -572,13 +575,14 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   info->tile = cp.path == kPathOnesweep || cp.path == kPathMsd ? pass_tile() : 0;
   info->msd_levels = cp.msd.levels;
   info->leaf_bits = cp.path == kPathMsd || cp.path == kPathLocal ? cp.msd.rb : 0;
+  info->leaf_kind = cp.path == kPathLocal ? 2 : (cp.path == kPathMsd ? (cp.msd.cta ? 2 : 1) : 0);
   info->model_bytes = cp.cost;
   // kernels of this library per call (cudaMemsetAsync not counted)
   int launches = 0;
   if (nnz > 0) {
     if (cp.path == kPathCopy || cp.path == kPathLocal) launches = 1;
     else if (cp.path == kPathOnesweep) launches = 4 * cp.passes;
-    else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 1;
+    else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 2;  // passes, leaves, deferred
   }
   info->launches = launches;
   return LCO_OK;

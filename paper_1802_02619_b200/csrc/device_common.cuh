@@ -129,6 +129,7 @@ struct PassParams {
   int world;
   const TileEntry* ttab;      // segmented mode: tile table (else tiles are t * kTile)
   const uint32_t* ntiles;     // segmented mode: number of valid table entries
+  int ablate;                 // experiment hook (0 in production)
 };
 
 // Shaved key q = K' div T.
@@ -151,10 +152,32 @@ struct DigitFn {
     sh = (a.qshift >= 0 && !a.splitters) ? a.qshift + a.kp.dshift[a.pass] : -1;
   }
   __device__ __forceinline__ uint32_t operator()(const PassParams& a, uint64_t k2) const {
-    if (sh >= 0) return (uint32_t)(k2 >> sh) & mask;
+    if (sh >= 0) return bm_window((uint32_t)k2, (uint32_t)(k2 >> 32), sh) & mask;
     return digit_new(a, k2);
   }
 };
+
+// LIV shuffle of N keys in registers: bit moves for power-of-two plans, fast division
+// otherwise.
+template <int N>
+__device__ __forceinline__ void reencode_keys(const KeyPlan& p, uint64_t (&k)[N]) {
+  if (p.pow2 && p.nmv > 0) reencode_moves<N>(p, k);
+  else reencode_n<N>(p, k);
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // Element range of tile t; false if t is past the end of a segmented table.
 __device__ __forceinline__ bool tile_range(const PassParams& a, uint32_t t, uint64_t* base,

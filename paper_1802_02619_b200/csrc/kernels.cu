@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_common.cuh"
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   if (!tile_range(a, t, &base, &n, &seg)) return;
   for (int i = tid; i < BINS; i += kThreads) h[i] = 0;
   const DigitFn dg(a);
+  // pow2 first pass: the digit is a few bit fields of the OLD key, no full shuffle
+  const bool direct = FIRST && !a.splitters && a.kp.ndmv[a.pass] >= 0;
   __syncthreads();
   constexpr int H = kItems / 2;  // two rounds of 8 keys keep the registers low
 #pragma unroll
@@ -81,7 +84,15 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
       const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
       k[it] = pos < n ? __ldcs(keys + base + pos) : 0ull;
     }
-    if (FIRST) reencode_n<H>(a.kp, k);  // LIV shuffle
+    if (direct) {
+#pragma unroll
+      for (int it = 0; it < H; ++it) {
+        const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
+        if (pos < n) atomicAdd(&h[digit_from_old(a.kp, a.pass, k[it])], 1u);
+      }
+      continue;
+    }
+    if (FIRST) reencode_keys<H>(a.kp, k);  // LIV shuffle
 #pragma unroll
     for (int it = 0; it < H; ++it) {
       const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
@@ -154,7 +165,46 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ cs
 
 // ---------------------------------------------------------------------------------
 // k_offsets: toff[t][d] = bucket[d] + csum[c][d] + sum of thist rows before t in c.
+// Thread = PER consecutive digits (vector loads of the u16 rows, vector stores of the
+// offsets); rows are fetched four at a time so the loads overlap.
 // ---------------------------------------------------------------------------------
+template <int PER>
+struct RowVec;
+template <>
+struct RowVec<8> {
+  __device__ static void load(const uint16_t* p, uint32_t (&h)[8]) {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      h[2 * i] = w[i] & 0xFFFFu;
+      h[2 * i + 1] = w[i] >> 16;
+    }
+  }
+  __device__ static void store(uint32_t* p, const uint32_t (&r)[8]) {
+    reinterpret_cast<uint4*>(p)[0] = make_uint4(r[0], r[1], r[2], r[3]);
+    reinterpret_cast<uint4*>(p)[1] = make_uint4(r[4], r[5], r[6], r[7]);
+  }
+};
+template <>
+struct RowVec<4> {
+  __device__ static void load(const uint16_t* p, uint32_t (&h)[4]) {
+    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(p));
+    h[0] = v.x & 0xFFFFu;
+    h[1] = v.x >> 16;
+    h[2] = v.y & 0xFFFFu;
+    h[3] = v.y >> 16;
+  }
+  __device__ static void store(uint32_t* p, const uint32_t (&r)[4]) {
+    reinterpret_cast<uint4*>(p)[0] = make_uint4(r[0], r[1], r[2], r[3]);
+  }
+};
+template <>
+struct RowVec<1> {
+  __device__ static void load(const uint16_t* p, uint32_t (&h)[1]) { h[0] = __ldcg(p); }
+  __device__ static void store(uint32_t* p, const uint32_t (&r)[1]) { p[0] = r[0]; }
+};
+
 template <int RB>
 __global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ PassParams a,
                                                       const uint16_t* __restrict__ thist,
@@ -162,38 +212,72 @@ __global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ Pa
                                                       const uint32_t* __restrict__ bucket,
                                                       uint32_t* __restrict__ toff) {
   constexpr int BINS = 1 << RB;
+  constexpr int PER = BINS / kThreads;
+  static_assert(PER == 1 || PER == 4 || PER == 8, "digit widths 8, 10, 11");
+  constexpr int U = 4;
   const uint32_t c = blockIdx.x;
   const uint32_t t0 = c * a.ctiles, t1 = min(a.tiles, t0 + a.ctiles);
-  for (int d = threadIdx.x; d < BINS; d += kThreads) {
-    uint32_t run = __ldg(bucket + d) + __ldcg(csum + (size_t)c * BINS + d);
-    for (uint32_t t = t0; t < t1; ++t) {
-      toff[(size_t)t * BINS + d] = run;
-      run += __ldcg(thist + (size_t)t * BINS + d);
+  const int d0 = threadIdx.x * PER;
+  uint32_t run[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    run[i] = __ldg(bucket + d0 + i) + __ldcg(csum + (size_t)c * BINS + d0 + i);
+  for (uint32_t t = t0; t < t1; t += U) {
+    uint32_t h[U][PER];
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      if (t + r < t1) RowVec<PER>::load(thist + (size_t)(t + r) * BINS + d0, h[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      if (t + r < t1) {
+        RowVec<PER>::store(toff + (size_t)(t + r) * BINS + d0, run);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) run[i] += h[r][i];
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------------------------
 // k_scatter: one tile per CTA.
+//   rank    every warp ranks its 512 nonzeros in input order: match.any finds the lanes
+//           holding the same digit, per-warp u16 counters give the running count, so
+//           rank = (earlier warps, earlier items, earlier lanes) = the stable order;
+//   stage   keys go to shared memory at their tile-sorted slot; values and source
+//           positions are gathered straight from global memory into their slots with
+//           cp.async (no registers, the loads fly during the bookkeeping);
+//   write   one loop writes K', V and the position of each slot to toff + rank:
+//           consecutive threads write consecutive slots, i.e. runs of equal digit.
+// Shared memory: sK [tile] u64 | sV [tile] f64 (holds the per-warp counters while
+// ranking) | sP [tile] u32 | sdig [tile] u16 | gbase [bins] u32 | loff [bins] u32.
 // ---------------------------------------------------------------------------------
+constexpr int scatter_nt(int rb) { return rb <= 10 ? 512 : 256; }
+
 template <int RB>
 constexpr size_t scatter_smem_bytes() {
-  return (size_t)kTile * 8 + (size_t)(kThreads / 32) * (1 << RB) * 2 + (size_t)(1 << RB) * 8 +
-         (size_t)kTile * 2;
+  return (size_t)kTile * (8 + 8 + 4 + 2) + (size_t)(1 << RB) * 8;
 }
 
-template <int RB, bool FIRST, bool LAST, bool VALS>
-__global__ void __launch_bounds__(kThreads, 2)
+// NT threads (IT = kTile / NT nonzeros each): 512 for digits of <= 10 bits (more warps
+// in flight per SM, half the serial work per thread), 256 for 11-bit digits (whose
+// per-warp counters would not fit in sV with 16 warps).
+template <int RB, bool FIRST, bool LAST, bool VALS, int NT>
+__global__ void __launch_bounds__(NT, 2)
     k_scatter(const __grid_constant__ PassParams a, const __grid_constant__ ScatterIO io) {
   constexpr int BINS = 1 << RB;
-  constexpr int W = kThreads / 32;
-  constexpr int NB = BINS >= kThreads ? BINS / kThreads : 1;
+  constexpr int W = NT / 32;
+  constexpr int IT = kTile / NT;
+  constexpr int NB = BINS >= NT ? BINS / NT : 1;
+  static_assert(W * BINS * 2 <= kTile * 8, "warp counters must fit in sV");
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* stage = reinterpret_cast<uint64_t*>(smem);              // [kTile]
-  uint16_t* whist = reinterpret_cast<uint16_t*>(stage + kTile);     // [W][BINS]
-  uint32_t* gbase = reinterpret_cast<uint32_t*>(whist + W * BINS);  // [BINS]
-  uint32_t* loff = gbase + BINS;                                    // [BINS]
-  uint16_t* sdig = reinterpret_cast<uint16_t*>(loff + BINS);        // [kTile]
+  uint64_t* sK = reinterpret_cast<uint64_t*>(smem);              // [kTile]
+  double* sV = reinterpret_cast<double*>(sK + kTile);             // [kTile]
+  uint16_t* whist = reinterpret_cast<uint16_t*>(sV);              // [W][BINS] (ranking only)
+  uint32_t* sP = reinterpret_cast<uint32_t*>(sV + kTile);         // [kTile]
+  uint16_t* sdig = reinterpret_cast<uint16_t*>(sP + kTile);       // [kTile]
+  uint32_t* gbase = reinterpret_cast<uint32_t*>(sdig + kTile);    // [BINS]
+  uint32_t* loff = gbase + BINS;                                  // [BINS]
   __shared__ uint32_t s_warp[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -201,44 +285,44 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint64_t base;
   uint32_t n, seg;
   if (!tile_range(a, t, &base, &n, &seg)) return;
-  for (int i = tid; i < W * BINS / 2; i += kThreads) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
+  for (int i = tid; i < W * BINS / 2; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
   // ---- load keys; warp w owns a contiguous slice, lanes consecutive ----
-  uint64_t key[kItems];
-  uint32_t meta[kItems];
+  uint64_t key[IT];
+  uint32_t meta[IT];
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+  for (int it = 0; it < IT; ++it) {
+    const uint32_t pos = warp * 32 * IT + it * 32 + lane;
     key[it] = pos < n ? __ldcs((FIRST ? io.keys_in : io.kin) + base + pos) : 0ull;
   }
   // global offsets of this tile's digit runs (from the exclusive scan)
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    const int d = tid + b * kThreads;
+    const int d = tid + b * NT;
     if (d < BINS) gbase[d] = __ldcs(io.toff + (size_t)t * BINS + d);
   }
   {
     const DigitFn dg(a);
     if (FIRST && io.keep_old_key) {  // partition: route by K', move the old key
 #pragma unroll
-      for (int it = 0; it < kItems; ++it) {
-        const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+      for (int it = 0; it < IT; ++it) {
+        const uint32_t pos = warp * 32 * IT + it * 32 + lane;
         meta[it] = pos < n ? dg(a, reencode(a.kp, key[it])) : kInvalid;
       }
     } else {
-      if (FIRST) {  // LIV shuffle, in place, two rounds of 8 keys
+      if (FIRST && a.ablate != 3) {  // LIV shuffle, in place, two rounds
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          uint64_t kk[kItems / 2];
+          uint64_t kk[IT / 2];
 #pragma unroll
-          for (int i = 0; i < kItems / 2; ++i) kk[i] = key[half * (kItems / 2) + i];
-          reencode_n<kItems / 2>(a.kp, kk);
+          for (int i = 0; i < IT / 2; ++i) kk[i] = key[half * (IT / 2) + i];
+          reencode_keys<IT / 2>(a.kp, kk);
 #pragma unroll
-          for (int i = 0; i < kItems / 2; ++i) key[half * (kItems / 2) + i] = kk[i];
+          for (int i = 0; i < IT / 2; ++i) key[half * (IT / 2) + i] = kk[i];
         }
       }
 #pragma unroll
-      for (int it = 0; it < kItems; ++it) {
-        const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
+      for (int it = 0; it < IT; ++it) {
+        const uint32_t pos = warp * 32 * IT + it * 32 + lane;
         meta[it] = pos < n ? dg(a, key[it]) : kInvalid;
       }
     }
@@ -248,26 +332,29 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint16_t* wh = whist + warp * BINS;
   const uint32_t ltm = lanemask_lt();
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
+  for (int it = 0; it < IT; ++it) {
     const uint32_t d = meta[it];
     const bool ok = d != kInvalid;
-    const uint32_t peers = peers_of<RB>(d, ok);
-    uint32_t before = 0;
-    const bool leader = ok && (peers & ltm) == 0;
-    if (leader) {
-      before = wh[d];
-      wh[d] = (uint16_t)(before + __popc(peers));
+    // lanes holding the same digit: one ballot per digit bit (ALU pipe; match.any goes
+    // through the MIO queue and its latency dominated the ranking loop, ncu)
+    uint32_t peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const uint32_t bit = (d >> b) & 1u;
+      peers &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
     }
-    const int src = ok ? __ffs(peers) - 1 : lane;
-    before = __shfl_sync(0xffffffffu, before, src);
-    meta[it] = d | ((before + __popc(peers & ltm)) << 16);
+    const uint32_t below = __popc(peers & ltm);
+    const uint32_t before = ok ? (uint32_t)wh[d] : 0u;  // every peer reads the same counter
+    __syncwarp();
+    if (ok && below == 0) wh[d] = (uint16_t)(before + __popc(peers));
+    meta[it] = d | ((before + below) << 16);
     __syncwarp();
   }
   __syncthreads();
   // ---- per digit: exclusive prefix across warps, tile count ----
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    const int d = tid + b * kThreads;
+    const int d = tid + b * NT;
     if (d < BINS) {
       uint32_t s = 0;
 #pragma unroll
@@ -280,63 +367,56 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
   }
   __syncthreads();
-  block_scan_bins<kThreads, BINS>(loff, loff, s_warp);
-  // ---- local (tile-sorted) positions; stage keys ----
+  block_scan_bins<NT, BINS>(loff, loff, s_warp);
+  // ---- local (tile-sorted) slots; stage keys and digits ----
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
+  for (int it = 0; it < IT; ++it) {
     const uint32_t d = meta[it] & 0xFFFFu;
     if (d != kInvalid) {
       const uint32_t lp = loff[d] + whist[warp * BINS + d] + (meta[it] >> 16);
-      stage[lp] = key[it];
+      sK[lp] = key[it];
       sdig[lp] = (uint16_t)d;
       meta[it] = d | (lp << 16);
     }
   }
-  // ---- values: load now, they fly while the keys are written ----
-  double val[VALS ? kItems : 1];
-  if constexpr (VALS) {
+  __syncthreads();  // the warp counters (in sV) are dead from here on
+  // ---- gather values / positions into their slots (cp.async, global -> shared) ----
+  const bool want_p = io.pout != nullptr;
 #pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
-      val[it] = pos < n ? __ldcs((FIRST ? io.vals_in : io.vin) + base + pos) : 0.0;
-    }
-  }
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int d = tid + b * kThreads;
-    if (d < BINS) gbase[d] -= loff[d];  // global position of local slot 0 of digit d
-  }
-  __syncthreads();
-  for (uint32_t p = tid; p < n; p += kThreads) io.kout[gbase[sdig[p]] + p] = stage[p];
-  __syncthreads();
-  if constexpr (VALS) {
-    double* sv = reinterpret_cast<double*>(stage);
-#pragma unroll
-    for (int it = 0; it < kItems; ++it)
-      if ((meta[it] & 0xFFFFu) != kInvalid) sv[meta[it] >> 16] = val[it];
-    __syncthreads();
-    for (uint32_t p = tid; p < n; p += kThreads) io.vout[gbase[sdig[p]] + p] = sv[p];
-    __syncthreads();
-  }
-  if (io.pout) {
-    uint32_t* s32 = reinterpret_cast<uint32_t*>(stage);
-#pragma unroll
-    for (int it = 0; it < kItems; ++it) {
-      const uint32_t pos = warp * 32 * kItems + it * 32 + lane;
-      if ((meta[it] & 0xFFFFu) != kInvalid) {
-        uint32_t v;
-        if (FIRST) {
-          v = (LAST && io.idx_in) ? __ldg(io.idx_in + base + pos)
-                                  : (uint32_t)(base + pos) + (LAST ? io.idx_base : 0u);
-        } else {
-          v = __ldcs(io.pin + base + pos);
-          if (LAST && io.idx_in) v = __ldg(io.idx_in + v);
-        }
-        s32[meta[it] >> 16] = v;
+  for (int it = 0; it < IT; ++it) {
+    if ((meta[it] & 0xFFFFu) == kInvalid) continue;
+    const uint32_t pos = warp * 32 * IT + it * 32 + lane;
+    const uint32_t lp = meta[it] >> 16;
+    if (VALS) cp_async8(sV + lp, (FIRST ? io.vals_in : io.vin) + base + pos);
+    if (want_p) {
+      if (FIRST) {
+        if (LAST && io.idx_in) cp_async4(sP + lp, io.idx_in + base + pos);
+        else sP[lp] = (uint32_t)(base + pos) + (LAST ? io.idx_base : 0u);
+      } else {
+        cp_async4(sP + lp, io.pin + base + pos);
       }
     }
-    __syncthreads();
-    for (uint32_t p = tid; p < n; p += kThreads) io.pout[gbase[sdig[p]] + p] = s32[p];
+  }
+  cp_async_commit();
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int d = tid + b * NT;
+    if (d < BINS) gbase[d] -= loff[d];  // global position of local slot 0 of digit d
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // ---- one write loop: K', V, position of each slot ----
+  const bool remap = !FIRST && LAST && io.idx_in != nullptr;
+  for (uint32_t p = tid; p < n; p += NT) {
+    uint32_t g = gbase[sdig[p]] + p;
+    if (a.ablate == 1 && g != 0xFFFFFFFFu) continue;  // compute only
+    if (a.ablate == 2) g = (uint32_t)base + p;         // coalesced writes
+    io.kout[g] = sK[p];
+    if (VALS) io.vout[g] = sV[p];
+    if (want_p) {
+      const uint32_t v = sP[p];
+      io.pout[g] = remap ? __ldg(io.idx_in + v) : v;
+    }
   }
 }
 
@@ -385,7 +465,10 @@ static cudaError_t set_smem_attrs() {
   const int bytes = (int)scatter_smem_bytes<RB>();
   cudaError_t e = cudaSuccess;
 #define LCO_ATTR(F, L, V)                                                       \
-  e = cudaFuncSetAttribute(k_scatter<RB, F, L, V>,                              \
+  e = cudaFuncSetAttribute(k_scatter<RB, F, L, V, scatter_nt(RB)>,              \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+  if (e != cudaSuccess) return e;                                               \
+  e = cudaFuncSetAttribute(k_scatter<RB, F, L, V, 256>,                         \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
   if (e != cudaSuccess) return e;
   LCO_ATTR(true, true, false)
@@ -457,9 +540,16 @@ static cudaError_t launch_scatter_rb(bool first, bool last, bool vals, const Pas
   cudaError_t e = set_smem_attrs<RB>();
   if (e != cudaSuccess) return e;
   const size_t smem = scatter_smem_bytes<RB>();
-#define LCO_LAUNCH(F, LST)                                                      \
-  if (vals) k_scatter<RB, F, LST, true><<<grid, kThreads, smem, s>>>(a, io);   \
-  else k_scatter<RB, F, LST, false><<<grid, kThreads, smem, s>>>(a, io);
+  constexpr int NT = scatter_nt(RB);
+  static const int nt_env = getenv("LCO_NT") ? atoi(getenv("LCO_NT")) : 0;
+#define LCO_LAUNCH(F, LST)                                                           \
+  if (NT == 512 && nt_env == 256) {                                                  \
+    if (vals) k_scatter<RB, F, LST, true, 256><<<grid, 256, smem, s>>>(a, io);       \
+    else k_scatter<RB, F, LST, false, 256><<<grid, 256, smem, s>>>(a, io);           \
+  } else {                                                                           \
+    if (vals) k_scatter<RB, F, LST, true, NT><<<grid, NT, smem, s>>>(a, io);         \
+    else k_scatter<RB, F, LST, false, NT><<<grid, NT, smem, s>>>(a, io);             \
+  }
   if (first && last) {
     LCO_LAUNCH(true, true)
   } else if (first) {
@@ -565,6 +655,7 @@ cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch
   PassParams a;
   memset(&a, 0, sizeof a);
   a.kp = kp;
+  a.ablate = getenv("LCO_ABLATE") ? atoi(getenv("LCO_ABLATE")) : 0;
   if (part) a.kp.passes = 1;
   a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
   a.nnz = io.nnz;

@@ -55,6 +55,7 @@ struct MsdPlan {
   int levels;
   int b1, b2;
   int rb;
+  int cta;  // leaves sorted by k_leafc (one CTA per leaf) instead of k_leafw (one warp)
 };
 
 struct PassParams;
@@ -75,6 +76,7 @@ cudaError_t run_pass(int rb, const PassParams& a, const PassIO& io, int j, bool 
 cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
 uint32_t leaf_cap();      // largest leaf one CTA sorts in shared memory
 uint32_t leaf_target();   // expected leaf size the MSD digits aim for (warp leaves)
+uint32_t cta_leaf_cap();  // largest leaf k_leafc sorts
 size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
 cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
 cudaError_t run_copy(uint64_t nnz, const uint64_t* keys_in, const double* vals_in,

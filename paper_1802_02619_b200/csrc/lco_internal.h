@@ -53,6 +53,21 @@ FastDiv make_fastdiv(uint64_t d);  // host (plan.cpp); d >= 1
 // ---------------------------------------------------------------------------------
 constexpr int kMaxModes = LCO_MAX_ORDER;
 constexpr int kMaxPasses = 8;
+constexpr int kMaxMoves = 40;       // bit moves of a power-of-two LIV shuffle
+constexpr int kMaxDigitMoves = 12;  // bit moves that build one radix digit of q
+
+// One bit-field move of a power-of-two LIV shuffle, in 32-bit words: take the 32-bit
+// window of the old key starting at bit `a`, keep the low bits under `mask`, and add
+// them at bit `b` of output word `hi` (0: bits 0-31, 1: bits 32-63).  Fields never
+// overlap, so add == or.  The host splits every mode's field so that no move crosses
+// an output word (build_moves, plan.cpp).
+struct BitMove {
+  uint32_t mask;
+  uint8_t a;
+  uint8_t hi;
+  uint8_t b;
+  uint8_t pad;
+};
 
 struct KeyPlan {
   int n;                          // normalized order (>= 2 on the radix path)
@@ -68,7 +83,57 @@ struct KeyPlan {
   int passes;                     // P
   int dshift[kMaxPasses];         // digit j = (q >> dshift[j]) & ((1 << dbits[j]) - 1)
   int dbits[kMaxPasses];
+  // pow2 plans: the shuffle as word-local bit moves, and every digit of q straight from
+  // the OLD key (so a histogram of the first pass never builds K'); ndmv[j] < 0: the
+  // digit needs the full shuffle.  Filled by build_moves / build_digit_moves.
+  int nmv;
+  BitMove mv[kMaxMoves];
+  int ndmv[kMaxPasses];
+  BitMove dmv[kMaxPasses][kMaxDigitMoves];
 };
+
+#if defined(__CUDACC__)
+// 32-bit window of the key (hi:lo) starting at bit a (0..63).
+__device__ __forceinline__ uint32_t bm_window(uint32_t lo, uint32_t hi, int a) {
+  return a < 32 ? __funnelshift_r(lo, hi, a) : (hi >> (a - 32));
+}
+
+// LIV shuffle of N keys by bit moves (pow2 plans): two 32-bit output words per key.
+template <int N>
+__device__ __forceinline__ void reencode_moves(const KeyPlan& p, uint64_t (&k)[N]) {
+  uint32_t olo[N], ohi[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) olo[i] = ohi[i] = 0u;
+#pragma unroll 1
+  for (int j = 0; j < p.nmv; ++j) {
+    const BitMove m = p.mv[j];
+    const uint32_t mul = 1u << m.b;
+    if (m.hi) {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        ohi[i] += (bm_window((uint32_t)k[i], (uint32_t)(k[i] >> 32), m.a) & m.mask) * mul;
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        olo[i] += (bm_window((uint32_t)k[i], (uint32_t)(k[i] >> 32), m.a) & m.mask) * mul;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) k[i] = ((uint64_t)ohi[i] << 32) | olo[i];
+}
+
+// Digit `pass` of q straight from an OLD key (pow2 plans, p.ndmv[pass] >= 0).
+__device__ __forceinline__ uint32_t digit_from_old(const KeyPlan& p, int pass, uint64_t k) {
+  const uint32_t lo = (uint32_t)k, hi = (uint32_t)(k >> 32);
+  uint32_t d = 0;
+#pragma unroll 1
+  for (int j = 0; j < p.ndmv[pass]; ++j) {
+    const BitMove m = p.dmv[pass][j];
+    d += (bm_window(lo, hi, m.a) & m.mask) << m.b;
+  }
+  return d;
+}
+#endif
 
 // LIV shuffle of one key: decode old coordinates from the last mode
 // with fast division, accumulate the new key with the new strides.
@@ -177,6 +242,7 @@ constexpr int kProfStages = 48;
 // Host planning (plan.cpp)
 lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int32_t* perm);
 void choose_passes(OpPlan* op, int sort_bits);
+void build_digit_moves(KeyPlan* kp);  // after dshift / dbits are final (pow2 plans)
 int ceil_log2(uint64_t x);  // smallest b with 2^b >= x
 void set_error(const char* fmt, ...);
 }  // namespace lco

@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_common.cuh"
@@ -203,20 +205,6 @@ __device__ __forceinline__ bool next_leaf(const LeafArgs& L, uint32_t& k, LeafDe
   return false;
 }
 
-__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
 // Sort key of a staged record: the leaf's remaining bits of q = K' div T.
 __device__ __forceinline__ uint64_t leaf_key(const LeafArgs& L, uint64_t k2, uint64_t mask) {
   return q_of(L.a, k2) & mask;
@@ -226,12 +214,14 @@ __device__ __forceinline__ uint64_t leaf_key(const LeafArgs& L, uint64_t k2, uin
 // `shift` of the staged keys: per-warp contiguous slices, counts, then an in-order
 // ballot ranking sweep.  On return io holds the sorted indices, loff[d] the first slot
 // of digit d and cnt[d] its count.
-template <int LB>
+template <int LB, int NT = kLeafThreads>
 __device__ __forceinline__ void leaf_rank_pass(const LeafArgs& L, const uint64_t* Kp,
                                                uint64_t mask, const uint16_t* ii, uint16_t* io,
                                                uint32_t m, int shift, uint32_t* whist,
                                                uint32_t* loff, uint32_t* cnt, uint32_t* s_warp) {
   constexpr int BINS = 1 << LB;
+  constexpr int kLeafWarps = NT / 32;
+  constexpr int kLeafThreads = NT;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t slice = ((m + kLeafWarps - 1) / kLeafWarps + 31) / 32 * 32;
   const uint32_t s0 = min(m, warp * slice), s1 = min(m, s0 + slice);
@@ -637,6 +627,564 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------------
+// k_leafc: one CTA per leaf of up to kCCap nonzeros (the leaves of 8-bit MSD levels,
+// ~6-8K nonzeros, and the whole input of small calls).  Persistent over the leaf slots
+// of one level, in slot order.
+//   stage   K' of the leaf -> shared memory (cp.async); values and positions stay in
+//           global memory (L2-prefetched) and are gathered when the outputs are written;
+//   bucket  shared atomics on tb <= 12 bits of (key - min key of the leaf): about two
+//           nonzeros per bucket whatever the key range of the leaf; scan; placement;
+//   rank    one thread per bucket sorts it in place by insertion on (key, staging
+//           index); the staging index is the stable order, so the result is exactly
+//           the stable sort;
+//   write   keys_out / vals_out / perm_out of the leaf, contiguous, the value and
+//           position gathers batched four deep.
+// A leaf with a bucket of more than kCBig nonzeros (skewed or duplicate keys) is sorted
+// by stable 8-bit radix passes in shared memory (BIG: one CTA per SM, the single-leaf
+// call) or sent to the deferred list of the block-level k_leaf (leaf levels, two CTAs
+// per SM).
+// ---------------------------------------------------------------------------------
+constexpr int kCCap = 8192;
+constexpr int kCBucketBits = 12;
+constexpr int kCThreads = 512;
+constexpr int kCBig = 48;
+
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
+               : "memory");
+}
+constexpr size_t leafc_smem(bool big) {
+  return (size_t)kCCap * (8 + 2) + ((size_t)1 << kCBucketBits) * 4 +
+         (big ? (size_t)kCCap * 2 + (size_t)(kCThreads / 32) * 256 * 4 : 0);
+}
+
+template <bool VALS, bool BIG>
+__global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_constant__ LeafArgs L) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* K = reinterpret_cast<uint64_t*>(smem);                 // [cap] staged K'
+  uint16_t* X = reinterpret_cast<uint16_t*>(K + kCCap);            // [cap] order
+  uint32_t* B = reinterpret_cast<uint32_t*>(X + kCCap);            // [2^12] buckets
+  uint16_t* F = reinterpret_cast<uint16_t*>(B + (1 << kCBucketBits));  // BIG: [cap]
+  uint32_t* WH = reinterpret_cast<uint32_t*>(F + kCCap);           // BIG: radix counters
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_loff[256], s_cnt[256];
+  __shared__ unsigned long long s_min, s_max;
+  __shared__ int s_big;
+  const int tid = threadIdx.x;
+  const bool want_pos = L.perm_out != nullptr;
+  const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
+  uint32_t k = blockIdx.x;
+  LeafDesc d;
+  while (next_leaf(L, k, &d)) {
+    const uint32_t n = d.n, start = d.start;
+    const uint64_t* sk = d.src == 0 ? L.keys_in : (d.src == 1 ? L.kA : L.kB);
+    const double* sv = d.src == 0 ? L.vals_in : (d.src == 1 ? L.vA : L.vB);
+    const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
+    if (n > (uint32_t)kCCap) {  // oversize (skewed) leaf: the block kernel streams it
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      k += gridDim.x;
+      continue;
+    }
+    if (tid == 0) {
+      s_min = ~0ull;
+      s_max = 0ull;
+      s_big = 0;
+    }
+    if (d.src == 0) {  // raw input (the whole call is one leaf): re-encode while staging
+      for (uint32_t i = tid; i < n; i += kCThreads) K[i] = reencode(L.a.kp, __ldcs(sk + start + i));
+    } else {
+      for (uint32_t i = tid; i < n; i += kCThreads) cp_async8(K + i, sk + (uint64_t)start + i);
+      cp_async_commit();
+      if (tid == 0) {  // the gathers of the write phase then hit L2
+        if (VALS) prefetch_l2(sv + start, (size_t)n * 8);
+        if (want_pos) prefetch_l2(sp + start, (size_t)n * 4);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    {  // key range of the leaf
+      uint64_t mn = ~0ull, mx = 0ull;
+      for (uint32_t i = tid; i < n; i += kCThreads) {
+        const uint64_t kk = leaf_key(L, K[i], mask);
+        mn = kk < mn ? kk : mn;
+        mx = kk > mx ? kk : mx;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o);
+        const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+      }
+      if ((tid & 31) == 0) {
+        atomicMin(&s_min, (unsigned long long)mn);
+        atomicMax(&s_max, (unsigned long long)mx);
+      }
+    }
+    int lg = 0;
+    while ((1u << lg) < n) ++lg;
+    const int tb = min(max(lg - 1, 1), kCBucketBits);
+    const uint32_t nbk = 1u << tb;
+    for (uint32_t b = tid; b < nbk; b += kCThreads) B[b] = 0;
+    __syncthreads();
+    const uint64_t kmin = s_min, range = s_max - s_min;
+    int rbits = 0;
+    while (rbits < 64 && (range >> rbits) != 0) ++rbits;
+    const int bshift = rbits > tb ? rbits - tb : 0;
+    for (uint32_t i = tid; i < n; i += kCThreads)
+      atomicAdd(&B[(uint32_t)((leaf_key(L, K[i], mask) - kmin) >> bshift)], 1u);
+    __syncthreads();
+    {  // exclusive scan of the bucket counts: 8 per thread
+      constexpr int PER = (1 << kCBucketBits) / kCThreads;
+      uint32_t v[PER], sum = 0;
+      const uint32_t b0 = tid * PER;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        v[i] = b0 + i < nbk ? B[b0 + i] : 0u;
+        sum += v[i];
+      }
+      const int lane = tid & 31, warp = tid >> 5;
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_warp[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t w = lane < kCThreads / 32 ? s_warp[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+          if (lane >= o) wi += y;
+        }
+        if (lane < kCThreads / 32) s_warp[lane] = wi - w;
+      }
+      __syncthreads();
+      uint32_t r = s_warp[warp] + incl - sum;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        if (b0 + i < nbk) B[b0 + i] = r;
+        r += v[i];
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kCThreads)
+      X[atomicAdd(&B[(uint32_t)((leaf_key(L, K[i], mask) - kmin) >> bshift)], 1u)] = (uint16_t)i;
+    __syncthreads();
+    // B[b] is now the end of bucket b: one thread per bucket sorts it in place
+    for (uint32_t b = tid; b < nbk; b += kCThreads) {
+      const uint32_t lo = b ? B[b - 1] : 0u, hi = B[b];
+      if (hi - lo > (uint32_t)kCBig) {
+        s_big = 1;
+        continue;
+      }
+      for (uint32_t i = lo + 1; i < hi; ++i) {
+        const uint16_t x = X[i];
+        const uint64_t kx = leaf_key(L, K[x], mask);
+        uint32_t j = i;
+        while (j > lo) {
+          const uint16_t y = X[j - 1];
+          const uint64_t ky = leaf_key(L, K[y], mask);
+          if (ky < kx || (ky == kx && y < x)) break;
+          X[j] = y;
+          --j;
+        }
+        X[j] = x;
+      }
+    }
+    __syncthreads();
+    const uint16_t* order = X;
+    if (s_big) {
+      if constexpr (BIG) {  // stable LSD radix passes of 8 bits on chip
+        uint16_t* xa = X;
+        uint16_t* xb = F;
+        for (uint32_t i = tid; i < n; i += kCThreads) xa[i] = (uint16_t)i;
+        __syncthreads();
+        for (int sh = 0; sh < L.rb; sh += 8) {
+          leaf_rank_pass<8, kCThreads>(L, K, mask, xa, xb, n, sh, WH, s_loff, s_cnt, s_warp);
+          uint16_t* t = xa;
+          xa = xb;
+          xb = t;
+        }
+        order = xa;
+      } else {  // skewed leaf: the block-level kernel sorts it
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+        __syncthreads();
+        k += gridDim.x;
+        continue;
+      }
+    }
+    constexpr int U = 4;
+    for (uint32_t j0 = 0; j0 < n; j0 += U * kCThreads) {
+      uint16_t e[U];
+      double v[U];
+      uint32_t pos[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * kCThreads + tid;
+        e[u] = j < n ? order[j] : 0;
+        if (VALS) v[u] = j < n ? __ldg(sv + start + e[u]) : 0.0;
+        if (want_pos) pos[u] = j < n ? (d.src == 0 ? start + e[u] : __ldg(sp + start + e[u])) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * kCThreads + tid;
+        if (j < n) {
+          const uint64_t g = (uint64_t)start + j;
+          L.keys_out[g] = K[e[u]];
+          if (VALS) L.vals_out[g] = v[u];
+          if (want_pos) L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pos[u]) : pos[u];
+        }
+      }
+    }
+    __syncthreads();  // K / X are reused by the next leaf
+    k += gridDim.x;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_leafr: the leaf sort of k_leafc for leaves whose remaining key bits span <= 32 bits
+// (C5: 48-bit q, 16 MSD bits -> 32), with 32-bit keys in shared memory:
+//   load    each thread reads its K' (16 per thread, coalesced) and reduces the leaf's
+//           key range; R[i] = key - min as 32 bits; bucket counts of its top bits;
+//   place   scan + shared atomics (X: bucket order);
+//   rank    every thread ranks one element inside its (small) bucket by counting smaller
+//           (R, staging index) pairs -> F (final order, exactly the stable order);
+//   write   K', V and the position are gathered from L2 (the leaf's ranges were
+//           prefetched at its start) and written contiguously, four deep.
+// 80 KB of shared memory: two CTAs per SM.  A leaf whose key range needs more than 32
+// bits, or with a bucket of more than kCBig nonzeros, goes to the deferred list.
+// ---------------------------------------------------------------------------------
+constexpr int kRItems = kCCap / kCThreads;  // 16
+constexpr size_t kRSmem = (size_t)kCCap * (4 + 2 + 2) + ((size_t)1 << kCBucketBits) * 4;
+
+template <bool VALS>
+__global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ LeafArgs L) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* R = reinterpret_cast<uint32_t*>(smem);                 // [cap] key - min
+  uint16_t* X = reinterpret_cast<uint16_t*>(R + kCCap);            // [cap] bucket order
+  uint16_t* F = X + kCCap;                                         // [cap] final order
+  uint32_t* B = reinterpret_cast<uint32_t*>(F + kCCap);            // [2^12] buckets
+  __shared__ uint32_t s_warp[32];
+  __shared__ unsigned long long s_min, s_max;
+  __shared__ int s_big;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool want_pos = L.perm_out != nullptr;
+  const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
+  uint32_t k = blockIdx.x;
+  LeafDesc d;
+  while (next_leaf(L, k, &d)) {
+    const uint32_t n = d.n, start = d.start;
+    const uint64_t* sk = d.src == 1 ? L.kA : L.kB;
+    const double* sv = d.src == 1 ? L.vA : L.vB;
+    const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
+    if (n > (uint32_t)kCCap) {  // oversize (skewed) leaf: the block kernel streams it
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      k += gridDim.x;
+      continue;
+    }
+    if (tid == 0) {
+      s_min = ~0ull;
+      s_max = 0ull;
+      s_big = 0;
+      if (L.a.ablate != 5) {
+        prefetch_l2(sk + start, (size_t)n * 8);  // the write phase gathers from L2
+        if (VALS) prefetch_l2(sv + start, (size_t)n * 8);
+        if (want_pos) prefetch_l2(sp + start, (size_t)n * 4);
+      }
+    }
+    uint64_t lk[kRItems];
+    uint64_t mn = ~0ull, mx = 0ull;
+#pragma unroll
+    for (int r = 0; r < kRItems; ++r) {
+      const uint32_t i = r * kCThreads + tid;
+      lk[r] = i < n ? leaf_key(L, __ldcg(sk + start + i), mask) : 0ull;
+      if (i < n) {
+        mn = lk[r] < mn ? lk[r] : mn;
+        mx = lk[r] > mx ? lk[r] : mx;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o);
+      const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
+      mn = a < mn ? a : mn;
+      mx = b > mx ? b : mx;
+    }
+    int lg = 0;
+    while ((1u << lg) < n) ++lg;
+    const int tb = min(max(lg - 1, 1), kCBucketBits);
+    const uint32_t nbk = 1u << tb;
+    for (uint32_t b = tid; b < nbk; b += kCThreads) B[b] = 0;
+    __syncthreads();  // s_min / s_max initialised, B zeroed
+    if (lane == 0) {
+      atomicMin(&s_min, (unsigned long long)mn);
+      atomicMax(&s_max, (unsigned long long)mx);
+    }
+    __syncthreads();
+    const uint64_t kmin = s_min, range = s_max - s_min;
+    const int rbits = range ? 64 - __clzll((long long)range) : 0;
+    if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      k += gridDim.x;
+      __syncthreads();
+      continue;
+    }
+    const int bshift = rbits > tb ? rbits - tb : 0;
+#pragma unroll
+    for (int r = 0; r < kRItems; ++r) {
+      const uint32_t i = r * kCThreads + tid;
+      if (i < n) {
+        const uint32_t rel = (uint32_t)(lk[r] - kmin);
+        R[i] = rel;
+        atomicAdd(&B[rel >> bshift], 1u);
+      }
+    }
+    __syncthreads();
+    {  // exclusive scan of the bucket counts: 8 per thread
+      constexpr int PER = (1 << kCBucketBits) / kCThreads;
+      uint32_t v[PER], sum = 0;
+      const uint32_t b0 = tid * PER;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        v[i] = b0 + i < nbk ? B[b0 + i] : 0u;
+        sum += v[i];
+      }
+      uint32_t incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_warp[warp] = incl;
+      __syncthreads();
+      if (warp == 0) {
+        const uint32_t w = lane < kCThreads / 32 ? s_warp[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+          if (lane >= o) wi += y;
+        }
+        if (lane < kCThreads / 32) s_warp[lane] = wi - w;
+      }
+      __syncthreads();
+      uint32_t r = s_warp[warp] + incl - sum;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        if (b0 + i < nbk) B[b0 + i] = r;
+        r += v[i];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRItems; ++r) {
+      const uint32_t i = r * kCThreads + tid;
+      if (i < n) X[atomicAdd(&B[(uint32_t)(lk[r] - kmin) >> bshift], 1u)] = (uint16_t)i;
+    }
+    __syncthreads();
+    // B[b] is now the end of bucket b
+    bool big = false;
+    for (uint32_t p = tid; p < n; p += kCThreads) {
+      const uint16_t x = X[p];
+      const uint32_t kx = R[x];
+      const uint32_t b = kx >> bshift;
+      const uint32_t lo = b ? B[b - 1] : 0u, hi = B[b];
+      if (hi - lo > (uint32_t)kCBig) {
+        big = true;
+        continue;
+      }
+      uint32_t rk = lo;
+      for (uint32_t j = lo; j < hi; ++j) {
+        const uint16_t y = X[j];
+        const uint32_t ky = R[y];
+        rk += (ky < kx || (ky == kx && y < x)) ? 1u : 0u;
+      }
+      F[rk] = x;
+    }
+    if (big) s_big = 1;
+    __syncthreads();
+    if (s_big) {  // skewed leaf: the block-level kernel sorts it
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      k += gridDim.x;
+      __syncthreads();  // everyone has read s_big before the next leaf resets it
+      continue;
+    }
+    constexpr int U = 4;
+    for (uint32_t j0 = 0; j0 < n; j0 += U * kCThreads) {
+      uint16_t e[U];
+      uint64_t kk[U];
+      double v[U];
+      uint32_t pos[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * kCThreads + tid;
+        e[u] = j < n ? F[j] : 0;
+        kk[u] = j < n ? __ldcg(sk + start + e[u]) : 0ull;
+        if (VALS) v[u] = j < n ? __ldcg(sv + start + e[u]) : 0.0;
+        if (want_pos) pos[u] = j < n ? __ldcg(sp + start + e[u]) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t j = j0 + u * kCThreads + tid;
+        if (j < n) {
+          const uint64_t g = (uint64_t)start + j;
+          L.keys_out[g] = kk[u];
+          if (VALS) L.vals_out[g] = v[u];
+          if (want_pos) L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pos[u]) : pos[u];
+        }
+      }
+    }
+    __syncthreads();  // R / X / F are reused by the next leaf
+    k += gridDim.x;
+  }
+}
+
+// ---------------------------------------------------------------------------------
+// k_leafs: fully staged CTA leaf sort for leaves of up to SCAP nonzeros (~1.9K: the
+// leaves of two 9-bit MSD levels at C5 scale).  K', V and the position of the leaf are
+// copied into shared memory with cp.async (input order, no registers), the leaf is
+// sorted as in k_leafr (32-bit keys relative to the leaf's minimum, ~2 per bucket,
+// rank by counting on (key, staging index) = the stable order), and the outputs are
+// written contiguously from shared memory.  72 KB: three CTAs per SM, so one CTA's
+// loads overlap another's sorting.  Leaves that do not fit, need more than 32 key bits,
+// or have a bucket of more than kCBig nonzeros go to the deferred list.
+// ---------------------------------------------------------------------------------
+constexpr int kSCap = 2304;
+constexpr int kSThreads = 256;
+constexpr int kSBucketBits = 11;
+constexpr size_t kSSmem = (size_t)kSCap * (8 + 8 + 4 + 4 + 2 + 2) + ((size_t)1 << kSBucketBits) * 4;
+
+template <bool VALS>
+__global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ LeafArgs L) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint64_t* K = reinterpret_cast<uint64_t*>(smem);   // [cap] K' (input order)
+  double* V = reinterpret_cast<double*>(K + kSCap);   // [cap] values
+  uint32_t* P = reinterpret_cast<uint32_t*>(V + kSCap);  // [cap] positions
+  uint32_t* R = P + kSCap;                            // [cap] key - min
+  uint16_t* X = reinterpret_cast<uint16_t*>(R + kSCap);  // [cap] bucket order
+  uint16_t* F = X + kSCap;                            // [cap] final order
+  uint32_t* B = reinterpret_cast<uint32_t*>(F + kSCap);  // [2^11] buckets
+  __shared__ uint32_t s_warp[32];
+  __shared__ unsigned long long s_min, s_max;
+  __shared__ int s_big;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool want_pos = L.perm_out != nullptr;
+  const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
+  uint32_t k = blockIdx.x;
+  LeafDesc d;
+  while (next_leaf(L, k, &d)) {
+    const uint32_t n = d.n, start = d.start;
+    const uint64_t* sk = d.src == 1 ? L.kA : L.kB;
+    const double* sv = d.src == 1 ? L.vA : L.vB;
+    const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
+    if (n > (uint32_t)kSCap) {  // oversize (skewed) leaf: the block kernel streams it
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      k += gridDim.x;
+      continue;
+    }
+    for (uint32_t i = tid; i < n; i += kSThreads) {
+      cp_async8(K + i, sk + (uint64_t)start + i);
+      if (VALS) cp_async8(V + i, sv + (uint64_t)start + i);
+      if (want_pos) cp_async4(P + i, sp + (uint64_t)start + i);
+    }
+    cp_async_commit();
+    if (tid == 0) {
+      s_min = ~0ull;
+      s_max = 0ull;
+      s_big = 0;
+    }
+    int lg = 0;
+    while ((1u << lg) < n) ++lg;
+    const int tb = min(max(lg - 1, 1), kSBucketBits);
+    const uint32_t nbk = 1u << tb;
+    for (uint32_t b = tid; b < nbk; b += kSThreads) B[b] = 0;
+    cp_async_wait<0>();
+    __syncthreads();
+    uint64_t mn = ~0ull, mx = 0ull;
+    for (uint32_t i = tid; i < n; i += kSThreads) {
+      const uint64_t kk = leaf_key(L, K[i], mask);
+      mn = kk < mn ? kk : mn;
+      mx = kk > mx ? kk : mx;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o);
+      const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
+      mn = a < mn ? a : mn;
+      mx = b > mx ? b : mx;
+    }
+    if (lane == 0) {
+      atomicMin(&s_min, (unsigned long long)mn);
+      atomicMax(&s_max, (unsigned long long)mx);
+    }
+    __syncthreads();
+    const uint64_t kmin = s_min, range = s_max - s_min;
+    const int rbits = range ? 64 - __clzll((long long)range) : 0;
+    if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      k += gridDim.x;
+      __syncthreads();
+      continue;
+    }
+    const int bshift = rbits > tb ? rbits - tb : 0;
+    for (uint32_t i = tid; i < n; i += kSThreads) {
+      const uint32_t rel = (uint32_t)(leaf_key(L, K[i], mask) - kmin);
+      R[i] = rel;
+      atomicAdd(&B[rel >> bshift], 1u);
+    }
+    __syncthreads();
+    block_scan_bins<kSThreads, (1 << kSBucketBits)>(B, B, s_warp);  // nbk <= 2^11; rest 0
+    for (uint32_t i = tid; i < n; i += kSThreads) X[atomicAdd(&B[R[i] >> bshift], 1u)] = (uint16_t)i;
+    __syncthreads();
+    // B[b] is now the end of bucket b
+    bool big = false;
+    for (uint32_t p = tid; p < n; p += kSThreads) {
+      const uint16_t x = X[p];
+      const uint32_t kx = R[x];
+      const uint32_t b = kx >> bshift;
+      const uint32_t lo = b ? B[b - 1] : 0u, hi = B[b];
+      if (hi - lo > (uint32_t)kCBig) {
+        big = true;
+        continue;
+      }
+      uint32_t rk = lo;
+      for (uint32_t j = lo; j < hi; ++j) {
+        const uint16_t y = X[j];
+        const uint32_t ky = R[y];
+        rk += (ky < kx || (ky == kx && y < x)) ? 1u : 0u;
+      }
+      F[rk] = x;
+    }
+    if (big) s_big = 1;
+    __syncthreads();
+    if (s_big) {  // skewed leaf: the block-level kernel sorts it
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      k += gridDim.x;
+      __syncthreads();
+      continue;
+    }
+    for (uint32_t j = tid; j < n; j += kSThreads) {
+      const uint16_t e = F[j];
+      const uint64_t g = (uint64_t)start + j;
+      L.keys_out[g] = K[e];
+      if (VALS) L.vals_out[g] = V[e];
+      if (want_pos) {
+        const uint32_t pos = P[e];
+        L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pos) : pos;
+      }
+    }
+    __syncthreads();  // shared arrays are reused by the next leaf
+    k += gridDim.x;
+  }
+}
+
+// ---------------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------------
 template <int LB, bool VALS>
@@ -684,7 +1232,85 @@ static cudaError_t launch_leafw(const LeafArgs& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-uint32_t leaf_cap() { return kLeafCap; }
+uint32_t leaf_cap() { return kCCap; }
+uint32_t cta_leaf_cap() { return kCCap; }
+
+template <bool VALS, bool BIG>
+static cudaError_t launch_leafc_t(const LeafArgs& L, uint32_t grid_cap, cudaStream_t s) {
+  static bool attr = false;
+  static int per_sm = 1;
+  constexpr size_t smem = leafc_smem(BIG);
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_leafc<VALS, BIG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leafc<VALS, BIG>, kCThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t persistent = (uint32_t)(sms * per_sm);
+  k_leafc<VALS, BIG><<<grid_cap < persistent ? grid_cap : persistent, kCThreads, smem, s>>>(L);
+  return cudaGetLastError();
+}
+
+template <bool VALS>
+static cudaError_t launch_leafr_t(const LeafArgs& L, cudaStream_t s) {
+  static bool attr = false;
+  static int per_sm = 1;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_leafr<VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kRSmem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leafr<VALS>, kCThreads, kRSmem);
+    if (per_sm < 1) per_sm = 1;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_leafr<VALS><<<sms * per_sm, kCThreads, kRSmem, s>>>(L);
+  const cudaError_t e = cudaGetLastError();
+  if (getenv("LCO_DEBUG"))
+    fprintf(stderr, "k_leafr grid %d smem %zu: %s\n", sms * per_sm, kRSmem, cudaGetErrorString(e));
+  return e;
+}
+
+template <bool VALS>
+static cudaError_t launch_leafs_t(const LeafArgs& L, cudaStream_t s) {
+  static bool attr = false;
+  static int per_sm = 1;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_leafs<VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSSmem);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leafs<VALS>, kSThreads, kSSmem);
+    if (per_sm < 1) per_sm = 1;
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_leafs<VALS><<<sms * per_sm, kSThreads, kSSmem, s>>>(L);
+  return cudaGetLastError();
+}
+
+// Leaf levels (defer list present): 32-bit keys when the leaf bits allow, two CTAs per
+// SM; the single-leaf call: 64-bit keys and the in-smem radix fallback.
+static cudaError_t launch_leafc(const LeafArgs& L, bool vals, bool single, uint32_t grid_cap,
+                                cudaStream_t s) {
+  if (getenv("LCO_DEBUG"))
+    fprintf(stderr, "launch_leafc: single %d rb %d level %d vals %d\n", (int)single, L.rb,
+            L.only_level, (int)vals);
+  if (!single && L.rb <= 32 && getenv("LCO_LEAFS"))
+    return vals ? launch_leafs_t<true>(L, s) : launch_leafs_t<false>(L, s);
+  if (!single && L.rb <= 32 && !getenv("LCO_NO_LEAFR"))
+    return vals ? launch_leafr_t<true>(L, s) : launch_leafr_t<false>(L, s);
+  if (single) return vals ? launch_leafc_t<true, true>(L, grid_cap, s) : launch_leafc_t<false, true>(L, grid_cap, s);
+  return vals ? launch_leafc_t<true, false>(L, grid_cap, s) : launch_leafc_t<false, false>(L, grid_cap, s);
+}
 
 // Workspace of the MSD schedule beyond the ping-pong buffers: the level-1 pass control
 // block, then the level-2 tables.
@@ -715,6 +1341,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   a.kp = kp;
   a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
   a.nnz = nnz;
+  a.ablate = getenv("LCO_ABLATE") ? atoi(getenv("LCO_ABLATE")) : 0;
   LeafArgs L;
   memset(&L, 0, sizeof L);
   L.a = a;
@@ -734,10 +1361,10 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   L.keys_out = io.keys_out;
   L.vals_out = io.vals_out;
   L.perm_out = io.perm_out;
-  if (mp.levels == 0) {
+  if (mp.levels == 0) {  // the whole input is one leaf (nnz <= kCCap)
     L.only_level = 0;
-    if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf");
-    return run_leaf(L, 1, vals, Lc.stream);
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_leafc");
+    return launch_leafc(L, vals, true, 1, Lc.stream);
   }
   // ---- level 1: stable global pass on the top b1 bits of q, into buffer A ----
   const int rb1 = pass_rb(mp.b1);
@@ -769,8 +1396,8 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     uint32_t* toff2 = reinterpret_cast<uint32_t*>(cb);
     cb += (tiles2 * rbins2 * 4 + 255) / 256 * 256;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
-    k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1, kLeafCap, ttab, tfirst,
-                                          tcnt, ntiles);
+    k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1,
+                                          mp.cta ? kCCap : kLeafCap, ttab, tfirst, tcnt, ntiles);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess)
       return e;
@@ -810,19 +1437,27 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     LeafArgs L2 = L;
     L2.only_level = 2;
     L2.rb = mp.rb;
-    if (Lc.mark) Lc.mark(Lc.ctx, "k_leafw");
-    if ((e = vals ? launch_leafw<true>(L2, Lc.stream) : launch_leafw<false>(L2, Lc.stream)) !=
-        cudaSuccess)
-      return e;
+    if (mp.cta) {
+      if (Lc.mark) Lc.mark(Lc.ctx, "k_leafc");
+      e = launch_leafc(L2, vals, false, 1u << 30, Lc.stream);
+    } else {
+      if (Lc.mark) Lc.mark(Lc.ctx, "k_leafw");
+      e = vals ? launch_leafw<true>(L2, Lc.stream) : launch_leafw<false>(L2, Lc.stream);
+    }
+    if (e != cudaSuccess) return e;
   }
   // level-1 buckets that were not split again sort the bits left after level 1
   LeafArgs L1 = L;
   L1.only_level = 1;
   L1.rb = mp.rb + (mp.levels == 2 ? mp.b2 : 0);
-  if (Lc.mark) Lc.mark(Lc.ctx, "k_leafw_l1");
-  if ((e = vals ? launch_leafw<true>(L1, Lc.stream) : launch_leafw<false>(L1, Lc.stream)) !=
-      cudaSuccess)
-    return e;
+  if (mp.cta) {
+    if (Lc.mark) Lc.mark(Lc.ctx, mp.levels == 2 ? "k_leafc_l1" : "k_leafc");
+    e = launch_leafc(L1, vals, false, 1u << 30, Lc.stream);
+  } else {
+    if (Lc.mark) Lc.mark(Lc.ctx, mp.levels == 2 ? "k_leafw_l1" : "k_leafw");
+    e = vals ? launch_leafw<true>(L1, Lc.stream) : launch_leafw<false>(L1, Lc.stream);
+  }
+  if (e != cudaSuccess) return e;
   // deferred leaves (both levels share one list; rb depends on the entry's level)
   if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf_deferred");
   LeafArgs LD = L;

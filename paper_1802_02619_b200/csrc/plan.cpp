@@ -78,6 +78,61 @@ void choose_passes(OpPlan* op, int bits) {
     op->kp.dbits[j] = (j < P - 1) ? b : bits - (P - 1) * b;
   }
   op->tile = 4096;
+  build_digit_moves(&op->kp);
+}
+
+// Power-of-two plans: every mode is a bit field of the key, so the LIV shuffle
+// is a set of bit-field moves.  Split each mode's field at bit 32 of the
+// NEW key so that every move lands inside one 32-bit output word.
+static void build_moves(KeyPlan* kp) {
+  kp->nmv = 0;
+  for (int m = 0; m < kp->n; ++m) {
+    int o = kp->oshift[m], nn = kp->nshift[m], w = kp->width[m];
+    while (w > 0) {
+      const int room = nn < 32 ? 32 - nn : 64 - nn;  // bits left in the output word
+      const int take = w < room ? w : room;
+      BitMove& mv = kp->mv[kp->nmv++];
+      mv.a = (uint8_t)o;
+      mv.hi = (uint8_t)(nn >= 32);
+      mv.b = (uint8_t)(nn >= 32 ? nn - 32 : nn);
+      mv.mask = take >= 32 ? 0xffffffffu : ((1u << take) - 1u);
+      mv.pad = 0;
+      o += take;
+      nn += take;
+      w -= take;
+    }
+  }
+}
+
+// Digit j of q = K' div T covers bits [log2 T + dshift[j], + dbits[j]) of K'; collect the
+// pieces of the mode fields that land there, as moves from the OLD key.
+void build_digit_moves(KeyPlan* kp) {
+  for (int j = 0; j < kMaxPasses; ++j) kp->ndmv[j] = -1;
+  if (!kp->pow2) return;
+  const int tbits = kp->divT.kind == 1 ? (int)kp->divT.s : 0;
+  if (kp->divT.kind == 2) return;
+  for (int j = 0; j < kp->passes && j < kMaxPasses; ++j) {
+    const int D = tbits + kp->dshift[j], E = D + kp->dbits[j];
+    int cnt = 0;
+    bool ok = true;
+    for (int m = 0; m < kp->n && ok; ++m) {
+      const int n0 = kp->nshift[m], n1 = n0 + kp->width[m];
+      const int x0 = n0 > D ? n0 : D, x1 = n1 < E ? n1 : E;
+      if (x0 >= x1) continue;
+      if (cnt >= kMaxDigitMoves) {
+        ok = false;
+        break;
+      }
+      BitMove& mv = kp->dmv[j][cnt++];
+      const int w = x1 - x0;
+      mv.a = (uint8_t)(kp->oshift[m] + (x0 - n0));
+      mv.hi = 0;
+      mv.b = (uint8_t)(x0 - D);
+      mv.mask = w >= 32 ? 0xffffffffu : ((1u << w) - 1u);
+      mv.pad = 0;
+    }
+    kp->ndmv[j] = ok ? cnt : -1;
+  }
 }
 
 static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64_t T) {
@@ -97,6 +152,7 @@ static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64
   }
   if (n == 0) kp.nstride[0] = 1;
   kp.divT = make_fastdiv(T);
+  for (int j = 0; j < kMaxPasses; ++j) kp.ndmv[j] = -1;
   kp.pow2 = n >= 1;
   for (int m = 0; m < n; ++m)
     if (nd[m] & (nd[m] - 1)) kp.pow2 = 0;
@@ -109,6 +165,7 @@ static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64
       acc_old += kp.width[m];
     }
     for (int m = 0; m < n; ++m) kp.nshift[m] = (uint8_t)__builtin_ctzll(kp.nstride[m]);
+    build_moves(&kp);
   }
   return kp;
 }

@@ -63,6 +63,7 @@ class PlanInfo(ctypes.Structure):
         ("tile", ctypes.c_int),
         ("msd_levels", ctypes.c_int),
         ("leaf_bits", ctypes.c_int),
+        ("leaf_kind", ctypes.c_int),
         ("model_bytes", ctypes.c_double),
     ]
 
@@ -207,6 +208,7 @@ class Plan:
             "tile": pi.tile,
             "msd_levels": pi.msd_levels,
             "leaf_bits": pi.leaf_bits,
+            "leaf_kind": {0: None, 1: "warp", 2: "cta"}.get(pi.leaf_kind, pi.leaf_kind),
             "model_bytes": pi.model_bytes,
         }
 

@@ -100,7 +100,7 @@ def test_baseline_config_plans():
     """Key bits the passes sort per BASELINE config (SURVEY.md §8(a) sizes table) and the
     schedule chosen at the config's nnz."""
     cases = {
-        ("C1", (64, 48, 32), (2, 0, 1), 5000): (5, "lsd"),
+        ("C1", (64, 48, 32), (2, 0, 1), 5000): (5, "leaf"),
         ("C2a", (512,) * 4, (2, 3, 0, 1), 1308672): (18, "lsd"),
         ("C2b", (512,) * 4, (0, 2, 1, 3), 1308672): (18, "lsd"),
         ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2), 14581760): (21, "lsd"),
@@ -125,6 +125,9 @@ def test_call_schedules():
     i = p.info(500_000_000)
     assert i["path"] == "msd" and i["msd_levels"] == 2
     assert sum(i["digit_bits"]) + i["leaf_bits"] == 48
+    # 8-bit MSD digits (runs of ~16 per tile), ~7.6K-nonzero leaves sorted by one CTA
+    assert i["digit_bits"] == [8, 8] and i["leaf_kind"] == "cta"
+    assert p.info(8192)["path"] == "leaf" and p.info(8193)["path"] == "msd"
     assert p.info(40_000)["msd_levels"] == 1
     assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54_484_996)["path"] == "lsd"
 
