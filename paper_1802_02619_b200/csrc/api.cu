@@ -42,6 +42,7 @@ struct CallPlan {
   MsdPlan msd;
   KeyPlan kp;
   double cost;  // modelled bytes per nonzero
+  uint64_t segdiv, segments;  // tile path: identity-prefix segments
 };
 
 CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
@@ -59,6 +60,16 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     c.msd.levels = 0;
     c.msd.rb = B;
     c.cost = 36;
+    return c;
+  }
+  // Identity prefix with small segments: every segment stays in place, so one on-chip
+  // sort per tile of whole segments finishes the permutation (one read, one write).
+  if (op.segments > 1 && nnz / op.segments <= 3072 && !getenv("LCO_NO_TILE")) {
+    c.path = kPathTile;
+    c.segdiv = op.segdiv;
+    c.segments = op.segments;
+    c.msd.rb = B;
+    c.cost = 40;
     return c;
   }
   c.path = kPathOnesweep;
@@ -97,7 +108,8 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
   // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
   // and with a clear modelled win.
-  if (op.segments == 1 && mcost < 0.75 * c.cost) {
+  const bool seg_ok = op.segments == 1 || getenv("LCO_MSD_SEG");
+  if (seg_ok && mcost < 0.75 * c.cost) {
     c.path = kPathMsd;
     c.msd = m;
     c.cost = mcost;
@@ -120,11 +132,14 @@ WsLayout layout_for(const CallPlan& c, uint64_t nnz) {
   WsLayout w;
   memset(&w, 0, sizeof w);
   size_t off = 0;
-  const bool lsd = c.path == kPathOnesweep, msd = c.path == kPathMsd;
-  if ((lsd || msd) && nnz > 0) {
+  const bool lsd = c.path == kPathOnesweep, msd = c.path == kPathMsd, tile = c.path == kPathTile;
+  if ((lsd || msd || tile) && nnz > 0) {
     w.ctrl = off;
-    off += align_up(lsd ? pass_ctrl_bytes(c.rb, nnz) : msd_ctrl_bytes(c.msd.b1, c.msd.b2, nnz));
-    if (msd || c.passes >= 2) {
+    off += align_up(lsd ? pass_ctrl_bytes(c.rb, nnz)
+                        : (msd ? msd_ctrl_bytes(c.msd.b1, c.msd.b2, nnz)
+                               : tile_ctrl_bytes(nnz, c.segments)));
+    // the tile path needs both buffers only as scratch of the rare streaming fallback
+    if (msd || tile || c.passes >= 2) {
       w.kA = off;
       off += align_up(nnz * 8);
       w.vA = off;
@@ -132,7 +147,7 @@ WsLayout layout_for(const CallPlan& c, uint64_t nnz) {
       w.pA = off;
       off += align_up(nnz * 4);
     }
-    if (msd || c.passes >= 3) {
+    if (msd || tile || c.passes >= 3) {
       w.kB = off;
       off += align_up(nnz * 8);
       w.vB = off;
@@ -297,8 +312,8 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
     io.perm_out = perm_out;
     io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
     const bool mv = vals_out != nullptr, mp = perm_out != nullptr;
-    const bool hasA = cp.path == kPathMsd || cp.passes >= 2;
-    const bool hasB = cp.path == kPathMsd || cp.passes >= 3;
+    const bool hasA = cp.path == kPathMsd || cp.path == kPathTile || cp.passes >= 2;
+    const bool hasB = cp.path == kPathMsd || cp.path == kPathTile || cp.passes >= 3;
     io.kA = hasA ? reinterpret_cast<uint64_t*>(ws + w.kA) : nullptr;
     io.vA = hasA && mv ? reinterpret_cast<double*>(ws + w.vA) : nullptr;
     io.pA = hasA && mp ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
@@ -306,6 +321,7 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
     io.vB = hasB && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
     io.pB = hasB && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
     if (cp.path == kPathOnesweep) e = run_passes(cp.rb, cp.kp, io, L);
+    else if (cp.path == kPathTile) e = run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
     else e = run_msd(cp.msd, cp.kp, io, L);
   }
   if (prof) prof_end(&pc);
@@ -572,15 +588,20 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   for (int j = 0; j < cp.passes && j < 8; ++j) info->digit_bits[j] = cp.kp.dbits[j];
   info->radix_bits = cp.path == kPathOnesweep ? cp.rb : (cp.path == kPathMsd ? 8 : 0);
   info->path = cp.path;
-  info->tile = cp.path == kPathOnesweep || cp.path == kPathMsd ? pass_tile() : 0;
+  info->tile = cp.path == kPathOnesweep || cp.path == kPathMsd
+                   ? pass_tile()
+                   : (cp.path == kPathTile ? (int)tile_nominal(nnz, cp.segments) : 0);
   info->msd_levels = cp.msd.levels;
   info->leaf_bits = cp.path == kPathMsd || cp.path == kPathLocal ? cp.msd.rb : 0;
-  info->leaf_kind = cp.path == kPathLocal ? 2 : (cp.path == kPathMsd ? (cp.msd.cta ? 2 : 1) : 0);
+  info->leaf_kind = (cp.path == kPathLocal || cp.path == kPathTile) ? 2
+                                                                     : (cp.path == kPathMsd ? (cp.msd.cta ? 2 : 1) : 0);
+  if (cp.path == kPathTile) info->leaf_bits = cp.msd.rb;
   info->model_bytes = cp.cost;
   // kernels of this library per call (cudaMemsetAsync not counted)
   int launches = 0;
   if (nnz > 0) {
     if (cp.path == kPathCopy || cp.path == kPathLocal) launches = 1;
+    else if (cp.path == kPathTile) launches = 3;  // bounds, tile sorts, deferred tiles
     else if (cp.path == kPathOnesweep) launches = 4 * cp.passes;
     else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 2;  // passes, leaves, deferred
   }

@@ -130,6 +130,7 @@ struct PassParams {
   const TileEntry* ttab;      // segmented mode: tile table (else tiles are t * kTile)
   const uint32_t* ntiles;     // segmented mode: number of valid table entries
   int ablate;                 // experiment hook (0 in production)
+  uint32_t pf_dist;           // L2 prefetch distance in tiles (resident CTAs), 0 = off
 };
 
 // Shaved key q = K' div T.
@@ -174,6 +175,14 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Bulk prefetch of [p, p + bytes) into L2 (no registers, no completion tracking).
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
+               : "memory");
+}
+
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");

@@ -285,6 +285,18 @@ __global__ void __launch_bounds__(NT, 2)
   uint64_t base;
   uint32_t n, seg;
   if (!tile_range(a, t, &base, &n, &seg)) return;
+  if (tid == 0 && a.pf_dist && !a.ttab) {
+    // the tile the CTA launched pf_dist later will load: bring it into L2 now, so its
+    // loads see L2 latency while HBM streams in the background
+    const uint64_t b2 = (uint64_t)(t + a.pf_dist) * kTile;
+    if (b2 < a.nnz) {
+      const size_t m = (size_t)umin64(kTile, a.nnz - b2);
+      prefetch_l2((FIRST ? io.keys_in : io.kin) + b2, m * 8);
+      if (VALS) prefetch_l2((FIRST ? io.vals_in : io.vin) + b2, m * 8);
+      if (!FIRST && io.pout) prefetch_l2(io.pin + b2, m * 4);
+      prefetch_l2(io.toff + (size_t)(t + a.pf_dist) * BINS, (size_t)BINS * 4);
+    }
+  }
   for (int i = tid; i < W * BINS / 2; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
   // ---- load keys; warp w owns a contiguous slice, lanes consecutive ----
   uint64_t key[IT];
@@ -656,6 +668,7 @@ cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch
   memset(&a, 0, sizeof a);
   a.kp = kp;
   a.ablate = getenv("LCO_ABLATE") ? atoi(getenv("LCO_ABLATE")) : 0;
+  a.pf_dist = getenv("LCO_PF") ? (uint32_t)atoi(getenv("LCO_PF")) : 0;
   if (part) a.kp.passes = 1;
   a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
   a.nnz = io.nnz;

@@ -79,6 +79,10 @@ uint32_t leaf_target();   // expected leaf size the MSD digits aim for (warp lea
 uint32_t cta_leaf_cap();  // largest leaf k_leafc sorts
 size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
 cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
+uint32_t tile_nominal(uint64_t nnz, uint64_t segments);  // segment-local path (msd.cu)
+size_t tile_ctrl_bytes(uint64_t nnz, uint64_t segments);
+cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int key_bits,
+                      const PassIO& io, const Launch& L);
 cudaError_t run_copy(uint64_t nnz, const uint64_t* keys_in, const double* vals_in,
                      const uint32_t* idx_in, uint64_t* keys_out, double* vals_out,
                      uint32_t* perm_out, const Launch& L);

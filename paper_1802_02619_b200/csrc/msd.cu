@@ -141,6 +141,10 @@ struct LeafArgs {
   uint32_t* ndefer;
   const uint32_t* dlist;   // block kernel: deferred list to drain (null: slot mode)
   const uint32_t* dcount;
+  // level 3: segment-aligned tiles of the raw input (k_tile_bounds), tstart[0..ntiles]
+  const uint32_t* tstart;
+  uint32_t ntiles;
+  int keymode;             // 0: sort on q = K' div T (rb low bits); 1: on K' (rb bits)
 };
 
 // A readable (K', V, position) array set.
@@ -167,7 +171,8 @@ struct LeafDesc {
 };
 
 __device__ __forceinline__ uint32_t leaf_slots(const LeafArgs& L, int level) {
-  return level == 0 ? 1u : (level == 1 ? (1u << L.b1) : (1u << (L.b1 + L.b2)));
+  return level == 0 ? 1u
+                    : (level == 1 ? (1u << L.b1) : (level == 2 ? (1u << (L.b1 + L.b2)) : L.ntiles));
 }
 
 // Leaf `slot` of MSD level `level` (0: the raw input as one leaf); false if empty or
@@ -180,9 +185,12 @@ __device__ __forceinline__ bool leaf_at(const LeafArgs& L, int level, uint32_t s
   } else if (level == 1) {
     if (L.levels == 2 && L.tcnt[slot] > 0) return false;  // split again at level 2
     *d = LeafDesc{L.bucket1[slot], L.totals1[slot], 1};
-  } else {
+  } else if (level == 2) {
     if (L.tcnt[slot >> L.b2] == 0) return false;
     *d = LeafDesc{L.base2[slot], L.btot[slot], 2};
+  } else {  // segment-aligned tile of the raw input
+    const uint32_t s0 = L.tstart[slot];
+    *d = LeafDesc{s0, L.tstart[slot + 1] - s0, 0};
   }
   return d->n > 0;
 }
@@ -205,20 +213,38 @@ __device__ __forceinline__ bool next_leaf(const LeafArgs& L, uint32_t& k, LeafDe
   return false;
 }
 
-// Sort key of a staged record: the leaf's remaining bits of q = K' div T.
+// Sort key of a staged record: the leaf's remaining bits of q = K' div T, or (tile path,
+// keymode 1) K' itself: within whole segments a stable sort on q equals the sort on K'
+// (equal q differ only in suffix modes, which the input already orders as the output
+// does), and unique K' leaves no ties however many nonzeros share a q.
 __device__ __forceinline__ uint64_t leaf_key(const LeafArgs& L, uint64_t k2, uint64_t mask) {
-  return q_of(L.a, k2) & mask;
+  return (L.keymode ? k2 : q_of(L.a, k2)) & mask;
 }
 
 // Block-wide stable counting sort of m <= kLeafCap indices by the LB-bit digit at
 // `shift` of the staged keys: per-warp contiguous slices, counts, then an in-order
 // ballot ranking sweep.  On return io holds the sorted indices, loff[d] the first slot
 // of digit d and cnt[d] its count.
+template <int LB, int NT, class KeyF>
+__device__ __forceinline__ void rank_pass(KeyF keyf, const uint16_t* ii, uint16_t* io,
+                                          uint32_t m, int shift, uint32_t* whist,
+                                          uint32_t* loff, uint32_t* cnt, uint32_t* s_warp);
+
 template <int LB, int NT = kLeafThreads>
 __device__ __forceinline__ void leaf_rank_pass(const LeafArgs& L, const uint64_t* Kp,
                                                uint64_t mask, const uint16_t* ii, uint16_t* io,
                                                uint32_t m, int shift, uint32_t* whist,
                                                uint32_t* loff, uint32_t* cnt, uint32_t* s_warp) {
+  rank_pass<LB, NT>([&](uint16_t x) { return leaf_key(L, Kp[x], mask); }, ii, io, m, shift, whist,
+                    loff, cnt, s_warp);
+}
+
+// One stable counting pass of m <= cap indices by the LB-bit digit at `shift` of
+// keyf(index): per-warp contiguous slices, counts, then an in-order ballot ranking sweep.
+template <int LB, int NT, class KeyF>
+__device__ __forceinline__ void rank_pass(KeyF keyf, const uint16_t* ii, uint16_t* io,
+                                          uint32_t m, int shift, uint32_t* whist,
+                                          uint32_t* loff, uint32_t* cnt, uint32_t* s_warp) {
   constexpr int BINS = 1 << LB;
   constexpr int kLeafWarps = NT / 32;
   constexpr int kLeafThreads = NT;
@@ -229,7 +255,7 @@ __device__ __forceinline__ void leaf_rank_pass(const LeafArgs& L, const uint64_t
   for (int i = tid; i < kLeafWarps * BINS; i += kLeafThreads) whist[i] = 0;
   __syncthreads();
   for (uint32_t i = s0 + lane; i < s1; i += 32)
-    atomicAdd(&wh[(uint32_t)(leaf_key(L, Kp[ii[i]], mask) >> shift) & (BINS - 1)], 1u);
+    atomicAdd(&wh[(uint32_t)(keyf(ii[i]) >> shift) & (BINS - 1)], 1u);
   __syncthreads();
   for (int d = tid; d < BINS; d += kLeafThreads) {
     uint32_t s = 0;
@@ -251,7 +277,7 @@ __device__ __forceinline__ void leaf_rank_pass(const LeafArgs& L, const uint64_t
     const uint32_t i = s0 + r * 32 + lane;
     const bool ok = i < s1;
     const uint16_t x = ok ? ii[i] : (uint16_t)0;
-    const uint32_t d = ok ? (uint32_t)(leaf_key(L, Kp[x], mask) >> shift) & (BINS - 1) : 0u;
+    const uint32_t d = ok ? (uint32_t)(keyf(x) >> shift) & (BINS - 1) : 0u;
     const uint32_t peers = peers_of<LB>(d, ok);
     const bool leader = ok && (peers & ltm) == 0;
     uint32_t before = 0;
@@ -448,7 +474,8 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(const __grid_constant__ L
         for (int d = tid; d < BINS; d += kLeafThreads) cnt[d] = 0;
         __syncthreads();
         for (uint32_t i = tid; i < n; i += kLeafThreads) {
-          const uint64_t k = __ldcs(rcur.k + (uint64_t)start + i);
+          const uint64_t kr = __ldcs(rcur.k + (uint64_t)start + i);
+          const uint64_t k = rcur.raw ? reencode(L.a.kp, kr) : kr;
           atomicAdd(&cnt[(uint32_t)(leaf_key(L, k, mask) >> shift) & (BINS - 1)], 1u);
         }
         __syncthreads();
@@ -649,15 +676,9 @@ constexpr int kCBucketBits = 12;
 constexpr int kCThreads = 512;
 constexpr int kCBig = 48;
 
-__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
-  const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + bytes + 15) & ~(uintptr_t)15;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a))
-               : "memory");
-}
 constexpr size_t leafc_smem(bool big) {
   return (size_t)kCCap * (8 + 2) + ((size_t)1 << kCBucketBits) * 4 +
-         (big ? (size_t)kCCap * 2 + (size_t)(kCThreads / 32) * 256 * 4 : 0);
+         (big ? (size_t)kCCap * (2 + 4) + (size_t)(kCThreads / 32) * 256 * 4 : 0);
 }
 
 template <bool VALS, bool BIG>
@@ -668,9 +689,10 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
   uint32_t* B = reinterpret_cast<uint32_t*>(X + kCCap);            // [2^12] buckets
   uint16_t* F = reinterpret_cast<uint16_t*>(B + (1 << kCBucketBits));  // BIG: [cap]
   uint32_t* WH = reinterpret_cast<uint32_t*>(F + kCCap);           // BIG: radix counters
+  uint32_t* Q = WH + (kCThreads / 32) * 256;                       // BIG: q - min q
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_loff[256], s_cnt[256];
-  __shared__ unsigned long long s_min, s_max;
+  __shared__ unsigned long long s_min, s_max, s_qmin, s_qmax;
   __shared__ int s_big;
   const int tid = threadIdx.x;
   const bool want_pos = L.perm_out != nullptr;
@@ -683,13 +705,13 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
     const double* sv = d.src == 0 ? L.vals_in : (d.src == 1 ? L.vA : L.vB);
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)kCCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       continue;
     }
     if (tid == 0) {
-      s_min = ~0ull;
-      s_max = 0ull;
+      s_min = s_qmin = ~0ull;
+      s_max = s_qmax = 0ull;
       s_big = 0;
     }
     if (d.src == 0) {  // raw input (the whole call is one leaf): re-encode while staging
@@ -704,12 +726,17 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
     }
     cp_async_wait<0>();
     __syncthreads();
-    {  // key range of the leaf
-      uint64_t mn = ~0ull, mx = 0ull;
+    {  // key range of the leaf (and, BIG, the range of q = K' div T)
+      uint64_t mn = ~0ull, mx = 0ull, qmn = ~0ull, qmx = 0ull;
       for (uint32_t i = tid; i < n; i += kCThreads) {
         const uint64_t kk = leaf_key(L, K[i], mask);
         mn = kk < mn ? kk : mn;
         mx = kk > mx ? kk : mx;
+        if (BIG) {
+          const uint64_t q = q_of(L.a, K[i]);
+          qmn = q < qmn ? q : qmn;
+          qmx = q > qmx ? q : qmx;
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -717,10 +744,20 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
         const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
         mn = a < mn ? a : mn;
         mx = b > mx ? b : mx;
+        if (BIG) {
+          const uint64_t c = __shfl_xor_sync(0xffffffffu, qmn, o);
+          const uint64_t e = __shfl_xor_sync(0xffffffffu, qmx, o);
+          qmn = c < qmn ? c : qmn;
+          qmx = e > qmx ? e : qmx;
+        }
       }
       if ((tid & 31) == 0) {
         atomicMin(&s_min, (unsigned long long)mn);
         atomicMax(&s_max, (unsigned long long)mx);
+        if (BIG) {
+          atomicMin(&s_qmin, (unsigned long long)qmn);
+          atomicMax(&s_qmax, (unsigned long long)qmx);
+        }
       }
     }
     int lg = 0;
@@ -730,9 +767,13 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
     for (uint32_t b = tid; b < nbk; b += kCThreads) B[b] = 0;
     __syncthreads();
     const uint64_t kmin = s_min, range = s_max - s_min;
-    int rbits = 0;
-    while (rbits < 64 && (range >> rbits) != 0) ++rbits;
+    const int rbits = range ? 64 - __clzll((long long)range) : 0;
     const int bshift = rbits > tb ? rbits - tb : 0;
+    // BIG (tile path): few distinct q (many nonzeros share their prefix + middle modes,
+    // e.g. a stencil row) -> straight to stable radix passes on q - min q
+    const uint64_t qrange = BIG ? s_qmax - s_qmin : 0;
+    const bool q_radix = BIG && qrange < 0xffffffffull && qrange < 2ull * n;
+    if (!q_radix) {
     for (uint32_t i = tid; i < n; i += kCThreads)
       atomicAdd(&B[(uint32_t)((leaf_key(L, K[i], mask) - kmin) >> bshift)], 1u);
     __syncthreads();
@@ -798,22 +839,39 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
       }
     }
     __syncthreads();
+    }  // !q_radix
     const uint16_t* order = X;
-    if (s_big) {
+    if (s_big || q_radix) {
       if constexpr (BIG) {  // stable LSD radix passes of 8 bits on chip
         uint16_t* xa = X;
         uint16_t* xb = F;
-        for (uint32_t i = tid; i < n; i += kCThreads) xa[i] = (uint16_t)i;
+        const bool on_q = qrange < 0xffffffffull;
+        const uint64_t qmin = s_qmin;
+        for (uint32_t i = tid; i < n; i += kCThreads) {
+          xa[i] = (uint16_t)i;
+          if (on_q) Q[i] = (uint32_t)(q_of(L.a, K[i]) - qmin);
+        }
         __syncthreads();
-        for (int sh = 0; sh < L.rb; sh += 8) {
-          leaf_rank_pass<8, kCThreads>(L, K, mask, xa, xb, n, sh, WH, s_loff, s_cnt, s_warp);
-          uint16_t* t = xa;
-          xa = xb;
-          xb = t;
+        if (on_q) {  // stable on q (ties: input order = suffix order) over its range bits
+          const int qbits = qrange ? 64 - __clzll((long long)qrange) : 0;
+          for (int sh = 0; sh < qbits; sh += 8) {
+            rank_pass<8, kCThreads>([&](uint16_t x) { return (uint64_t)Q[x]; }, xa, xb, n, sh, WH,
+                                    s_loff, s_cnt, s_warp);
+            uint16_t* t = xa;
+            xa = xb;
+            xb = t;
+          }
+        } else {
+          for (int sh = 0; sh < L.rb; sh += 8) {
+            leaf_rank_pass<8, kCThreads>(L, K, mask, xa, xb, n, sh, WH, s_loff, s_cnt, s_warp);
+            uint16_t* t = xa;
+            xa = xb;
+            xb = t;
+          }
         }
         order = xa;
       } else {  // skewed leaf: the block-level kernel sorts it
-        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
         __syncthreads();
         k += gridDim.x;
         continue;
@@ -884,7 +942,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     const double* sv = d.src == 1 ? L.vA : L.vB;
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)kCCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       continue;
     }
@@ -930,7 +988,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     const uint64_t kmin = s_min, range = s_max - s_min;
     const int rbits = range ? 64 - __clzll((long long)range) : 0;
     if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       __syncthreads();
       continue;
@@ -1010,7 +1068,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     if (big) s_big = 1;
     __syncthreads();
     if (s_big) {  // skewed leaf: the block-level kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       __syncthreads();  // everyone has read s_big before the next leaf resets it
       continue;
@@ -1084,7 +1142,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
     const double* sv = d.src == 1 ? L.vA : L.vB;
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)kSCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       continue;
     }
@@ -1099,9 +1157,8 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       s_max = 0ull;
       s_big = 0;
     }
-    int lg = 0;
-    while ((1u << lg) < n) ++lg;
-    const int tb = min(max(lg - 1, 1), kSBucketBits);
+    const int lg = n > 1 ? 32 - __clz((int)(n - 1)) : 0;  // ceil(log2 n)
+    const int tb = min(max(lg, 1), kSBucketBits);          // ~1 nonzero per bucket
     const uint32_t nbk = 1u << tb;
     for (uint32_t b = tid; b < nbk; b += kSThreads) B[b] = 0;
     cp_async_wait<0>();
@@ -1127,7 +1184,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
     const uint64_t kmin = s_min, range = s_max - s_min;
     const int rbits = range ? 64 - __clzll((long long)range) : 0;
     if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       __syncthreads();
       continue;
@@ -1149,6 +1206,10 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       const uint32_t kx = R[x];
       const uint32_t b = kx >> bshift;
       const uint32_t lo = b ? B[b - 1] : 0u, hi = B[b];
+      if (hi - lo == 1u) {  // the common case: alone in its bucket
+        F[lo] = x;
+        continue;
+      }
       if (hi - lo > (uint32_t)kCBig) {
         big = true;
         continue;
@@ -1164,7 +1225,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
     if (big) s_big = 1;
     __syncthreads();
     if (s_big) {  // skewed leaf: the block-level kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)d.src << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       __syncthreads();
       continue;
@@ -1312,6 +1373,104 @@ static cudaError_t launch_leafc(const LeafArgs& L, bool vals, bool single, uint3
   return vals ? launch_leafc_t<true, false>(L, grid_cap, s) : launch_leafc_t<false, false>(L, grid_cap, s);
 }
 
+// ---------------------------------------------------------------------------------
+// Segment-local schedule ("tile" path).  With an identity prefix the output keeps every
+// segment of constant prefix coordinates in place ("regions where k is
+// constant"), so when segments are small the whole permutation is one
+// on-chip sort per tile of whole segments: one read and one write of every nonzero.
+// k_tile_bounds cuts the input into tiles that start at segment boundaries
+// (tstart[c] = first boundary >= c * T, found by binary search on the sorted keys);
+// k_leafc sorts each tile on q = K' div T (stable: ties keep input order); a tile
+// holding a segment too large for shared memory goes to the deferred list.
+// ---------------------------------------------------------------------------------
+__global__ void k_tile_bounds(const uint64_t* __restrict__ keys, uint64_t nnz, FastDiv segd,
+                              uint64_t D, uint32_t T, uint32_t ntiles, uint32_t* __restrict__ tstart) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > ntiles) return;
+  const uint64_t x = (uint64_t)c * T;
+  if (c == 0 || x >= nnz) {
+    tstart[c] = c == 0 ? 0u : (uint32_t)nnz;
+    return;
+  }
+  const uint64_t sprev = fdiv(segd, __ldg(keys + x - 1));
+  if (fdiv(segd, __ldg(keys + x)) != sprev) {
+    tstart[c] = (uint32_t)x;
+    return;
+  }
+  const uint64_t bound = (sprev + 1) * D;  // first key of the next segment, <= prod(dims)
+  uint64_t lo = x + 1, hi = nnz;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (__ldg(keys + mid) < bound) lo = mid + 1;
+    else hi = mid;
+  }
+  tstart[c] = (uint32_t)lo;
+}
+
+uint32_t tile_nominal(uint64_t nnz, uint64_t segments) {
+  const uint64_t avg = segments ? (nnz + segments - 1) / segments : nnz;
+  const uint64_t t = (uint64_t)kCCap > 2 * avg + 2048 ? kCCap - 2 * avg : 2048;
+  return (uint32_t)(t / 256 * 256);
+}
+
+size_t tile_ctrl_bytes(uint64_t nnz, uint64_t segments) {
+  const uint64_t nt = (nnz + tile_nominal(nnz, segments) - 1) / tile_nominal(nnz, segments);
+  return ((nt + 1) * 4 + 255) / 256 * 256 + (nt + 64) * 4 + 256;
+}
+
+cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int key_bits,
+                      const PassIO& io, const Launch& Lc) {
+  cudaError_t e;
+  const uint64_t nnz = io.nnz;
+  const bool vals = io.vals_out != nullptr;
+  const uint32_t T = tile_nominal(nnz, segments);
+  const uint32_t nt = (uint32_t)((nnz + T - 1) / T);
+  uint32_t* tstart = io.ctrl;
+  uint32_t* defer = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(io.ctrl) +
+                                                ((size_t)(nt + 1) * 4 + 255) / 256 * 256);
+  uint32_t* ndefer = defer + nt + 32;
+  if ((e = cudaMemsetAsync(ndefer, 0, 4, Lc.stream)) != cudaSuccess) return e;
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_tile_bounds");
+  k_tile_bounds<<<(nt + 1 + 255) / 256, 256, 0, Lc.stream>>>(io.keys_in, nnz, make_fastdiv(segdiv),
+                                                            segdiv, T, nt, tstart);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  LeafArgs L;
+  memset(&L, 0, sizeof L);
+  L.a.kp = kp;
+  L.a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
+  L.a.nnz = nnz;
+  L.levels = 3;
+  L.only_level = 3;
+  L.keymode = 1;
+  L.rb = key_bits;  // tiles sort on K' (all key bits; the key range of a tile is small)
+  L.cap = kLeafCap;
+  L.keys_in = io.keys_in;
+  L.vals_in = io.vals_in;
+  L.idx_in = io.idx_in;
+  L.kA = io.kA;
+  L.vA = io.vA;
+  L.pA = io.pA;
+  L.kB = io.kB;
+  L.vB = io.vB;
+  L.pB = io.pB;
+  L.keys_out = io.keys_out;
+  L.vals_out = io.vals_out;
+  L.perm_out = io.perm_out;
+  L.tstart = tstart;
+  L.ntiles = nt;
+  L.defer = defer;
+  L.ndefer = ndefer;
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_leafc_tiles");
+  e = vals ? launch_leafc_t<true, true>(L, 1u << 30, Lc.stream)
+           : launch_leafc_t<false, true>(L, 1u << 30, Lc.stream);
+  if (e != cudaSuccess) return e;
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf_deferred");
+  LeafArgs LD = L;
+  LD.dlist = defer;
+  LD.dcount = ndefer;
+  return run_leaf(LD, 1u << 20, vals, Lc.stream);
+}
+
 // Workspace of the MSD schedule beyond the ping-pong buffers: the level-1 pass control
 // block, then the level-2 tables.
 size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz) {
@@ -1342,6 +1501,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
   a.nnz = nnz;
   a.ablate = getenv("LCO_ABLATE") ? atoi(getenv("LCO_ABLATE")) : 0;
+  a.pf_dist = getenv("LCO_PF") ? (uint32_t)atoi(getenv("LCO_PF")) : 0;
   LeafArgs L;
   memset(&L, 0, sizeof L);
   L.a = a;
