@@ -102,7 +102,7 @@ def test_baseline_config_plans():
     cases = {
         ("C1", (64, 48, 32), (2, 0, 1), 5000): (5, "leaf"),
         ("C2a", (512,) * 4, (2, 3, 0, 1), 1308672): (18, "lsd"),
-        ("C2b", (512,) * 4, (0, 2, 1, 3), 1308672): (18, "lsd"),
+        ("C2b", (512,) * 4, (0, 2, 1, 3), 1308672): (18, "tile"),
         ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2), 14581760): (21, "lsd"),
         ("C3b", (128,) * 6, (0, 3, 1, 4, 2, 5), 14581760): (28, "lsd"),
         ("C4", (2048,) * 4, (1, 0, 2, 3), 54484996): (11, "lsd"),
@@ -111,7 +111,11 @@ def test_baseline_config_plans():
     for (name, dims, perm, nnz), (bits, path) in cases.items():
         info = lco.Plan(dims, perm).info(nnz)
         assert (info["sort_bits"], info["path"]) == (bits, path), (name, info)
-        assert sum(info["digit_bits"]) + info["leaf_bits"] == bits
+        if path != "tile":  # the tile path sorts each tile on chip on K' (no passes)
+            assert sum(info["digit_bits"]) + info["leaf_bits"] == bits
+    # C2b: 512 segments of ~2.5K nonzeros (the x rows), sorted in place tile by tile
+    c2b = lco.Plan((512,) * 4, (0, 2, 1, 3)).info(1308672)
+    assert c2b["num_segments"] == 512 and c2b["leaf_kind"] == "cta" and c2b["launches"] == 3
     c4 = lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54484996)
     assert c4["norm_dims"] == [2048, 2048, 2 ** 22] and c4["norm_perm"] == [1, 0, 2]
     assert c4["trailing"] == 2048 * 2 ** 22 and c4["passes"] == 1
