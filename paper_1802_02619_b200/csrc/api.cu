@@ -102,7 +102,7 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     mcost = 8 + 36 + 8 + 40 + 40;
   }
   if (getenv("LCO_MSD_B1")) m.b1 = atoi(getenv("LCO_MSD_B1"));  // experiment hooks
-  if (getenv("LCO_MSD_B2")) m.b2 = atoi(getenv("LCO_MSD_B2"));
+  if (getenv("LCO_MSD_B2") && m.levels == 2) m.b2 = atoi(getenv("LCO_MSD_B2"));
   if (getenv("LCO_MSD_CTA")) m.cta = atoi(getenv("LCO_MSD_CTA"));
   m.rb = B - m.b1 - m.b2;
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,

@@ -340,3 +340,72 @@ def test_combinatorial_laplacian_all_perms(cuda_device):
     for perm in itertools.permutations(range(4)):
         check((63,) * 4, perm, keys, vals)
         check((63,) * 4, perm, keys, vals, sort=True)
+
+
+# ------------------------------------------------------------------ segment-local tiles
+def _prefix_tensor(rng, seg_sizes, inner_dims):
+    """Sorted unique keys of (len(seg_sizes),) + inner_dims where segment s (mode 0 = s)
+    holds seg_sizes[s] random nonzeros."""
+    inner = int(np.prod(inner_dims))
+    keys = []
+    for s, m in enumerate(seg_sizes):
+        m = min(m, inner)
+        keys.append(s * inner + np.sort(rng.choice(inner, m, replace=False)))
+    return np.concatenate(keys).astype(np.uint64)
+
+
+def test_tile_path_random_segments(cuda_device):
+    """Identity prefix with small segments: one on-chip sort per tile of whole segments
+    (tile boundaries found by binary search on the keys), including ragged segment
+    sizes, empty segments and a tail tile."""
+    rng = np.random.default_rng(41)
+    inner = (37, 64, 29)
+    sizes = rng.integers(0, 2500, 300)
+    sizes[::17] = 0
+    keys = _prefix_tensor(rng, sizes, inner)
+    dims = (len(sizes),) + inner
+    for perm in [(0, 2, 1, 3), (0, 3, 2, 1), (0, 1, 3, 2), (0, 3, 1, 2)]:
+        assert lco.plan(dims, perm).info(len(keys))["path"] == "tile", perm
+        check(dims, perm, keys, rng.standard_normal(len(keys)))
+
+
+def test_tile_path_oversize_segment(cuda_device):
+    """A segment larger than an on-chip tile goes to the deferred streaming sort (raw
+    input re-encoded on the fly), the other tiles stay on chip."""
+    rng = np.random.default_rng(42)
+    inner = (128, 96, 16)
+    sizes = np.full(400, 300)
+    sizes[123] = 60_000
+    keys = _prefix_tensor(rng, sizes, inner)
+    dims = (len(sizes),) + inner
+    assert lco.plan(dims, (0, 3, 1, 2)).info(len(keys))["path"] == "tile"
+    check(dims, (0, 3, 1, 2), keys, rng.standard_normal(len(keys)))
+    check(dims, (0, 2, 3, 1), keys, None)
+
+
+def test_tile_path_clustered_q(cuda_device):
+    """C2b-like: thousands of nonzeros share each (prefix, middle) value; the tile sort
+    takes stable radix passes on q (ties keep input order = suffix order)."""
+    w = workloads.config("C2", scale=160)
+    dims, perm = w.dims, (0, 2, 1, 3)
+    assert lco.plan(dims, perm).info(w.keys.numel())["path"] == "tile"
+    check(dims, perm, _np_u64(w.keys), w.vals.numpy())
+    check(dims, perm, _np_u64(w.keys), w.vals.numpy(), return_perm=False)
+
+
+@pytest.mark.parametrize("env", [{}, {"LCO_LEAFS": "1", "LCO_MSD_B1": "9", "LCO_MSD_B2": "9"},
+                                 {"LCO_NO_LEAFR": "1"}])
+def test_msd_leaf_variants(env, cuda_device, monkeypatch):
+    """8+8 MSD levels with 32-bit-key CTA leaves (default), 9+9 levels with fully staged
+    leaves, and 64-bit-key CTA leaves: all bit-exact."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(43)
+    dims = (4096,) * 5
+    for n, levels in ((14_000_000, 2), (1_000_000, 1)):
+        keys = np.unique(rng.integers(0, 2 ** 60, n + n // 20, dtype=np.int64))[:n]
+        keys = keys.astype(np.uint64)
+        info = lco.plan(dims, (4, 3, 2, 1, 0)).info(len(keys))
+        assert info["msd_levels"] == levels and info["leaf_kind"] == "cta"
+        check(dims, (4, 3, 2, 1, 0), keys, rng.standard_normal(len(keys)))
+        check(dims, (1, 4, 0, 3, 2), keys, None)
