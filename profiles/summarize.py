@@ -15,7 +15,7 @@ import subprocess
 import sys
 
 OURS = ("k_count", "k_scan", "k_offsets", "k_scatter", "k_msd_tiles", "k_offsets_seg",
-        "k_leaf", "k_copy", "k_keyhist", "k_validate")
+        "k_leaf", "k_copy", "k_keyhist", "k_validate", "k_tile_bounds")
 
 
 def short(name):
