@@ -76,6 +76,28 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   c.passes = op.passes;
   c.rb = op.radix_bits;
   c.cost = 4 + 48.0 * op.passes;
+  // Identity prefix with large segments and a power-of-two middle of <= 11 bits: one
+  // stable pass of the middle digit inside every segment (segment starts from a count of
+  // the prefix digit), straight from the input to the outputs.
+  {
+    const int gb = ceil_log2(op.segments), mb = ceil_log2(op.middle);
+    const bool pow2_mid = (op.middle & (op.middle - 1)) == 0;
+    if (op.segments > 1 && gb <= 10 && mb >= 1 && mb <= 11 && pow2_mid && op.passes >= 2 &&
+        !getenv("LCO_NO_SEG")) {
+      c.path = kPathSeg;
+      c.passes = 1;
+      c.msd.b1 = gb;
+      c.msd.b2 = mb;
+      c.cost = 52;
+      c.kp.passes = 2;
+      c.kp.dshift[0] = mb;
+      c.kp.dbits[0] = gb;
+      c.kp.dshift[1] = 0;
+      c.kp.dbits[1] = mb;
+      build_digit_moves(&c.kp);
+      return c;
+    }
+  }
   if (B <= 11) return c;
   // MSD levels of 8-bit digits (a 4,096-nonzero tile then writes runs of ~16 nonzeros
   // per digit, which the HBM write path sustains; 10-11-bit digits write runs of 2-4 and
@@ -133,11 +155,12 @@ WsLayout layout_for(const CallPlan& c, uint64_t nnz) {
   memset(&w, 0, sizeof w);
   size_t off = 0;
   const bool lsd = c.path == kPathOnesweep, msd = c.path == kPathMsd, tile = c.path == kPathTile;
-  if ((lsd || msd || tile) && nnz > 0) {
+  const bool seg = c.path == kPathSeg;
+  if ((lsd || msd || tile || seg) && nnz > 0) {
     w.ctrl = off;
     off += align_up(lsd ? pass_ctrl_bytes(c.rb, nnz)
-                        : (msd ? msd_ctrl_bytes(c.msd.b1, c.msd.b2, nnz)
-                               : tile_ctrl_bytes(nnz, c.segments)));
+                        : ((msd || seg) ? msd_ctrl_bytes(c.msd.b1, c.msd.b2, nnz)
+                                        : tile_ctrl_bytes(nnz, c.segments)));
     // the tile path needs both buffers only as scratch of the rare streaming fallback
     if (msd || tile || c.passes >= 2) {
       w.kA = off;
@@ -322,6 +345,7 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
     io.pB = hasB && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
     if (cp.path == kPathOnesweep) e = run_passes(cp.rb, cp.kp, io, L);
     else if (cp.path == kPathTile) e = run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
+    else if (cp.path == kPathSeg) e = run_seg(cp.msd.b1, cp.msd.b2, cp.kp, io, L);
     else e = run_msd(cp.msd, cp.kp, io, L);
   }
   if (prof) prof_end(&pc);
@@ -586,7 +610,9 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   const CallPlan cp = choose_plan(op, nnz);
   info->passes = cp.passes;
   for (int j = 0; j < cp.passes && j < 8; ++j) info->digit_bits[j] = cp.kp.dbits[j];
-  info->radix_bits = cp.path == kPathOnesweep ? cp.rb : (cp.path == kPathMsd ? 8 : 0);
+  if (cp.path == kPathSeg) info->digit_bits[0] = cp.msd.b2;  // the middle digit
+  info->radix_bits = cp.path == kPathOnesweep ? cp.rb
+                                                : (cp.path == kPathMsd ? 8 : (cp.path == kPathSeg ? pass_rb(cp.msd.b2) : 0));
   info->path = cp.path;
   info->tile = cp.path == kPathOnesweep || cp.path == kPathMsd
                    ? pass_tile()
@@ -602,6 +628,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   if (nnz > 0) {
     if (cp.path == kPathCopy || cp.path == kPathLocal) launches = 1;
     else if (cp.path == kPathTile) launches = 3;  // bounds, tile sorts, deferred tiles
+    else if (cp.path == kPathSeg) launches = 6;   // count, scan, tiles, count, offsets, scatter
     else if (cp.path == kPathOnesweep) launches = 4 * cp.passes;
     else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 2;  // passes, leaves, deferred
   }

@@ -605,9 +605,10 @@ ScatterIO pass_buffers(const PassIO& io, int j, bool last, const uint32_t* toff)
   return s;
 }
 
-// One unsegmented pass: count -> scan -> offsets -> scatter.
+// One unsegmented pass: count -> scan -> offsets -> scatter (count_only: stop after the
+// scan, leaving digit totals and bucket starts in the control block).
 cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool first,
-                     bool last, const Launch& L) {
+                     bool last, const Launch& L, bool count_only) {
   const int BINS = 1 << rb;
   const PassCtrl c = pass_ctrl_layout(rb, io.nnz, io.ctrl);
   PassParams a = a0;
@@ -644,6 +645,7 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
       break;
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (count_only) return cudaSuccess;
   if (L.mark) L.mark(L.ctx, "k_offsets");
   switch (rb) {
     case 8: k_offsets<8><<<c.nchunks, kThreads, 0, L.stream>>>(a, c.thist, c.csum, c.bucket, c.toff); break;

@@ -72,7 +72,7 @@ cudaError_t launch_scatter(int rb, bool first, bool last, bool vals, const PassP
                            const ScatterIO& io, uint32_t grid, cudaStream_t s);
 ScatterIO pass_buffers(const PassIO& io, int j, bool last, const uint32_t* toff);
 cudaError_t run_pass(int rb, const PassParams& a, const PassIO& io, int j, bool first, bool last,
-                     const Launch& L);
+                     const Launch& L, bool count_only = false);
 cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
 uint32_t leaf_cap();      // largest leaf one CTA sorts in shared memory
 uint32_t leaf_target();   // expected leaf size the MSD digits aim for (warp leaves)
@@ -80,6 +80,7 @@ uint32_t cta_leaf_cap();  // largest leaf k_leafc sorts
 size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
 cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
 uint32_t tile_nominal(uint64_t nnz, uint64_t segments);  // segment-local path (msd.cu)
+cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const Launch& L);
 size_t tile_ctrl_bytes(uint64_t nnz, uint64_t segments);
 cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int key_bits,
                       const PassIO& io, const Launch& L);

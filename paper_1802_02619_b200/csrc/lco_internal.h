@@ -197,7 +197,8 @@ LCO_HD uint32_t digit_of(const KeyPlan& p, uint64_t q, int pass) {
   return (uint32_t)(q >> p.dshift[pass]) & ((1u << p.dbits[pass]) - 1u);
 }
 
-enum Path { kPathCopy = 0, kPathOnesweep = 1, kPathLocal = 2, kPathMsd = 3, kPathTile = 4 };
+enum Path { kPathCopy = 0, kPathOnesweep = 1, kPathLocal = 2, kPathMsd = 3, kPathTile = 4,
+            kPathSeg = 5 };
 
 // Host plan for one operation (permute or sort) of a handle.
 struct OpPlan {

@@ -1471,6 +1471,76 @@ cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int
   return run_leaf(LD, 1u << 20, vals, Lc.stream);
 }
 
+// ---------------------------------------------------------------------------------
+// Segmented single pass ("seg" path): identity-prefix segments too large for a tile and
+// a middle of <= 11 bits.  Segments keep their position ranges, so only
+// the middle digit is sorted, inside every segment, in one stable pass straight from
+// the input to the outputs ("sorting can be performed on each of these
+// regions"):
+//   count + scan of the prefix digit -> segment sizes and starts (no data movement);
+//   k_msd_tiles -> tiles that never straddle a segment;
+//   k_count (segment mode) -> per-tile middle-digit histograms and segment totals;
+//   k_offsets_seg -> per-tile offsets; k_scatter (first and last pass, segment mode).
+// kp: pass 0 = the prefix digit (gb bits above the mb middle bits), pass 1 = the middle.
+// ---------------------------------------------------------------------------------
+cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const Launch& Lc) {
+  cudaError_t e;
+  const uint64_t nnz = io.nnz;
+  const bool vals = io.vals_out != nullptr;
+  PassParams a;
+  memset(&a, 0, sizeof a);
+  a.kp = kp;
+  a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
+  a.nnz = nnz;
+  const int rb1 = pass_rb(gb);
+  char* cb = reinterpret_cast<char*>(io.ctrl);
+  PassIO io1 = io;
+  io1.ctrl = reinterpret_cast<uint32_t*>(cb);
+  cb += (pass_ctrl_bytes(rb1, nnz) + 255) / 256 * 256;
+  if ((e = run_pass(rb1, a, io1, 0, true, false, Lc, true)) != cudaSuccess) return e;
+  const PassCtrl c1 = pass_ctrl_layout(rb1, nnz, io1.ctrl);
+  const uint32_t nb1 = 1u << gb;
+  const int rb2 = pass_rb(mb);
+  const size_t rbins2 = (size_t)1 << rb2;
+  const uint64_t tiles2 = pass_tiles(nnz) + nb1;
+  TileEntry* ttab = reinterpret_cast<TileEntry*>(cb);
+  cb += (tiles2 * sizeof(TileEntry) + 255) / 256 * 256;
+  uint32_t* tfirst = reinterpret_cast<uint32_t*>(cb);
+  uint32_t* tcnt = tfirst + nb1;
+  uint32_t* ntiles = tcnt + nb1;
+  cb += ((size_t)nb1 * 12 + 4 + 255) / 256 * 256;
+  uint32_t* btot = reinterpret_cast<uint32_t*>(cb);
+  uint32_t* base2 = btot + (size_t)nb1 * rbins2;
+  cb += ((size_t)nb1 * rbins2 * 8 + 255) / 256 * 256;
+  uint16_t* thist2 = reinterpret_cast<uint16_t*>(cb);
+  cb += (tiles2 * rbins2 * 2 + 255) / 256 * 256;
+  uint32_t* toff2 = reinterpret_cast<uint32_t*>(cb);
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
+  k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1, 0u, ttab, tfirst, tcnt,
+                                        ntiles);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess) return e;
+  PassParams a2 = a;
+  a2.pass = 1;
+  a2.ttab = ttab;
+  a2.ntiles = ntiles;
+  a2.tiles = (uint32_t)tiles2;
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_count_seg");
+  if ((e = launch_count(rb2, true, a2, io.keys_in, thist2, btot, (uint32_t)tiles2, Lc.stream)) !=
+      cudaSuccess)
+    return e;
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg");
+  switch (rb2) {
+    case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+    case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+    case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const ScatterIO sio = pass_buffers(io, 0, true, toff2);
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_scatter_single");
+  return launch_scatter(rb2, true, true, vals, a2, sio, (uint32_t)tiles2, Lc.stream);
+}
+
 // Workspace of the MSD schedule beyond the ping-pong buffers: the level-1 pass control
 // block, then the level-2 tables.
 size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz) {

@@ -409,3 +409,22 @@ def test_msd_leaf_variants(env, cuda_device, monkeypatch):
         assert info["msd_levels"] == levels and info["leaf_kind"] == "cta"
         check(dims, (4, 3, 2, 1, 0), keys, rng.standard_normal(len(keys)))
         check(dims, (1, 4, 0, 3, 2), keys, None)
+
+
+# ------------------------------------------------------------------ segmented single pass
+@pytest.mark.parametrize("dims,perm,nnz", [((256, 16, 64, 32), (0, 2, 1, 3), 1_000_000),
+                                           ((128, 16, 2048, 4), (0, 2, 1, 3), 1_000_000),
+                                           ((1000, 8, 16, 64), (0, 3, 1, 2), 5_000_000),
+                                           ((128, 8, 8, 128, 8, 8), (0, 3, 1, 2, 4, 5), 1_000_000)])
+def test_seg_path(dims, perm, nnz, cuda_device):
+    """Identity prefix with large segments and a power-of-two middle of <= 11 bits: one
+    stable pass of the middle digit inside every segment (segments found by a count of
+    the prefix digit), incl. empty segments and multi-tile segments with ragged tails."""
+    rng = np.random.default_rng(51)
+    keys, vals = _rand_sorted(rng, dims, nnz)
+    keys = keys[(keys // int(np.prod(dims[1:]))) % 5 != 3]  # some empty segments
+    vals = vals[: len(keys)]
+    info = lco.plan(dims, perm).info(len(keys))
+    assert info["path"] == "seg", info["path"]
+    check(dims, perm, keys, vals)
+    check(dims, perm, keys, None, return_perm=False)
