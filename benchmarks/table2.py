@@ -68,12 +68,25 @@ def run(name, keys, vals, dims, reps):
         t_sort = timed(lambda: p.sort(keys, vals, out=out_s, workspace=ws), reps)
         same = all(torch.equal(x, y) for x, y in zip(out_p, out_s))
         ip, isr = p.info(n), p.info(n, sort=True)
+        # the hierarchical plan (LCO_FLAG_HIERARCHICAL): one stable sort per run of
+        # rearrangement indices, where the permutation has >= 2 runs
+        t_h, h_paths = None, None
+        if ip["stages"] >= 2:
+            ph = lco.Plan(dims, perm, hierarchical=True)
+            wsh = torch.empty(ph.workspace_size(n) + 256, dtype=torch.uint8, device=keys.device)
+            out_h = (torch.empty_like(keys), torch.empty_like(vals),
+                     torch.empty(n, dtype=torch.int32, device=keys.device))
+            t_h = timed(lambda: ph.permute(keys, vals, out=out_h, workspace=wsh), reps)
+            same = same and all(torch.equal(x, y) for x, y in zip(out_p, out_h))
+            h_paths = ph.info(n)["stage_paths"]
+            del wsh, out_h
         lex = perm_to_lex(perm)
         rows.append({"tensor": name, "perm": perm, "paper_lex": lex,
                      "rearrangement_indices": sum(ip["rearrangement"]),
                      "rp_ms": t_rp, "sort_ms": t_sort, "speedup": t_sort / t_rp,
                      "rp_bits": ip["sort_bits"], "sort_bits": isr["sort_bits"],
                      "rp_path": ip["path"], "sort_path": isr["path"], "identical": same,
+                     "hier_ms": t_h, "hier_stage_paths": h_paths,
                      "paper": TABLE2.get(lex)})
         del ws, out_p, out_s
     return rows
@@ -92,14 +105,16 @@ def main():
     del k, v
     k, v = workloads.fill_tensor(args.fill_n, 0.02, seed=3, device=dev)
     rows += run(f"2% fill N={args.fill_n} ({k.numel()} nnz)", k, v, (args.fill_n,) * 4, args.reps)
-    lines = ["| tensor | perm (row-major) | paper lex | R idx | RP bits | sort bits | RP ms | "
-             "sort ms | sort/RP | identical | paper (MSD s / RP s) |", "|" + "---|" * 11]
+    lines = ["| tensor | perm (row-major) | paper lex | R idx | RP bits | sort bits | RP path | "
+             "RP ms | sort ms | sort/RP | staged RP ms (stage paths) | identical | "
+             "paper (MSD s / RP s) |", "|" + "---|" * 13]
     for r in rows:
         pap = "" if not r["paper"] else f"{r['paper'][0]}: {r['paper'][1]} / {r['paper'][2]}"
+        hier = "" if r["hier_ms"] is None else f"{r['hier_ms']:.3f} ({'+'.join(r['hier_stage_paths'])})"
         lines.append(f"| {r['tensor']} | {r['perm']} | {r['paper_lex']} | "
                      f"{r['rearrangement_indices']} | {r['rp_bits']} | {r['sort_bits']} | "
-                     f"{r['rp_ms']:.3f} | {r['sort_ms']:.3f} | {r['speedup']:.2f} | "
-                     f"{r['identical']} | {pap} |")
+                     f"{r['rp_path']} | {r['rp_ms']:.3f} | {r['sort_ms']:.3f} | "
+                     f"{r['speedup']:.2f} | {hier} | {r['identical']} | {pap} |")
     text = "\n".join(lines)
     print(text)
     for name in {r["tensor"] for r in rows}:

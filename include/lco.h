@@ -67,6 +67,9 @@ typedef enum lco_status {
 
 #define LCO_MAX_ORDER 16
 #define LCO_FLAG_VALIDATE 1u /* O(nnz) precondition check; SYNCHRONIZES the stream */
+#define LCO_FLAG_HIERARCHICAL 2u /* lco_permute runs the hierarchical plan (one stable
+                                    sort per run of rearrangement indices, PAPER.md:
+                                    245-247) when it has >= 2 stages; default: flat plan */
 
 typedef struct lco_plan_s* lco_handle;
 
@@ -76,7 +79,7 @@ typedef struct lco_plan_s* lco_handle;
  *   dims     [host] order positive sizes n_0..n_{N-1}, prod <= 2^63-1.
  *   perm     [host] order ints, a bijection (torch.permute semantics); NULL = identity.
  *   max_nnz  largest nnz the handle will be called with (< 2^32).
- *   flags    0 or LCO_FLAG_VALIDATE.
+ *   flags    0 or LCO_FLAG_VALIDATE | LCO_FLAG_HIERARCHICAL.
  * The plan normalizes the permutation (drops size-1 modes, fuses modes adjacent in
  * both orders), classifies indices as rearrangement / resting, and
  * selects the key digits to sort: the middle modes between the identity prefix and the
@@ -173,7 +176,9 @@ typedef struct lco_plan_info {
   int digit_bits[8];                   /* bits per pass, least significant first */
   int radix_bits;                      /* bins per pass = 2^radix_bits */
   int path;                            /* 0 copy, 1 LSD passes, 2 one on-chip leaf,
-                                          3 MSD passes + on-chip leaf sorts */
+                                          3 MSD passes + on-chip leaf sorts, 4 segment-
+                                          local tiles, 5 segmented single pass,
+                                          6 hierarchical stages */
   int launches;                        /* kernels this library launches per call */
   int tile;                            /* nonzeros per tile (CTA) */
   int msd_levels;                      /* path 3: MSD passes before the leaves */
@@ -181,8 +186,23 @@ typedef struct lco_plan_info {
   int leaf_kind;                       /* paths 2/3: 1 one warp per leaf (<= 384 nonzeros),
                                           2 one CTA per leaf (<= 8192 nonzeros) */
   double model_bytes;                  /* modelled HBM bytes per nonzero of the plan */
+  int stages;                          /* permute: stages of the hierarchical plan (one per
+                                          maximal run of rearrangement indices, PAPER.md:
+                                          245-247); 1 = flat.  path 6: the stages run */
+  int stage_path[8];                   /* path of each stage (0-5 as above) */
+  int stage_sort_bits[8];              /* bits of q each stage sorts */
+  double flat_model_bytes;             /* modelled bytes of the flat plan */
 } lco_plan_info;
 LCO_API lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* info);
+
+/* Stage j of the hierarchical plan (host only): the stage permutes keys of `dims` (its
+ * input order, normalized modes: size-1 modes dropped, modes that stay adjacent fused,
+ * so keys are unchanged) by the relative permutation `perm`.  Composing the stages in
+ * order gives the handle's permutation.  *n_stages = number of stages (1: flat plan,
+ * stage 0 = the normalized permutation).  dims/perm [host] of LCO_MAX_ORDER entries;
+ * LCO_ERR_ARG if j is out of range. */
+LCO_API lco_status lco_plan_stage(lco_handle h, int j, int* n_stages, int* order, uint64_t* dims,
+                                  int32_t* perm);
 
 /* Host reference of the device fast divisor (test hook for the host plan): writes
  * q[i] = x[i] / d computed with the same magic-number arithmetic the kernels use.

@@ -69,7 +69,10 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     c.segdiv = op.segdiv;
     c.segments = op.segments;
     c.msd.rb = B;
-    c.cost = 40;
+    // one read + one write; when many nonzeros share a q value (more per segment than
+    // middle values) the tile sort needs stable radix passes on chip, measured at about
+    // twice the cost (C3b stage 2, Table 2 2%-fill stage 2)
+    c.cost = nnz / op.segments > op.middle ? 80 : 40;
     return c;
   }
   c.path = kPathOnesweep;
@@ -248,6 +251,72 @@ lco_status check_handle(lco_handle h) {
   return LCO_OK;
 }
 
+// Run one flat plan on device buffers with the workspace `ws` (layout_for of its call
+// plan); launches only, no checks.
+cudaError_t execute(lco_plan_s* h, const OpPlan& op, uint64_t nnz, const uint64_t* keys_in,
+                    const double* vals_in, const uint32_t* idx_in, uint64_t* keys_out,
+                    double* vals_out, uint32_t* perm_out, char* ws, const Launch& L) {
+  const CallPlan cp = choose_plan(op, nnz);
+  const WsLayout w = layout_for(cp, nnz);
+  if (cp.path == kPathCopy)
+    return run_copy(nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, L);
+  PassIO io;
+  memset(&io, 0, sizeof io);
+  io.nnz = nnz;
+  io.keys_in = keys_in;
+  io.vals_in = vals_in;
+  io.idx_in = idx_in;
+  io.keys_out = keys_out;
+  io.vals_out = vals_out;
+  io.perm_out = perm_out;
+  io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
+  const bool mv = vals_out != nullptr, mp = perm_out != nullptr;
+  const bool hasA = cp.path == kPathMsd || cp.path == kPathTile || cp.passes >= 2;
+  const bool hasB = cp.path == kPathMsd || cp.path == kPathTile || cp.passes >= 3;
+  io.kA = hasA ? reinterpret_cast<uint64_t*>(ws + w.kA) : nullptr;
+  io.vA = hasA && mv ? reinterpret_cast<double*>(ws + w.vA) : nullptr;
+  io.pA = hasA && mp ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
+  io.kB = hasB ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
+  io.vB = hasB && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
+  io.pB = hasB && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
+  if (cp.path == kPathOnesweep) return run_passes(cp.rb, cp.kp, io, L);
+  if (cp.path == kPathTile) return run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
+  if (cp.path == kPathSeg) return run_seg(cp.msd.b1, cp.msd.b2, cp.kp, io, L);
+  return run_msd(cp.msd, cp.kp, io, L);
+}
+
+// Hierarchical execution of a permute call: taken when the handle was created with
+// LCO_FLAG_HIERARCHICAL and the plan has >= 2 stages.  (Measured on B200: the stages win
+// on the paper's addition permutation {1,0,3,2} and Table 2's median {2,1,3,0} of the
+// combinatorial Laplacian, by 14-18%, and lose where a stage's tile sort meets many
+// nonzeros per q value, which the host cannot see; hence opt-in.)
+struct Hier {
+  bool use;
+  double cost, flat_cost;
+  size_t buf_off[2], inner_off, total;
+};
+
+Hier hier_for(const lco_plan_s* h, bool sort, uint64_t nnz) {
+  Hier r;
+  memset(&r, 0, sizeof r);
+  r.flat_cost = choose_plan(sort ? h->op_sort : h->op_permute, nnz).cost;
+  if (sort || h->nstages < 2 || nnz == 0) return r;
+  size_t inner = 0;
+  for (int j = 0; j < h->nstages; ++j) {
+    const CallPlan cp = choose_plan(h->stages[j].op, nnz);
+    r.cost += cp.cost;
+    const size_t t = layout_for(cp, nnz).total;
+    inner = t > inner ? t : inner;
+  }
+  const size_t set = 2 * align_up(nnz * 8) + align_up(nnz * 4);
+  r.buf_off[0] = 0;
+  r.buf_off[1] = h->nstages >= 3 ? set : 0;
+  r.inner_off = (h->nstages >= 3 ? 2 : 1) * set;
+  r.total = r.inner_off + inner;
+  r.use = (h->flags & LCO_FLAG_HIERARCHICAL) != 0;
+  return r;
+}
+
 lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const uint64_t* keys_in,
                   const double* vals_in, const uint32_t* idx_in, uint64_t* keys_out,
                   double* vals_out, uint32_t* perm_out, void* workspace, size_t ws_bytes,
@@ -285,23 +354,23 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
         return LCO_ERR_ALIAS;
       }
   }
-  const CallPlan cp = choose_plan(op, nnz);
-  const WsLayout w = layout_for(cp, nnz);
-  if (!workspace || ws_bytes < w.total || (reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
-    set_error("workspace needs %zu bytes, 256-byte aligned (got %zu at %p)", w.total, ws_bytes,
+  const Hier hp = hier_for(h, sort, nnz);
+  const size_t need = hp.use ? hp.total : layout_for(choose_plan(op, nnz), nnz).total;
+  if (!workspace || ws_bytes < need || (reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
+    set_error("workspace needs %zu bytes, 256-byte aligned (got %zu at %p)", need, ws_bytes,
               workspace);
     return LCO_ERR_WORKSPACE;
   }
   for (int i = 0; i < 3; ++i)
-    if (overlaps(outs[i], outsz[i], workspace, w.total) ||
-        overlaps(ins[i], insz[i], workspace, w.total)) {
+    if (overlaps(outs[i], outsz[i], workspace, need) ||
+        overlaps(ins[i], insz[i], workspace, need)) {
       set_error("workspace overlaps an input or output");
       return LCO_ERR_ALIAS;
     }
   char* ws = static_cast<char*>(workspace);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (h->flags & LCO_FLAG_VALIDATE) {
-    uint32_t* flag = reinterpret_cast<uint32_t*>(ws + w.flag);
+    uint32_t* flag = reinterpret_cast<uint32_t*>(ws);
     cudaError_t e = run_validate(nnz, keys_in, h->total, sort ? 0 : 1, flag, s);
     if (e != cudaSuccess) return cuda_fail(e, "validate");
     uint32_t hf = 0;
@@ -320,33 +389,30 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
   Launch L{s, nullptr, nullptr};
   ProfCtx pc;
   const bool prof = prof_begin(h, s, &pc, &L);
-  cudaError_t e;
-  if (cp.path == kPathCopy) {
-    e = run_copy(nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, L);
+  cudaError_t e = cudaSuccess;
+  if (!hp.use) {
+    e = execute(h, op, nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, ws, L);
   } else {
-    PassIO io;
-    memset(&io, 0, sizeof io);
-    io.nnz = nnz;
-    io.keys_in = keys_in;
-    io.vals_in = vals_in;
-    io.idx_in = idx_in;
-    io.keys_out = keys_out;
-    io.vals_out = vals_out;
-    io.perm_out = perm_out;
-    io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
-    const bool mv = vals_out != nullptr, mp = perm_out != nullptr;
-    const bool hasA = cp.path == kPathMsd || cp.path == kPathTile || cp.passes >= 2;
-    const bool hasB = cp.path == kPathMsd || cp.path == kPathTile || cp.passes >= 3;
-    io.kA = hasA ? reinterpret_cast<uint64_t*>(ws + w.kA) : nullptr;
-    io.vA = hasA && mv ? reinterpret_cast<double*>(ws + w.vA) : nullptr;
-    io.pA = hasA && mp ? reinterpret_cast<uint32_t*>(ws + w.pA) : nullptr;
-    io.kB = hasB ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
-    io.vB = hasB && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
-    io.pB = hasB && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
-    if (cp.path == kPathOnesweep) e = run_passes(cp.rb, cp.kp, io, L);
-    else if (cp.path == kPathTile) e = run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
-    else if (cp.path == kPathSeg) e = run_seg(cp.msd.b1, cp.msd.b2, cp.kp, io, L);
-    else e = run_msd(cp.msd, cp.kp, io, L);
+    // stage j reads stage j-1's (K', V, position) from one of two intermediate buffer
+    // sets and the last stage writes the outputs; positions compose through idx_in.
+    char* inner = ws + hp.inner_off;
+    const bool mp = perm_out != nullptr;
+    const uint64_t* k_in = keys_in;
+    const double* v_in = vals_in;
+    const uint32_t* i_in = idx_in;
+    for (int j = 0; j < h->nstages && e == cudaSuccess; ++j) {
+      const bool last = j == h->nstages - 1;
+      char* buf = ws + hp.buf_off[j % 2];
+      uint64_t* k_out = last ? keys_out : reinterpret_cast<uint64_t*>(buf);
+      double* v_out = last ? vals_out
+                           : (vals_in ? reinterpret_cast<double*>(buf + align_up(nnz * 8)) : nullptr);
+      uint32_t* p_out = last ? perm_out
+                             : (mp ? reinterpret_cast<uint32_t*>(buf + 2 * align_up(nnz * 8)) : nullptr);
+      e = execute(h, h->stages[j].op, nnz, k_in, v_in, i_in, k_out, v_out, p_out, inner, L);
+      k_in = k_out;
+      v_in = v_out;
+      i_in = p_out;
+    }
   }
   if (prof) prof_end(&pc);
   if (e != cudaSuccess) return cuda_fail(e, sort ? "lco_sort" : "lco_permute");
@@ -372,7 +438,7 @@ lco_status lco_create(lco_handle* out, int order, const uint64_t* dims, const in
     set_error("max_nnz must be < 2^32 (uint32 permutation vector)");
     return LCO_ERR_CAPACITY;
   }
-  if (flags & ~LCO_FLAG_VALIDATE) {
+  if (flags & ~(LCO_FLAG_VALIDATE | LCO_FLAG_HIERARCHICAL)) {
     set_error("unknown flags 0x%x", flags);
     return LCO_ERR_ARG;
   }
@@ -414,6 +480,8 @@ lco_status lco_workspace_size(lco_handle h, uint64_t nnz, size_t* bytes) {
   const OpPlan& a = h->op_permute;
   const OpPlan& b = h->op_sort;
   size_t x = layout_for(choose_plan(a, nnz), nnz).total;
+  const Hier hp = hier_for(h, false, nnz);
+  if (hp.use && hp.total > x) x = hp.total;
   size_t y = layout_for(choose_plan(b, nnz), nnz).total;
   // partition (up to 2048 ranks) uses at most a single 11-bit pass
   CallPlan part;
@@ -623,6 +691,31 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
                                                                      : (cp.path == kPathMsd ? (cp.msd.cta ? 2 : 1) : 0);
   if (cp.path == kPathTile) info->leaf_bits = cp.msd.rb;
   info->model_bytes = cp.cost;
+  info->flat_model_bytes = cp.cost;
+  const Hier hp = hier_for(h, sort != 0, nnz);
+  info->stages = sort ? 1 : (h->nstages >= 2 ? h->nstages : 1);
+  for (int j = 0; j < h->nstages && j < 8 && !sort; ++j) {
+    const CallPlan sc = choose_plan(h->stages[j].op, nnz);
+    info->stage_path[j] = sc.path;
+    info->stage_sort_bits[j] = h->stages[j].op.sort_bits;
+  }
+  if (hp.use) {  // hierarchical: stages run one after another
+    info->path = 6;
+    info->model_bytes = hp.cost;
+    int launches_h = 0;
+    for (int j = 0; j < h->nstages; ++j) {
+      lco_plan_info si;
+      (void)si;
+      const CallPlan sc = choose_plan(h->stages[j].op, nnz);
+      launches_h += sc.path == kPathCopy || sc.path == kPathLocal ? 1
+                    : sc.path == kPathTile ? 3
+                    : sc.path == kPathSeg ? 6
+                    : sc.path == kPathOnesweep ? 4 * sc.passes
+                    : 4 + (sc.msd.levels == 2 ? 5 : 0) + 2;
+    }
+    info->launches = launches_h;
+    return LCO_OK;
+  }
   // kernels of this library per call (cudaMemsetAsync not counted)
   int launches = 0;
   if (nnz > 0) {
@@ -633,6 +726,36 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
     else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 2;  // passes, leaves, deferred
   }
   info->launches = launches;
+  return LCO_OK;
+}
+
+lco_status lco_plan_stage(lco_handle h, int j, int* n_stages, int* order, uint64_t* dims,
+                          int32_t* perm) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (!n_stages || !order || !dims || !perm) {
+    set_error("n_stages, order, dims and perm are required");
+    return LCO_ERR_NULL;
+  }
+  const int ns = h->nstages >= 2 ? h->nstages : 1;
+  *n_stages = ns;
+  if (j < 0 || j >= ns) {
+    set_error("stage %d outside 0..%d", j, ns - 1);
+    return LCO_ERR_ARG;
+  }
+  if (h->nstages >= 2) {
+    *order = h->stages[j].order;
+    for (int m = 0; m < *order; ++m) {
+      dims[m] = h->stages[j].dims[m];
+      perm[m] = h->stages[j].perm[m];
+    }
+  } else {
+    *order = h->norm_n;
+    for (int m = 0; m < *order; ++m) {
+      dims[m] = h->norm_dims[m];
+      perm[m] = h->norm_perm[m];
+    }
+  }
   return LCO_OK;
 }
 

@@ -211,6 +211,15 @@ struct OpPlan {
   uint64_t trailing, middle, segments, segdiv;
 };
 
+// One stage of a hierarchical plan: the flat plan of a relative permutation.
+constexpr int kMaxStages = 8;
+struct StagePlan {
+  int order;
+  uint64_t dims[LCO_MAX_ORDER];  // stage input order
+  int32_t perm[LCO_MAX_ORDER];   // relative permutation
+  OpPlan op;
+};
+
 }  // namespace lco
 
 struct lco_plan_s {
@@ -229,6 +238,8 @@ struct lco_plan_s {
   lco::OpPlan op_permute;  // nnz-independent parts; path refined per call
   lco::OpPlan op_sort;
   lco::KeyPlan kp_full;    // re-encode only (partition, histogram)
+  int nstages;             // hierarchical plan: stages (>= 2 when it differs from flat)
+  lco::StagePlan stages[lco::kMaxStages];
   // profiling
   int prof_calls_max;
   int prof_calls;

@@ -23,6 +23,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "device_common.cuh"
 #include "launch.h"
@@ -676,19 +677,20 @@ constexpr int kCBucketBits = 12;
 constexpr int kCThreads = 512;
 constexpr int kCBig = 48;
 
-constexpr size_t leafc_smem(bool big) {
-  return (size_t)kCCap * (8 + 2) + ((size_t)1 << kCBucketBits) * 4 +
-         (big ? (size_t)kCCap * (2 + 4) + (size_t)(kCThreads / 32) * 256 * 4 : 0);
+constexpr size_t leafc_smem(bool big, int cap) {
+  return (size_t)cap * (8 + 2) + ((size_t)1 << kCBucketBits) * 4 +
+         (big ? (size_t)cap * (2 + 4) + (size_t)(kCThreads / 32) * 256 * 4 : 0);
 }
 
-template <bool VALS, bool BIG>
-__global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_constant__ LeafArgs L) {
+template <bool VALS, bool BIG, int CAP = kCCap>
+__global__ void __launch_bounds__(kCThreads, (BIG && CAP > 4096) ? 1 : 2)
+    k_leafc(const __grid_constant__ LeafArgs L) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* K = reinterpret_cast<uint64_t*>(smem);                 // [cap] staged K'
-  uint16_t* X = reinterpret_cast<uint16_t*>(K + kCCap);            // [cap] order
-  uint32_t* B = reinterpret_cast<uint32_t*>(X + kCCap);            // [2^12] buckets
+  uint16_t* X = reinterpret_cast<uint16_t*>(K + CAP);            // [cap] order
+  uint32_t* B = reinterpret_cast<uint32_t*>(X + CAP);            // [2^12] buckets
   uint16_t* F = reinterpret_cast<uint16_t*>(B + (1 << kCBucketBits));  // BIG: [cap]
-  uint32_t* WH = reinterpret_cast<uint32_t*>(F + kCCap);           // BIG: radix counters
+  uint32_t* WH = reinterpret_cast<uint32_t*>(F + CAP);           // BIG: radix counters
   uint32_t* Q = WH + (kCThreads / 32) * 256;                       // BIG: q - min q
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_loff[256], s_cnt[256];
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
     const uint64_t* sk = d.src == 0 ? L.keys_in : (d.src == 1 ? L.kA : L.kB);
     const double* sv = d.src == 0 ? L.vals_in : (d.src == 1 ? L.vA : L.vB);
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
-    if (n > (uint32_t)kCCap) {  // oversize (skewed) leaf: the block kernel streams it
+    if (n > (uint32_t)CAP) {  // oversize (skewed) leaf: the block kernel streams it
       if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
       k += gridDim.x;
       continue;
@@ -714,15 +716,16 @@ __global__ void __launch_bounds__(kCThreads, BIG ? 1 : 2) k_leafc(const __grid_c
       s_max = s_qmax = 0ull;
       s_big = 0;
     }
-    if (d.src == 0) {  // raw input (the whole call is one leaf): re-encode while staging
-      for (uint32_t i = tid; i < n; i += kCThreads) K[i] = reencode(L.a.kp, __ldcs(sk + start + i));
-    } else {
-      for (uint32_t i = tid; i < n; i += kCThreads) cp_async8(K + i, sk + (uint64_t)start + i);
-      cp_async_commit();
-      if (tid == 0) {  // the gathers of the write phase then hit L2
-        if (VALS) prefetch_l2(sv + start, (size_t)n * 8);
-        if (want_pos) prefetch_l2(sp + start, (size_t)n * 4);
-      }
+    for (uint32_t i = tid; i < n; i += kCThreads) cp_async8(K + i, sk + (uint64_t)start + i);
+    cp_async_commit();
+    if (tid == 0) {  // the gathers of the write phase then hit L2
+      if (VALS) prefetch_l2(sv + start, (size_t)n * 8);
+      if (want_pos && d.src != 0) prefetch_l2(sp + start, (size_t)n * 4);
+      if (want_pos && d.src == 0 && L.idx_in) prefetch_l2(L.idx_in + start, (size_t)n * 4);
+    }
+    if (d.src == 0) {  // raw input (a whole-input leaf or a segment tile): re-encode in place
+      cp_async_wait<0>();
+      for (uint32_t i = tid; i < n; i += kCThreads) K[i] = reencode(L.a.kp, K[i]);
     }
     cp_async_wait<0>();
     __syncthreads();
@@ -1296,16 +1299,16 @@ static cudaError_t launch_leafw(const LeafArgs& L, cudaStream_t s) {
 uint32_t leaf_cap() { return kCCap; }
 uint32_t cta_leaf_cap() { return kCCap; }
 
-template <bool VALS, bool BIG>
+template <bool VALS, bool BIG, int CAP = kCCap>
 static cudaError_t launch_leafc_t(const LeafArgs& L, uint32_t grid_cap, cudaStream_t s) {
   static bool attr = false;
   static int per_sm = 1;
-  constexpr size_t smem = leafc_smem(BIG);
+  constexpr size_t smem = leafc_smem(BIG, CAP);
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_leafc<VALS, BIG>,
+    cudaError_t e = cudaFuncSetAttribute(k_leafc<VALS, BIG, CAP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leafc<VALS, BIG>, kCThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_leafc<VALS, BIG, CAP>, kCThreads, smem);
     if (per_sm < 1) per_sm = 1;
     attr = true;
   }
@@ -1313,7 +1316,7 @@ static cudaError_t launch_leafc_t(const LeafArgs& L, uint32_t grid_cap, cudaStre
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t persistent = (uint32_t)(sms * per_sm);
-  k_leafc<VALS, BIG><<<grid_cap < persistent ? grid_cap : persistent, kCThreads, smem, s>>>(L);
+  k_leafc<VALS, BIG, CAP><<<grid_cap < persistent ? grid_cap : persistent, kCThreads, smem, s>>>(L);
   return cudaGetLastError();
 }
 
@@ -1407,9 +1410,15 @@ __global__ void k_tile_bounds(const uint64_t* __restrict__ keys, uint64_t nnz, F
   tstart[c] = (uint32_t)lo;
 }
 
+// Tiles of the segment-local path are sorted by k_leafc with a 4K cap (two CTAs per
+// SM).  Nominal tile: a tile overshoots it by at most one segment, and segments are
+// uneven (only the average nnz / G is known on the host), so leave half the cap as
+// headroom; segments larger than the cap are deferred to the streaming sort.
+constexpr int kTileCap = 4096;
 uint32_t tile_nominal(uint64_t nnz, uint64_t segments) {
   const uint64_t avg = segments ? (nnz + segments - 1) / segments : nnz;
-  const uint64_t t = (uint64_t)kCCap > 2 * avg + 2048 ? kCCap - 2 * avg : 2048;
+  uint64_t t = (uint64_t)kTileCap > 2 * avg + 1024 ? kTileCap - 2 * avg : 1024;
+  if (t > kTileCap / 2) t = kTileCap / 2;
   return (uint32_t)(t / 256 * 256);
 }
 
@@ -1461,9 +1470,19 @@ cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int
   L.defer = defer;
   L.ndefer = ndefer;
   if (Lc.mark) Lc.mark(Lc.ctx, "k_leafc_tiles");
-  e = vals ? launch_leafc_t<true, true>(L, 1u << 30, Lc.stream)
-           : launch_leafc_t<false, true>(L, 1u << 30, Lc.stream);
+  e = vals ? launch_leafc_t<true, true, kTileCap>(L, 1u << 30, Lc.stream)
+           : launch_leafc_t<false, true, kTileCap>(L, 1u << 30, Lc.stream);
   if (e != cudaSuccess) return e;
+  if (getenv("LCO_DEBUG")) {  // debug: deferred tiles and the largest tile
+    uint32_t nd = 0;
+    cudaMemcpyAsync(&nd, ndefer, 4, cudaMemcpyDeviceToHost, Lc.stream);
+    std::vector<uint32_t> ts(nt + 1);
+    cudaMemcpyAsync(ts.data(), tstart, (nt + 1) * 4, cudaMemcpyDeviceToHost, Lc.stream);
+    cudaStreamSynchronize(Lc.stream);
+    uint32_t mx = 0;
+    for (uint32_t c = 0; c < nt; ++c) mx = ts[c + 1] - ts[c] > mx ? ts[c + 1] - ts[c] : mx;
+    fprintf(stderr, "run_tiles: T %u tiles %u deferred %u largest %u\n", T, nt, nd, mx);
+  }
   if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf_deferred");
   LeafArgs LD = L;
   LD.dlist = defer;

@@ -135,6 +135,13 @@ void build_digit_moves(KeyPlan* kp) {
   }
 }
 
+struct FlatInfo {
+  int n;
+  uint64_t nd[LCO_MAX_ORDER];
+  int32_t np[LCO_MAX_ORDER];
+  int a, b;
+};
+
 static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64_t T) {
   KeyPlan kp;
   memset(&kp, 0, sizeof kp);
@@ -168,6 +175,124 @@ static KeyPlan make_keyplan(int n, const uint64_t* nd, const int32_t* np, uint64
     build_moves(&kp);
   }
   return kp;
+}
+
+// Normalization (RP preprocessing): drop size-1 modes (their
+// coordinate is always 0), then fuse runs of modes that are consecutive in both orders
+// (they move as one mixed-radix digit); a = identity-prefix length, b = start of the
+// longest strictly increasing suffix.
+static void normalize(int order, const uint64_t* dims, const int32_t* perm, FlatInfo* fi) {
+  int keep[LCO_MAX_ORDER];
+  uint64_t d1[LCO_MAX_ORDER];
+  int n1 = 0;
+  for (int m = 0; m < order; ++m) {
+    keep[m] = dims[m] > 1 ? n1 : -1;
+    if (dims[m] > 1) d1[n1++] = dims[m];
+  }
+  int p1[LCO_MAX_ORDER];
+  int k = 0;
+  for (int t = 0; t < order; ++t)
+    if (keep[perm[t]] >= 0) p1[k++] = keep[perm[t]];
+  int gfirst[LCO_MAX_ORDER], glen[LCO_MAX_ORDER], ng = 0;
+  for (int t = 0; t < n1; ++t) {
+    if (t > 0 && p1[t] == p1[t - 1] + 1) {
+      glen[ng - 1]++;
+    } else {
+      gfirst[ng] = p1[t];
+      glen[ng] = 1;
+      ng++;
+    }
+  }
+  fi->n = ng;
+  for (int g = 0; g < ng; ++g) {
+    int rank = 0;
+    for (int g2 = 0; g2 < ng; ++g2)
+      if (gfirst[g2] < gfirst[g]) rank++;
+    uint64_t d = 1;
+    for (int i = 0; i < glen[g]; ++i) d *= d1[gfirst[g] + i];
+    fi->nd[rank] = d;
+    fi->np[g] = rank;
+  }
+  int a = 0;
+  while (a < ng && fi->np[a] == a) ++a;
+  int b = ng > 0 ? ng - 1 : 0;
+  while (b > 0 && fi->np[b - 1] < fi->np[b]) --b;
+  fi->a = a;
+  fi->b = b;
+}
+
+// The flat plan: sort on q = K' div T (prefix + middle digits), T = prod of suffix dims.
+static void flat_permute(const FlatInfo& fi, OpPlan* op) {
+  const int n = fi.n, a = fi.a, b = fi.b;
+  const uint64_t* nd = fi.nd;
+  const int32_t* np = fi.np;
+  uint64_t T = 1, S = 1, G = 1, D = 1;
+  for (int t = b; t < n; ++t) T *= nd[np[t]];
+  for (int t = a; t < b; ++t) S *= nd[np[t]];
+  for (int m = 0; m < a && m < n; ++m) G *= nd[m];
+  for (int m = a; m < n; ++m) D *= nd[m];
+  memset(op, 0, sizeof *op);
+  op->kp = make_keyplan(n, nd, np, n >= 2 ? T : 1);
+  op->trailing = T;
+  op->middle = S;
+  op->segments = G;
+  op->segdiv = D;
+  if (n <= 1) {
+    op->path = kPathCopy;
+    choose_passes(op, 0);
+  } else {
+    op->path = kPathOnesweep;
+    choose_passes(op, ceil_log2(G * S));
+  }
+}
+
+// Hierarchical plan ("the rearrangement procedure is recursively applied
+// to each of these sub-regions"): walking the new order from the most
+// significant mode, a resting mode refines the current regions (it is the old-most-
+// significant of the remaining modes, already in place), and each maximal run of
+// rearrangement modes is one stable sort inside the current regions.  Stage j permutes
+// the order O_{j-1} (the modes fixed so far, then the rest in old order) into O_j; its
+// own flat plan has the fixed modes as identity prefix and only that run as middle, so
+// interior resting modes are never sorted.  One stage = the flat plan.
+static void build_stages(lco_plan_s* h, const FlatInfo& fi) {
+  const int n = fi.n;
+  const int32_t* np = fi.np;
+  h->nstages = 0;
+  int O[LCO_MAX_ORDER];
+  for (int m = 0; m < n; ++m) O[m] = m;
+  auto resting = [&](int t) {
+    for (int u = t + 1; u < n; ++u)
+      if (np[u] < np[t]) return false;
+    return true;
+  };
+  int t = 0;
+  while (t < n && h->nstages < kMaxStages) {
+    if (resting(t)) {
+      ++t;
+      continue;
+    }
+    int u = t;
+    while (u < n && !resting(u)) ++u;
+    int On[LCO_MAX_ORDER], k = 0;
+    bool used[LCO_MAX_ORDER] = {false};
+    for (int i = 0; i < u; ++i) {
+      On[k++] = np[i];
+      used[np[i]] = true;
+    }
+    for (int m = 0; m < n; ++m)
+      if (!used[m]) On[k++] = m;
+    StagePlan& S = h->stages[h->nstages++];
+    S.order = n;
+    for (int i = 0; i < n; ++i) S.dims[i] = fi.nd[O[i]];
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        if (O[j] == On[i]) S.perm[i] = j;
+    FlatInfo sfi;
+    normalize(n, S.dims, S.perm, &sfi);
+    flat_permute(sfi, &S.op);
+    for (int i = 0; i < n; ++i) O[i] = On[i];
+    t = u;
+  }
 }
 
 lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int32_t* perm) {
@@ -209,74 +334,23 @@ lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int3
     h->rearr[t] = h->perm[t] != mn;
   }
 
-  // normalization 1: drop size-1 modes
-  int keep[LCO_MAX_ORDER];
-  uint64_t d1[LCO_MAX_ORDER];
-  int n1 = 0;
-  for (int m = 0; m < order; ++m) {
-    keep[m] = dims[m] > 1 ? n1 : -1;
-    if (dims[m] > 1) d1[n1++] = dims[m];
+  FlatInfo fi;
+  normalize(order, dims, h->perm, &fi);
+  const int n = fi.n;
+  const uint64_t* nd = fi.nd;
+  h->norm_n = n;
+  for (int m = 0; m < n; ++m) {
+    h->norm_dims[m] = fi.nd[m];
+    h->norm_perm[m] = fi.np[m];
   }
-  int p1[LCO_MAX_ORDER];
-  int k = 0;
-  for (int t = 0; t < order; ++t)
-    if (keep[h->perm[t]] >= 0) p1[k++] = keep[h->perm[t]];
-  // normalization 2: fuse runs m, m+1, ... that are consecutive in the new order
-  int gfirst[LCO_MAX_ORDER], glen[LCO_MAX_ORDER], ng = 0;
-  for (int t = 0; t < n1; ++t) {
-    if (t > 0 && p1[t] == p1[t - 1] + 1) {
-      glen[ng - 1]++;
-    } else {
-      gfirst[ng] = p1[t];
-      glen[ng] = 1;
-      ng++;
-    }
-  }
-  h->norm_n = ng;
-  for (int g = 0; g < ng; ++g) {
-    int rank = 0;
-    for (int g2 = 0; g2 < ng; ++g2)
-      if (gfirst[g2] < gfirst[g]) rank++;
-    uint64_t d = 1;
-    for (int i = 0; i < glen[g]; ++i) d *= d1[gfirst[g] + i];
-    h->norm_dims[rank] = d;
-    h->norm_perm[g] = rank;
-  }
-  const int n = ng;
-  const uint64_t* nd = h->norm_dims;
-  const int32_t* np = h->norm_perm;
-  int a = 0;
-  while (a < n && np[a] == a) ++a;
-  int b = n > 0 ? n - 1 : 0;
-  while (b > 0 && np[b - 1] < np[b]) --b;
-  h->prefix_len = a;
-  h->suffix_start = b;
-
-  uint64_t T = 1, S = 1, G = 1, D = 1;
-  for (int t = b; t < n; ++t) T *= nd[np[t]];
-  for (int t = a; t < b; ++t) S *= nd[np[t]];
-  for (int m = 0; m < a && m < n; ++m) G *= nd[m];
-  for (int m = a; m < n; ++m) D *= nd[m];
-
-  // permute: sort on q = K' div T (prefix + middle digits)
-  OpPlan& op = h->op_permute;
-  memset(&op, 0, sizeof op);
-  op.kp = make_keyplan(n, nd, np, n >= 2 ? T : 1);
-  op.trailing = T;
-  op.middle = S;
-  op.segments = G;
-  op.segdiv = D;
-  if (n <= 1) {
-    op.path = kPathCopy;
-    choose_passes(&op, 0);
-  } else {
-    op.path = kPathOnesweep;
-    choose_passes(&op, ceil_log2(G * S));
-  }
+  h->prefix_len = fi.a;
+  h->suffix_start = fi.b;
+  flat_permute(fi, &h->op_permute);
+  build_stages(h, fi);
   // sort: q = K' (all key digits)
   OpPlan& os = h->op_sort;
   memset(&os, 0, sizeof os);
-  os.kp = make_keyplan(n, nd, np, 1);
+  os.kp = make_keyplan(n, nd, fi.np, 1);
   os.trailing = 1;
   os.middle = total;
   os.segments = 1;
@@ -288,7 +362,7 @@ lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int3
     os.path = kPathOnesweep;
     choose_passes(&os, h->key_bits);
   }
-  h->kp_full = make_keyplan(n, nd, np, 1);
+  h->kp_full = make_keyplan(n, nd, fi.np, 1);
   return LCO_OK;
 }
 

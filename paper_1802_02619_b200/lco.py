@@ -21,8 +21,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblco.so")
 
 FLAG_VALIDATE = 1
+FLAG_HIERARCHICAL = 2
 MAX_ORDER = 16
-PATHS = {0: "copy", 1: "lsd", 2: "leaf", 3: "msd", 4: "tile", 5: "seg"}
+PATHS = {0: "copy", 1: "lsd", 2: "leaf", 3: "msd", 4: "tile", 5: "seg", 6: "hier"}
 
 _STATUS = {
     0: "LCO_OK", 1: "LCO_ERR_NULL", 2: "LCO_ERR_ORDER", 3: "LCO_ERR_DIM", 4: "LCO_ERR_PERM",
@@ -65,6 +66,10 @@ class PlanInfo(ctypes.Structure):
         ("leaf_bits", ctypes.c_int),
         ("leaf_kind", ctypes.c_int),
         ("model_bytes", ctypes.c_double),
+        ("stages", ctypes.c_int),
+        ("stage_path", ctypes.c_int * 8),
+        ("stage_sort_bits", ctypes.c_int * 8),
+        ("flat_model_bytes", ctypes.c_double),
     ]
 
 
@@ -86,6 +91,9 @@ _SIGS = {
                                      _P, _P, _P, ctypes.c_size_t, _P]),
     "lco_key_histogram": (ctypes.c_int, [_P, _U64, _P, ctypes.c_int, _P, _P]),
     "lco_plan_query": (ctypes.c_int, [_P, _U64, ctypes.c_int, ctypes.POINTER(PlanInfo)]),
+    "lco_plan_stage": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_U64),
+                                      ctypes.POINTER(ctypes.c_int32)]),
     "lco_fastdiv_host": (ctypes.c_int, [_U64, _U64, _P, _P]),
     "lco_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
     "lco_profile_read": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, _P,
@@ -148,7 +156,7 @@ def _workspace(nbytes, device):
 class Plan:
     """An lco_handle: the host plan for (dims, perm).  Immutable; reusable."""
 
-    def __init__(self, dims, perm=None, max_nnz=(1 << 32) - 1, validate=False):
+    def __init__(self, dims, perm=None, max_nnz=(1 << 32) - 1, validate=False, hierarchical=False):
         self.dims = tuple(int(d) for d in dims)
         order = len(self.dims)
         self.perm = tuple(range(order)) if perm is None else tuple(int(p) for p in perm)
@@ -156,7 +164,8 @@ class Plan:
         p = (ctypes.c_int32 * max(order, 1))(*self.perm)
         h = ctypes.c_void_p()
         _check(lib().lco_create(ctypes.byref(h), order, d, p, int(max_nnz),
-                                FLAG_VALIDATE if validate else 0))
+                                (FLAG_VALIDATE if validate else 0)
+                                | (FLAG_HIERARCHICAL if hierarchical else 0)))
         self._h = h
         self.max_nnz = int(max_nnz)
 
@@ -184,6 +193,20 @@ class Plan:
         _check(lib().lco_host_workspace_size(self._h, int(nnz), ctypes.byref(n)))
         return n.value
 
+    def stages(self) -> list:
+        """The hierarchical plan (lco_plan_stage): [(dims, perm)] per stage, in the
+        normalized key space; composing them gives this plan's permutation."""
+        out, j, ns = [], 0, 1
+        while j < ns:
+            n_st, order = ctypes.c_int(), ctypes.c_int()
+            dims = (_U64 * 16)()
+            perm = (ctypes.c_int32 * 16)()
+            _check(lib().lco_plan_stage(self._h, j, ctypes.byref(n_st), ctypes.byref(order), dims, perm))
+            ns = n_st.value
+            out.append((tuple(int(x) for x in dims[:order.value]), tuple(perm[:order.value])))
+            j += 1
+        return out
+
     def info(self, nnz: int, sort: bool = False) -> dict:
         pi = PlanInfo()
         _check(lib().lco_plan_query(self._h, int(nnz), 1 if sort else 0, ctypes.byref(pi)))
@@ -210,6 +233,10 @@ class Plan:
             "leaf_bits": pi.leaf_bits,
             "leaf_kind": {0: None, 1: "warp", 2: "cta"}.get(pi.leaf_kind, pi.leaf_kind),
             "model_bytes": pi.model_bytes,
+            "stages": pi.stages,
+            "stage_paths": [PATHS.get(x, x) for x in pi.stage_path[:pi.stages]] if pi.stages > 1 else [],
+            "stage_sort_bits": list(pi.stage_sort_bits[:pi.stages]) if pi.stages > 1 else [],
+            "flat_model_bytes": pi.flat_model_bytes,
         }
 
     # ---------------------------------------------------------------- device calls
@@ -329,18 +356,20 @@ class Plan:
 _plan_cache: dict = {}
 
 
-def plan(dims, perm=None, max_nnz=(1 << 32) - 1, validate=False) -> Plan:
+def plan(dims, perm=None, max_nnz=(1 << 32) - 1, validate=False, hierarchical=False) -> Plan:
     key = (tuple(int(d) for d in dims), None if perm is None else tuple(int(p) for p in perm),
-           int(max_nnz), bool(validate))
+           int(max_nnz), bool(validate), bool(hierarchical))
     p = _plan_cache.get(key)
     if p is None:
-        p = _plan_cache[key] = Plan(dims, perm, max_nnz, validate)
+        p = _plan_cache[key] = Plan(dims, perm, max_nnz, validate, hierarchical)
     return p
 
 
-def permute(keys, vals, dims, perm, idx=None, return_perm=True, validate=False, stream=None):
+def permute(keys, vals, dims, perm, idx=None, return_perm=True, validate=False, stream=None,
+            hierarchical=False):
     """Permute a sorted LCO tensor: returns (keys_out, vals_out, perm_out)."""
-    return plan(dims, perm, validate=validate).permute(keys, vals, idx, return_perm, stream)
+    return plan(dims, perm, validate=validate, hierarchical=hierarchical).permute(
+        keys, vals, idx, return_perm, stream)
 
 
 def sort(keys, vals, dims, perm=None, idx=None, return_perm=True, validate=False, stream=None):

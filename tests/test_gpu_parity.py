@@ -28,12 +28,13 @@ def _np_u64(t):
         t.detach().cpu().numpy().astype(np.uint64)
 
 
-def check(dims, perm, keys, vals, idx=None, sort=False, dev="cuda:0", return_perm=True):
+def check(dims, perm, keys, vals, idx=None, sort=False, dev="cuda:0", return_perm=True,
+          hierarchical=False):
     """Run the CUDA path and the oracle on the same inputs; compare bit-exactly."""
     k = torch.as_tensor(np.asarray(keys, dtype=np.uint64).view(np.int64)).to(dev)
     v = None if vals is None else torch.as_tensor(np.asarray(vals, dtype=np.float64)).to(dev)
     ix = None if idx is None else torch.as_tensor(np.asarray(idx, dtype=np.uint32).view(np.int32)).to(dev)
-    p = lco.plan(dims, perm)
+    p = lco.plan(dims, perm, hierarchical=hierarchical)
     fn = p.sort if sort else p.permute
     ko, vo, po = fn(k, v, ix, return_perm=return_perm)
     torch.cuda.synchronize()
@@ -428,3 +429,42 @@ def test_seg_path(dims, perm, nnz, cuda_device):
     assert info["path"] == "seg", info["path"]
     check(dims, perm, keys, vals)
     check(dims, perm, keys, None, return_perm=False)
+
+
+# ------------------------------------------------------------------ hierarchical plan
+@pytest.mark.parametrize("order", [4, 5, 6])
+def test_hierarchical_all_perms(order, cuda_device):
+    """Every permutation with >= 2 runs of rearrangement indices, executed in stages
+    (LCO_FLAG_HIERARCHICAL), bit-exact vs the oracle with and without
+    values / permutation vector; stage paths vary with the segment sizes."""
+    rng = np.random.default_rng(60 + order)
+    dims = {4: (64, 64, 48, 64), 5: (24, 16, 20, 16, 24), 6: (8, 12, 8, 10, 8, 12)}[order]
+    keys, vals = _rand_sorted(rng, dims, 400_000)
+    seen = 0
+    for perm in itertools.permutations(range(order)):
+        if lco.plan(dims, perm, hierarchical=True).info(len(keys))["path"] != "hier":
+            continue
+        seen += 1
+        check(dims, perm, keys, vals, hierarchical=True)
+        if seen % 5 == 0:
+            check(dims, perm, keys, None, return_perm=False, hierarchical=True)
+    assert seen >= 2
+
+
+def test_hierarchical_c3b_three_buffers(cuda_device):
+    """C3b at full size (two stages: segmented pass, then segment-local tiles) and an
+    order-6 permutation with three runs of rearrangement indices (three stages, both
+    intermediate buffer sets)."""
+    w = workloads.config("C3")
+    perm = (0, 3, 1, 4, 2, 5)
+    assert lco.plan(w.dims, perm, hierarchical=True).info(w.keys.numel())["path"] == "hier"
+    check(w.dims, perm, _np_u64(w.keys), w.vals.numpy(), hierarchical=True)
+    rng = np.random.default_rng(66)
+    dims = (16, 16, 16, 16, 16, 16)
+    keys, vals = _rand_sorted(rng, dims, 2_000_000)
+    perm3 = (1, 0, 3, 2, 5, 4)
+    p = lco.plan(dims, perm3, hierarchical=True)
+    assert len(p.stages()) == 3 and p.info(len(keys))["path"] == "hier"
+    check(dims, perm3, keys, vals, hierarchical=True)
+    check(dims, perm3, keys, None, return_perm=False, hierarchical=True)
+    check(dims, perm3, keys, vals)  # the flat plan of the same handle dims
