@@ -218,6 +218,26 @@ LCO_API lco_status lco_profile_enable(lco_handle h, int calls);
 LCO_API lco_status lco_profile_read(lco_handle h, int max_calls, int max_stages, float* ms,
                             int* n_calls, int* n_stages, char* names, size_t names_len);
 
+/* Index-matched addition C = A + sign * permute(B, match) (§3.2, the
+ * sum of c^(y) and c^(x) in Eq (2.3) after re-sorting one term into the {1,0,3,2} order;
+ * SURVEY.md §8(f) NEXT 3).  h is the plan of B: B's dims and the match permutation, so
+ * that permute(B, match) is in A's mode order (A's dims = B's dims permuted).
+ *   keys_a/vals_a  nnz_a nonzeros of A, keys strictly increasing (row-major, A's order).
+ *   keys_b/vals_b  nnz_b nonzeros of B, keys strictly increasing in B's own order.
+ *   sign           scales B's values (+1 or -1 in the paper; any finite double).
+ *   keys_c/vals_c  capacity nnz_a + nnz_b; receive the union of the supports, ascending;
+ *                  colliding keys hold a + sign*b (one IEEE addition), explicit zeros kept.
+ *   nnz_c          [device] one uint64: the number of outputs written.
+ * Workspace: lco_add_workspace_size bytes, 256-byte aligned.  Stream-ordered, no sync.
+ * Errors: LCO_ERR_NULL / LCO_ERR_CAPACITY (nnz_b > max_nnz) / LCO_ERR_WORKSPACE /
+ * LCO_ERR_ALIAS (outputs overlap inputs or workspace) / LCO_ERR_CUDA. */
+LCO_API lco_status lco_add_workspace_size(lco_handle h, uint64_t nnz_a, uint64_t nnz_b,
+                                          size_t* bytes);
+LCO_API lco_status lco_add(lco_handle h, uint64_t nnz_a, const uint64_t* keys_a,
+                           const double* vals_a, uint64_t nnz_b, const uint64_t* keys_b,
+                           const double* vals_b, double sign, uint64_t* keys_c, double* vals_c,
+                           uint64_t* nnz_c, void* workspace, size_t workspace_bytes, void* stream);
+
 LCO_API const char* lco_status_string(lco_status s);
 LCO_API const char* lco_last_error(void);
 LCO_API const char* lco_version(void);

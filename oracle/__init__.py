@@ -60,6 +60,11 @@ def _get():
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        _lib.oracle_add.restype = ctypes.c_int
+        _lib.oracle_add.argtypes = [ctypes.c_int, u64p, ctypes.c_void_p, ctypes.c_uint64,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     return _lib
 
 
@@ -161,3 +166,22 @@ def partition(dims, perm, keys, vals, idx_base, splitters):
     _check(_get().oracle_partition(len(d), dp, p.ctypes.data, n, _ptr(k), _ptr(v), int(idx_base),
                                    world, _ptr(s), _ptr(sk), _ptr(sv), _ptr(si), _ptr(cnt)))
     return sk, sv, si, cnt
+
+
+def add(dims_b, match, keys_a, vals_a, keys_b, vals_b, sign=1.0):
+    """Index-matched addition C = A + sign * permute(B, match):
+    union of supports, collisions summed, explicit zeros kept, ascending keys."""
+    d, dp = _dims(dims_b)
+    p = _perm(match, len(d))
+    ka = np.ascontiguousarray(np.asarray(keys_a, dtype=np.uint64))
+    va = np.ascontiguousarray(np.asarray(vals_a, dtype=np.float64))
+    kb = np.ascontiguousarray(np.asarray(keys_b, dtype=np.uint64))
+    vb = np.ascontiguousarray(np.asarray(vals_b, dtype=np.float64))
+    kc = np.empty(len(ka) + len(kb), dtype=np.uint64)
+    vc = np.empty(len(ka) + len(kb), dtype=np.float64)
+    n = np.zeros(1, dtype=np.uint64)
+    _check(_get().oracle_add(len(d), dp, p.ctypes.data, len(ka), _ptr(ka), _ptr(va), len(kb),
+                             _ptr(kb), _ptr(vb), ctypes.c_double(sign), _ptr(kc), _ptr(vc),
+                             _ptr(n)))
+    m = int(n[0])
+    return kc[:m].copy(), vc[:m].copy()

@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <vector>
 
 namespace {
@@ -289,6 +290,47 @@ int oracle_partition(int order, const uint64_t* dims, const int32_t* perm, uint6
         send_idx[pos] = idx_base + (uint32_t)i;
         ++pos;
       }
+  return 0;
+}
+
+// Index-matched addition C = A + sign * B (§3.2 "one of the tensors must
+// be re-sorted into the {1,0,3,2} lexicographical order ... the run time for the addition
+// operation"; SPEC add(tA, tB, match, sign)): B (dims_b, sorted) is permuted by `match`
+// into A's mode order with oracle_permute, then the union of the two supports is formed
+// with a std::map from key to value (A's value first, then sign * B's added): every key
+// of either operand appears once, collisions are summed, explicit zeros are kept, and the
+// output is ascending.  A's keys must be unique (a sorted LCO tensor); values are fp64,
+// one IEEE addition per collision.  *nnz_c receives the output size (<= nnz_a + nnz_b).
+int oracle_add(int order, const uint64_t* dims_b, const int32_t* match, uint64_t nnz_a,
+               const uint64_t* keys_a, const double* vals_a, uint64_t nnz_b,
+               const uint64_t* keys_b, const double* vals_b, double sign, uint64_t* keys_c,
+               double* vals_c, uint64_t* nnz_c) {
+  if (order < 1 || !dims_b || !match || !nnz_c || (nnz_a && (!keys_a || !vals_a)) ||
+      (nnz_b && (!keys_b || !vals_b)))
+    return 1;
+  std::vector<uint64_t> kb(nnz_b);
+  std::vector<double> vb(nnz_b);
+  std::vector<uint32_t> pb(nnz_b);
+  int rc = oracle_permute(order, dims_b, match, nnz_b, keys_b, vals_b, nullptr, kb.data(),
+                          vb.data(), pb.data());
+  if (rc) return rc;
+  std::map<uint64_t, double> c;
+  for (uint64_t i = 0; i < nnz_a; ++i) {
+    if (c.count(keys_a[i])) return 1;  // A must have unique keys
+    c[keys_a[i]] = vals_a[i];
+  }
+  for (uint64_t i = 0; i < nnz_b; ++i) {
+    auto it = c.find(kb[i]);
+    if (it == c.end()) c[kb[i]] = sign * vb[i];
+    else it->second = it->second + sign * vb[i];
+  }
+  uint64_t j = 0;
+  for (const auto& kv : c) {
+    keys_c[j] = kv.first;
+    vals_c[j] = kv.second;
+    ++j;
+  }
+  *nnz_c = j;
   return 0;
 }
 

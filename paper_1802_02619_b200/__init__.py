@@ -3,8 +3,10 @@
 The work runs in liblco.so (hand-written sm_100a CUDA behind the C ABI in
 include/lco.h); this package is the thin Python binding plus the sharded driver.
 """
-from .lco import (FLAG_VALIDATE, LcoError, LcoValueError, Plan, fastdiv_host, lib, permute,
+from .lco import (FLAG_HIERARCHICAL, FLAG_VALIDATE, LcoError, LcoValueError, Plan, add,
+                  fastdiv_host, lib, permute,
                   plan, sort, version)
 
-__all__ = ["FLAG_VALIDATE", "LcoError", "LcoValueError", "Plan", "fastdiv_host", "lib",
+__all__ = ["FLAG_HIERARCHICAL", "FLAG_VALIDATE", "LcoError", "LcoValueError", "Plan", "add",
+           "fastdiv_host", "lib",
            "permute", "plan", "sort", "version"]

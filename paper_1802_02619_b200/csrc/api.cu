@@ -633,6 +633,76 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
   return LCO_OK;
 }
 
+lco_status lco_add_workspace_size(lco_handle h, uint64_t nnz_a, uint64_t nnz_b, size_t* bytes) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (!bytes) {
+    set_error("bytes is NULL");
+    return LCO_ERR_NULL;
+  }
+  size_t inner = 0;
+  if ((st = lco_workspace_size(h, nnz_b, &inner)) != LCO_OK) return st;
+  *bytes = 2 * align_up(nnz_b * 8) + align_up(merge_ctrl_bytes(nnz_a, nnz_b)) + inner;
+  return LCO_OK;
+}
+
+lco_status lco_add(lco_handle h, uint64_t nnz_a, const uint64_t* keys_a, const double* vals_a,
+                   uint64_t nnz_b, const uint64_t* keys_b, const double* vals_b, double sign,
+                   uint64_t* keys_c, double* vals_c, uint64_t* nnz_c, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (!nnz_c || !keys_c || !vals_c || (nnz_a && (!keys_a || !vals_a)) ||
+      (nnz_b && (!keys_b || !vals_b))) {
+    set_error("nnz_c, keys_c, vals_c and the non-empty operands are required");
+    return LCO_ERR_NULL;
+  }
+  if (nnz_b > h->max_nnz || nnz_b >= (1ull << 32) || nnz_a >= (1ull << 32)) {
+    set_error("nnz_b above max_nnz, or an operand with 2^32 nonzeros or more");
+    return LCO_ERR_CAPACITY;
+  }
+  size_t need = 0;
+  lco_add_workspace_size(h, nnz_a, nnz_b, &need);
+  if (!workspace || workspace_bytes < need || reinterpret_cast<uintptr_t>(workspace) % kAlign) {
+    set_error("workspace needs %zu bytes, 256-byte aligned", need);
+    return LCO_ERR_WORKSPACE;
+  }
+  const size_t nc = (size_t)(nnz_a + nnz_b);
+  const void* ins[4] = {keys_a, vals_a, keys_b, vals_b};
+  const size_t insz[4] = {nnz_a * 8, nnz_a * 8, nnz_b * 8, nnz_b * 8};
+  const void* outs[3] = {keys_c, vals_c, nnz_c};
+  const size_t outsz[3] = {nc * 8, nc * 8, 8};
+  for (int i = 0; i < 3; ++i) {
+    for (int j = 0; j < 4; ++j)
+      if (overlaps(outs[i], outsz[i], ins[j], insz[j])) {
+        set_error("output %d overlaps input %d", i, j);
+        return LCO_ERR_ALIAS;
+      }
+    if (overlaps(outs[i], outsz[i], workspace, need)) {
+      set_error("output %d overlaps the workspace", i);
+      return LCO_ERR_ALIAS;
+    }
+  }
+  char* ws = static_cast<char*>(workspace);
+  uint64_t* kb2 = reinterpret_cast<uint64_t*>(ws);
+  double* vb2 = reinterpret_cast<double*>(ws + align_up(nnz_b * 8));
+  char* mctrl = ws + 2 * align_up(nnz_b * 8);
+  char* inner = mctrl + align_up(merge_ctrl_bytes(nnz_a, nnz_b));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // B -> A's order: the permutation hot path ("re-sorted into the {1,0,3,2}
+  // lexicographical order")
+  st = lco_permute(h, nnz_b, keys_b, vals_b, nullptr, kb2, vb2, nullptr, inner,
+                   workspace_bytes - (inner - ws), stream);
+  if (st) return st;
+  Launch L{s, nullptr, nullptr};
+  ProfCtx pc;
+  const bool prof = prof_begin(h, s, &pc, &L);
+  cudaError_t e = run_merge(nnz_a, keys_a, vals_a, nnz_b, kb2, vb2, sign, keys_c, vals_c, nnz_c,
+                            mctrl, L);
+  if (prof) prof_end(&pc);
+  return e == cudaSuccess ? LCO_OK : cuda_fail(e, "lco_add");
+}
+
 lco_status lco_key_histogram(lco_handle h, uint64_t nnz, const uint64_t* keys_in, int bits,
                              uint64_t* counts, void* stream) {
   lco_status st = check_handle(h);

@@ -81,6 +81,12 @@ size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
 cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
 uint32_t tile_nominal(uint64_t nnz, uint64_t segments);  // segment-local path (msd.cu)
 cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const Launch& L);
+// index-matched addition (add.cu)
+uint64_t merge_tiles(uint64_t na, uint64_t nb);
+size_t merge_ctrl_bytes(uint64_t na, uint64_t nb);
+cudaError_t run_merge(uint64_t na, const uint64_t* ka, const double* va, uint64_t nb,
+                      const uint64_t* kb, const double* vb, double sign, uint64_t* kc,
+                      double* vc, uint64_t* nnz_c, void* ctrl, const Launch& L);
 size_t tile_ctrl_bytes(uint64_t nnz, uint64_t segments);
 cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int key_bits,
                       const PassIO& io, const Launch& L);

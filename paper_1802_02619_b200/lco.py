@@ -90,6 +90,9 @@ _SIGS = {
     "lco_partition": (ctypes.c_int, [_P, _U64, _P, _P, ctypes.c_uint32, ctypes.c_int, _P, _P, _P,
                                      _P, _P, _P, ctypes.c_size_t, _P]),
     "lco_key_histogram": (ctypes.c_int, [_P, _U64, _P, ctypes.c_int, _P, _P]),
+    "lco_add_workspace_size": (ctypes.c_int, [_P, _U64, _U64, ctypes.POINTER(ctypes.c_size_t)]),
+    "lco_add": (ctypes.c_int, [_P, _U64, _P, _P, _U64, _P, _P, ctypes.c_double, _P, _P, _P, _P,
+                               ctypes.c_size_t, _P]),
     "lco_plan_query": (ctypes.c_int, [_P, _U64, ctypes.c_int, ctypes.POINTER(PlanInfo)]),
     "lco_plan_stage": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_U64),
@@ -273,6 +276,48 @@ class Plan:
                       wptr, wlen, _stream_ptr(stream, dev)))
         return ko, vo, po
 
+    def add_workspace_size(self, nnz_a: int, nnz_b: int) -> int:
+        b = ctypes.c_size_t()
+        _check(lib().lco_add_workspace_size(self._h, int(nnz_a), int(nnz_b), ctypes.byref(b)))
+        return b.value
+
+    def add(self, keys_a, vals_a, keys_b, vals_b, sign=1.0, stream=None, out=None,
+            workspace=None, trim=True):
+        """Index-matched addition (lco_add): A + sign * permute(B, match) where this plan
+        holds B's dims and the match.  Returns (keys_c, vals_c, nnz_c); with trim=True the
+        outputs are cut to nnz_c (one device->host read of the count)."""
+        for t in (keys_a, vals_a, keys_b, vals_b):
+            if not t.is_cuda:
+                raise ValueError("operands must be CUDA tensors (no CPU fallback)")
+        dev = keys_a.device
+        na, nb = keys_a.numel(), keys_b.numel()
+        if vals_a.numel() != na or vals_b.numel() != nb:
+            raise ValueError("keys and values of an operand must have the same length")
+        if vals_a.dtype != torch.float64 or vals_b.dtype != torch.float64:
+            raise ValueError("values must be float64")
+        keys_a, vals_a = keys_a.contiguous(), vals_a.contiguous()
+        keys_b, vals_b = keys_b.contiguous(), vals_b.contiguous()
+        if out is None:
+            kc = torch.empty(na + nb, dtype=keys_a.dtype, device=dev)
+            vc = torch.empty(na + nb, dtype=torch.float64, device=dev)
+            nc = torch.zeros(1, dtype=torch.int64, device=dev)
+        else:
+            kc, vc, nc = out
+        if workspace is None:
+            ws, off = _workspace(self.add_workspace_size(na, nb), dev)
+        else:
+            ws, off = workspace, (-workspace.data_ptr()) % 256
+        wptr = None if ws is None else ctypes.c_void_p(ws.data_ptr() + off)
+        wlen = 0 if ws is None else ws.numel() - off
+        with torch.cuda.device(dev):
+            _check(lib().lco_add(self._h, na, _ptr(keys_a), _ptr(vals_a), nb, _ptr(keys_b),
+                                 _ptr(vals_b), float(sign), _ptr(kc), _ptr(vc), _ptr(nc), wptr,
+                                 wlen, _stream_ptr(stream, dev)))
+        if trim:
+            m = int(nc.item())
+            return kc[:m], vc[:m], m
+        return kc, vc, nc
+
     def permute(self, keys, vals=None, idx=None, return_perm=True, stream=None, out=None,
                 workspace=None):
         return self._run(lib().lco_permute, keys, vals, idx, return_perm, stream, out, workspace)
@@ -370,6 +415,13 @@ def permute(keys, vals, dims, perm, idx=None, return_perm=True, validate=False, 
     """Permute a sorted LCO tensor: returns (keys_out, vals_out, perm_out)."""
     return plan(dims, perm, validate=validate, hierarchical=hierarchical).permute(
         keys, vals, idx, return_perm, stream)
+
+
+def add(keys_a, vals_a, keys_b, vals_b, dims_b, match, sign=1.0, stream=None):
+    """Index-matched addition A + sign * permute(B, match): B has dims
+    dims_b and is sorted in its own order; A is sorted in the matched order.  Returns the
+    trimmed (keys_c, vals_c, nnz_c)."""
+    return plan(dims_b, match).add(keys_a, vals_a, keys_b, vals_b, sign, stream)
 
 
 def sort(keys, vals, dims, perm=None, idx=None, return_perm=True, validate=False, stream=None):

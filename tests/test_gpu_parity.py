@@ -468,3 +468,67 @@ def test_hierarchical_c3b_three_buffers(cuda_device):
     check(dims, perm3, keys, vals, hierarchical=True)
     check(dims, perm3, keys, None, return_perm=False, hierarchical=True)
     check(dims, perm3, keys, vals)  # the flat plan of the same handle dims
+
+
+# ------------------------------------------------------------------ index-matched addition
+def _check_add(dims_b, match, ka, va, kb, vb, sign, dev="cuda:0"):
+    t = lambda a, dt: torch.as_tensor(np.asarray(a, dtype=dt)).to(dev)
+    kc, vc, m = lco.plan(dims_b, match).add(t(np.asarray(ka, np.uint64).view(np.int64), np.int64),
+                                            t(va, np.float64),
+                                            t(np.asarray(kb, np.uint64).view(np.int64), np.int64),
+                                            t(vb, np.float64), sign)
+    ek, ev = oracle.add(dims_b, match, ka, va, kb, vb, sign)
+    assert m == len(ek), (m, len(ek))
+    assert np.array_equal(_np_u64(kc), ek)
+    assert np.array_equal(vc.cpu().numpy().view(np.uint64), ev.view(np.uint64))
+
+
+@pytest.mark.parametrize("order", [3, 4])
+def test_add_random_all_matches(order, cuda_device):
+    """A + s * permute(B, match) for every match: overlapping supports (collisions summed,
+    explicit zeros kept), several merge tiles, duplicates straddling tile boundaries."""
+    rng = np.random.default_rng(70 + order)
+    dims_b = {3: (40, 33, 50), 4: (12, 17, 10, 14)}[order]
+    for match in itertools.permutations(range(order)):
+        dims_a = tuple(dims_b[m] for m in match)
+        kb, vb = _rand_sorted(rng, dims_b, 20_000)
+        kbp = np.sort(oracle.shuffle(dims_b, match, kb))
+        ka = np.union1d(kbp[::3], np.sort(rng.choice(int(np.prod(dims_a)), 9_000, replace=False)))
+        ka = ka.astype(np.uint64)
+        va = rng.standard_normal(len(ka))
+        _check_add(dims_b, match, ka, va, kb, vb, 1.0 if sum(match) % 2 else -1.0)
+
+
+def test_add_edge_cases(cuda_device):
+    rng = np.random.default_rng(77)
+    dims = (64, 48, 32)
+    k, v = _rand_sorted(rng, dims, 30_000)
+    _check_add(dims, (0, 1, 2), k, v, k, v, -1.0)          # t - t: explicit zeros
+    _check_add(dims, (2, 0, 1), k[:0], v[:0], k, v, 1.0)   # empty A
+    dims_a = (32, 64, 48)
+    ka, va = _rand_sorted(rng, dims_a, 10_000)
+    _check_add(dims, (2, 0, 1), ka, va, k[:0], v[:0], -1.0)  # empty B
+    _check_add(dims, (2, 0, 1), ka[:1], va[:1], k[:1], v[:1], 1.0)
+
+
+def test_add_laplacian_paper_match(cuda_device):
+    """The paper's addition: two order-4 operator tensors, one
+    re-sorted into the {1,0,3,2} order; the 5-point Laplacian is axis-swap symmetric, so
+    A + permute(A) = 2A (closed form) - and vs the oracle at full C2 size."""
+    w = workloads.config("C2")
+    k, v = _np_u64(w.keys), w.vals.numpy()
+    _check_add(w.dims, (1, 0, 3, 2), k, v, k, v, 1.0)
+    kc, vc, m = lco.add(w.keys.cuda(), w.vals.cuda(), w.keys.cuda(), w.vals.cuda(), w.dims,
+                        (1, 0, 3, 2))
+    assert m == len(k) and torch.equal(vc.cpu(), 2.0 * w.vals)
+
+
+def test_add_eq23_assembly(cuda_device):
+    """Eq (2.3) assembled on the GPU: term + permute(term, {1,0,3,2}) = the combinatorial
+    Laplacian (closed form), and bit-exact vs the oracle."""
+    n = 300
+    k, v = workloads.eq23_term(n)
+    _check_add((n,) * 4, (1, 0, 3, 2), _np_u64(k), v.numpy(), _np_u64(k), v.numpy(), 1.0)
+    kc, vc, m = lco.add(k.cuda(), v.cuda(), k.cuda(), v.cuda(), (n,) * 4, (1, 0, 3, 2))
+    ek, ev = workloads.combinatorial_laplacian(n)
+    assert torch.equal(kc.cpu(), ek) and torch.equal(vc.cpu(), ev)

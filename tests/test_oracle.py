@@ -227,3 +227,79 @@ def test_errors():
         oracle.rp_permute((4, 4), (1, 0), [3, 2])  # RP precondition: sorted input
     ko, vo, po = oracle.permute((4, 4), (1, 0), np.zeros(0, np.uint64), np.zeros(0))
     assert len(ko) == 0
+
+
+# ------------------------------------------------------------------ index-matched addition
+def test_add_self_negation_keeps_explicit_zeros():
+    """t + (-1) t over the identity match: t's support with +0.0 everywhere (SPEC add:
+    explicit zeros retained)."""
+    w = workloads.config("C1")
+    k, v = w.keys.numpy().astype(np.uint64), w.vals.numpy()
+    kc, vc = oracle.add(w.dims, tuple(range(len(w.dims))), k, v, k, v, -1.0)
+    assert np.array_equal(kc, k)
+    assert np.array_equal(vc.view(np.uint64), np.zeros(len(k), dtype=np.uint64))
+
+
+def test_add_disjoint_supports_concatenate():
+    rng = np.random.default_rng(3)
+    dims = (7, 9, 11)
+    total = int(np.prod(dims))
+    keys = rng.choice(total, 300, replace=False)
+    ka, kb = np.sort(keys[:120]).astype(np.uint64), keys[120:]
+    perm = (2, 0, 1)
+    # B given in its own order: invert the match on B's keys so that permute(B) = kb
+    inv = tuple(int(x) for x in np.argsort(perm))
+    dims_b = tuple(dims[i] for i in inv)
+    kb_own = np.sort(oracle.shuffle(dims, inv, kb.astype(np.uint64)))
+    va, vb = rng.standard_normal(120), rng.standard_normal(180)
+    kc, vc = oracle.add(dims_b, perm, ka, va, kb_own, vb, 1.0)
+    assert len(kc) == 300 and np.array_equal(kc, np.sort(keys).astype(np.uint64))
+    assert bool(np.all(np.diff(kc.astype(np.int64)) > 0))
+
+
+@pytest.mark.parametrize("order", [2, 3, 4])
+def test_add_dense_bruteforce(order):
+    """Dense oracle: C = A + s * transpose(B, match) on dense arrays; C's support is the
+    union of the supports (explicit zeros where values cancel), values match exactly."""
+    rng = np.random.default_rng(40 + order)
+    for match in itertools.permutations(range(order)):
+        dims_b = tuple(int(x) for x in rng.integers(1, 6, order))
+        dims_a = tuple(dims_b[m] for m in match)
+        B = np.where(rng.random(dims_b) < 0.4, rng.integers(-3, 4, dims_b).astype(float), 0.0)
+        A = np.where(rng.random(dims_a) < 0.4, rng.integers(-3, 4, dims_a).astype(float), 0.0)
+        Bm = np.zeros(dims_b, dtype=bool)
+        Bm[B != 0] = True
+        Am = A != 0
+        sign = -1.0 if order % 2 else 1.0
+        ka = np.flatnonzero(Am).astype(np.uint64)
+        kb = np.flatnonzero(Bm).astype(np.uint64)
+        kc, vc = oracle.add(dims_b, match, ka, A.ravel()[ka], kb, B.ravel()[kb], sign)
+        dense = A + sign * np.transpose(B, match)
+        support = Am | np.transpose(Bm, match)
+        assert np.array_equal(kc, np.flatnonzero(support).astype(np.uint64)), (dims_b, match)
+        assert np.array_equal(vc, dense.ravel()[kc])
+
+
+def test_add_laplacian_axis_swap_doubles():
+    """Closed form: the 2-D 5-point Laplacian operator (modes x, y, x', y') is symmetric
+    under swapping the axes, so with the paper's addition match {1,0,3,2}
+    A + permute(A) = 2A exactly, keys unchanged."""
+    w = workloads.config("C2", scale=12)
+    k, v = w.keys.numpy().astype(np.uint64), w.vals.numpy()
+    perm = paper_lex_to_perm((1, 0, 3, 2))
+    assert perm == (1, 0, 3, 2)
+    kc, vc = oracle.add(w.dims, perm, k, v, k, v, 1.0)
+    assert np.array_equal(kc, k) and np.array_equal(vc, 2.0 * v)
+
+
+def test_add_eq23_assembly():
+    """SPEC add example (Eq 2.3, :212-214): the two d.d terms, one re-sorted into
+    the {1,0,3,2} order and added, give the combinatorial Laplacian a_ijkl (support of
+    5 neighbours per (i, j), diagonal -1/2 - 1/2 = -1, off-diagonal 1/4)."""
+    for n in (6, 9):
+        k, v = workloads.eq23_term(n)
+        k, v = k.numpy().astype(np.uint64), v.numpy()
+        kc, vc = oracle.add((n,) * 4, (1, 0, 3, 2), k, v, k, v, 1.0)
+        ek, ev = workloads.combinatorial_laplacian(n)
+        assert np.array_equal(kc, ek.numpy().astype(np.uint64))
+        assert np.array_equal(vc, ev.numpy())

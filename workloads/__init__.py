@@ -167,6 +167,18 @@ def combinatorial_laplacian(n, device="cpu"):
     return _stencil(n, 2, offs, device)
 
 
+def eq23_term(n, device="cpu"):
+    """One of the two terms of PAPER.md Eq (2.3) as stored after its product: the
+    d(y) d(y) term c^(y)_{ijkl} = d(y)_ii' delta_jl d(y)_i'k couples (i, j) to
+    (i + {-2, 0, 2}, j) with the coefficients of d.d (d the central difference of Eq 2.1):
+    1/4, -1/2, 1/4.  The d(x) term in its own index order (j, i, l, k) has the same
+    layout, so both operands of the paper's addition come from this generator, and
+    term + permute(term, {1,0,3,2}) is the combinatorial Laplacian (same support and
+    coefficients as combinatorial_laplacian)."""
+    offs = [((-2, 0), 0.25), ((0, 0), -0.5), ((2, 0), 0.25)]
+    return _stencil(n, 2, offs, device)
+
+
 def fill_tensor(n, fill, seed, device="cpu"):
     """Order-4 n^4 tensor with a constant fill factor (PAPER.md:261 '2% fill')."""
     return random_tensor((n,) * 4, int(round(fill * n ** 4)), seed, "uniform", device)
