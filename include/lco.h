@@ -238,6 +238,39 @@ LCO_API lco_status lco_add(lco_handle h, uint64_t nnz_a, const uint64_t* keys_a,
                            const double* vals_b, double sign, uint64_t* keys_c, double* vals_c,
                            uint64_t* nnz_c, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- Matrix datatypes of a flattened tensor (§5.2 steps 1-2, :325-331;
+ * SURVEY.md §8(f) NEXT 4).  Flattening a tensor into an m x n matrix is a permutation
+ * (rows modes first, then column modes; lco_permute) -- a row-major LCO matrix has key
+ * row * n + col, a column-major one col * m + row.  Compression never sorts. */
+
+/* Compress a major-first LCO matrix: keys strictly increasing, key = major * n_minor +
+ * minor (CSR/DCSR from a row-major matrix: major = row; CSC/DCSC from a column-major
+ * one: major = column).  The values array of the LCO matrix is the MDT's value array.
+ *   doubly = 0 (CSR/CSC): ptr [n_major + 1] with ptr[r] = first nonzero of major >= r.
+ *   doubly = 1 (DCSR/DCSC, Buluc & Gilbert): ids [capacity nnz] receives
+ *            the non-empty majors ascending, ptr [capacity nnz + 1] their starts and
+ *            ptr[nz] = nnz, *n_nonempty [device] = nz; nothing is O(n_major).
+ *   minor    [nnz] receives key mod n_minor.
+ * Workspace: lco_compress_workspace_size (0 for doubly = 0).  Stream-ordered. */
+LCO_API lco_status lco_compress_workspace_size(uint64_t nnz, int doubly, size_t* bytes);
+LCO_API lco_status lco_compress(uint64_t nnz, const uint64_t* keys, uint64_t n_major,
+                                uint64_t n_minor, int doubly, uint64_t* ptr, uint64_t* ids,
+                                uint64_t* minor, uint64_t* n_nonempty, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* Hyper-sparsity of an m x n matrix with nnz nonzeros ("the ratio of NNZ to
+ * the dimension in question"; LibNT switches algorithms at ratio 3, :483): 0 sparse,
+ * 1 row-sparse (m / nnz > threshold, very tall), 2 column-sparse (n / nnz > threshold,
+ * very wide), 3 index-sparse (both).  nnz = 0 -> 0.  Host only. */
+LCO_API int lco_sparsity_class(uint64_t m, uint64_t n, uint64_t nnz, double threshold);
+
+/* The MDT / algorithm of the multiplication poly-algorithm for C = A B given the classes
+ * of A and B (PAPER.md Table "Multiplication possibilities", :340-352): returns a code
+ * whose name lco_mdt_name gives ("CSC/CSR", "CSC", "CSR", "DCSC/DCSR", "DCSC", "DCSR",
+ * "CSCNA/CSRNA", "CSCNA", "CSRNA", "SOP"); -1 for invalid classes.  Host only. */
+LCO_API int lco_mdt_choice(int class_a, int class_b);
+LCO_API const char* lco_mdt_name(int code);
+
 LCO_API const char* lco_status_string(lco_status s);
 LCO_API const char* lco_last_error(void);
 LCO_API const char* lco_version(void);

@@ -60,6 +60,10 @@ def _get():
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
                                           ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        _lib.oracle_compress.restype = ctypes.c_int
+        _lib.oracle_compress.argtypes = [ctypes.c_uint64, ctypes.c_void_p, ctypes.c_uint64,
+                                         ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p,
+                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         _lib.oracle_add.restype = ctypes.c_int
         _lib.oracle_add.argtypes = [ctypes.c_int, u64p, ctypes.c_void_p, ctypes.c_uint64,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
@@ -185,3 +189,23 @@ def add(dims_b, match, keys_a, vals_a, keys_b, vals_b, sign=1.0):
                              _ptr(n)))
     m = int(n[0])
     return kc[:m].copy(), vc[:m].copy()
+
+
+def compress(keys, n_major, n_minor, doubly=False):
+    """CSR/CSC (doubly=False): (ptr[n_major+1], minor); DCSR/DCSC: (ids, ptr[nz+1], minor),
+    from a major-first LCO matrix (§5.2 step 2)."""
+    k = np.ascontiguousarray(np.asarray(keys, dtype=np.uint64))
+    n = len(k)
+    minor = np.empty(n, dtype=np.uint64)
+    if not doubly:
+        ptr = np.empty(int(n_major) + 1, dtype=np.uint64)
+        _check(_get().oracle_compress(n, _ptr(k), int(n_major), int(n_minor), 0, _ptr(ptr), None,
+                                      _ptr(minor), None))
+        return ptr, minor
+    ids = np.empty(max(n, 1), dtype=np.uint64)
+    ptr = np.empty(n + 1, dtype=np.uint64)
+    nz = np.zeros(1, dtype=np.uint64)
+    _check(_get().oracle_compress(n, _ptr(k), int(n_major), int(n_minor), 1, _ptr(ptr), _ptr(ids),
+                                  _ptr(minor), _ptr(nz)))
+    m = int(nz[0])
+    return ids[:m].copy(), ptr[:m + 1].copy(), minor

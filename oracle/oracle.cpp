@@ -334,4 +334,38 @@ int oracle_add(int order, const uint64_t* dims_b, const int32_t* match, uint64_t
   return 0;
 }
 
+// Compression of a major-first LCO matrix into CSR/CSC (doubly = 0) or DCSR/DCSC
+// (doubly = 1) (§5.2 step 2, :325-331, :453), by the definitions: major =
+// key / n_minor, minor = key % n_minor; singly: ptr[r] = number of nonzeros with major
+// < r (r = 0..n_major); doubly: ids = the distinct majors in order, ptr[j] = position of
+// the first nonzero of ids[j], ptr[nz] = nnz.  Keys must be strictly increasing.
+int oracle_compress(uint64_t nnz, const uint64_t* keys, uint64_t n_major, uint64_t n_minor,
+                    int doubly, uint64_t* ptr, uint64_t* ids, uint64_t* minor, uint64_t* nz) {
+  if (!ptr || !minor || n_minor == 0 || (nnz && !keys) || (doubly && (!ids || !nz))) return 1;
+  for (uint64_t i = 0; i < nnz; ++i) {
+    if (keys[i] / n_minor >= n_major) return 2;
+    if (i && keys[i] <= keys[i - 1]) return 1;
+    minor[i] = keys[i] % n_minor;
+  }
+  if (!doubly) {
+    std::vector<uint64_t> count(n_major, 0);
+    for (uint64_t i = 0; i < nnz; ++i) count[keys[i] / n_minor] += 1;
+    ptr[0] = 0;
+    for (uint64_t r = 0; r < n_major; ++r) ptr[r + 1] = ptr[r] + count[r];
+    return 0;
+  }
+  uint64_t j = 0;
+  for (uint64_t i = 0; i < nnz; ++i) {
+    const uint64_t r = keys[i] / n_minor;
+    if (i == 0 || r != keys[i - 1] / n_minor) {
+      ids[j] = r;
+      ptr[j] = i;
+      ++j;
+    }
+  }
+  ptr[j] = nnz;
+  *nz = j;
+  return 0;
+}
+
 }  // extern "C"

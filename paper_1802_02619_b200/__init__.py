@@ -4,9 +4,9 @@ The work runs in liblco.so (hand-written sm_100a CUDA behind the C ABI in
 include/lco.h); this package is the thin Python binding plus the sharded driver.
 """
 from .lco import (FLAG_HIERARCHICAL, FLAG_VALIDATE, LcoError, LcoValueError, Plan, add,
-                  fastdiv_host, lib, permute,
-                  plan, sort, version)
+                  compress, fastdiv_host, flatten, lib, mdt_choice, permute, plan, sort,
+                  sparsity_class, version)
 
 __all__ = ["FLAG_HIERARCHICAL", "FLAG_VALIDATE", "LcoError", "LcoValueError", "Plan", "add",
-           "fastdiv_host", "lib",
-           "permute", "plan", "sort", "version"]
+           "compress", "fastdiv_host", "flatten", "lib", "mdt_choice", "permute", "plan", "sort",
+           "sparsity_class", "version"]

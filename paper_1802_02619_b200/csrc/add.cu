@@ -234,6 +234,13 @@ __global__ void __launch_bounds__(1024) k_merge_scan(const uint32_t* __restrict_
   if (tid == 0) *nnz_c = s_carry;
 }
 
+cudaError_t run_count_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, uint64_t* total,
+                           const Launch& L) {
+  if (L.mark) L.mark(L.ctx, "k_count_scan");
+  k_merge_scan<<<1, 1024, 0, L.stream>>>(counts, n, offsets, total);
+  return cudaGetLastError();
+}
+
 uint64_t merge_tiles(uint64_t na, uint64_t nb) { return (na + nb + kMTile - 1) / kMTile; }
 
 size_t merge_ctrl_bytes(uint64_t na, uint64_t nb) {

@@ -633,6 +633,65 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
   return LCO_OK;
 }
 
+lco_status lco_compress_workspace_size(uint64_t nnz, int doubly, size_t* bytes) {
+  if (!bytes) {
+    set_error("bytes is NULL");
+    return LCO_ERR_NULL;
+  }
+  *bytes = doubly ? align_up(compress_ctrl_bytes(nnz)) : 0;
+  return LCO_OK;
+}
+
+lco_status lco_compress(uint64_t nnz, const uint64_t* keys, uint64_t n_major, uint64_t n_minor,
+                        int doubly, uint64_t* ptr, uint64_t* ids, uint64_t* minor,
+                        uint64_t* n_nonempty, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  if (!ptr || (nnz && (!keys || !minor)) || (doubly && (!ids || !n_nonempty))) {
+    set_error("ptr, keys, minor (and ids, n_nonempty when doubly) are required");
+    return LCO_ERR_NULL;
+  }
+  if (n_minor == 0 || n_major == 0 || n_major > 0x7fffffffffffffffull / n_minor) {
+    set_error("n_major and n_minor must be positive with a product <= 2^63-1");
+    return LCO_ERR_DIM;
+  }
+  size_t need = 0;
+  lco_compress_workspace_size(nnz, doubly, &need);
+  if (need && (!workspace || workspace_bytes < need ||
+               reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
+    set_error("workspace needs %zu bytes, 256-byte aligned", need);
+    return LCO_ERR_WORKSPACE;
+  }
+  Launch L{static_cast<cudaStream_t>(stream), nullptr, nullptr};
+  const cudaError_t e = run_compress(nnz, keys, n_major, n_minor, doubly, ptr, ids, minor,
+                                     n_nonempty, workspace, L);
+  return e == cudaSuccess ? LCO_OK : cuda_fail(e, "lco_compress");
+}
+
+int lco_sparsity_class(uint64_t m, uint64_t n, uint64_t nnz, double threshold) {
+  if (nnz == 0) return 0;
+  const bool row = (double)m / (double)nnz > threshold, col = (double)n / (double)nnz > threshold;
+  return row && col ? 3 : (row ? 1 : (col ? 2 : 0));
+}
+
+// PAPER.md Table "Multiplication possibilities" (:340-352), rows = A, columns = B, in the
+// class order sparse, row-sparse, column-sparse, index-sparse.
+int lco_mdt_choice(int class_a, int class_b) {
+  enum { CSC_CSR = 0, CSC, CSR, DCSC_DCSR, DCSC, DCSR, CSCNA_CSRNA, CSCNA, CSRNA, SOP };
+  static const int table[4][4] = {
+      /* A sparse        */ {CSC_CSR, CSC, CSC, CSC},
+      /* A row-sparse    */ {CSR, DCSR, CSCNA_CSRNA, CSCNA},
+      /* A column-sparse */ {CSR, DCSC_DCSR, DCSC, DCSC},
+      /* A index-sparse  */ {CSR, DCSR, CSRNA, SOP}};
+  if (class_a < 0 || class_a > 3 || class_b < 0 || class_b > 3) return -1;
+  return table[class_a][class_b];
+}
+
+const char* lco_mdt_name(int code) {
+  static const char* names[] = {"CSC/CSR", "CSC", "CSR", "DCSC/DCSR", "DCSC",
+                                "DCSR", "CSCNA/CSRNA", "CSCNA", "CSRNA", "SOP"};
+  return code >= 0 && code < 10 ? names[code] : "invalid";
+}
+
 lco_status lco_add_workspace_size(lco_handle h, uint64_t nnz_a, uint64_t nnz_b, size_t* bytes) {
   lco_status st = check_handle(h);
   if (st) return st;

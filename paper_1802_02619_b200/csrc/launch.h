@@ -81,6 +81,14 @@ size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
 cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
 uint32_t tile_nominal(uint64_t nnz, uint64_t segments);  // segment-local path (msd.cu)
 cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const Launch& L);
+// exclusive scan of n uint32 counts into uint64 offsets and *total (one CTA, add.cu)
+cudaError_t run_count_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, uint64_t* total,
+                           const Launch& L);
+// compressed matrix datatypes (mdt.cu)
+size_t compress_ctrl_bytes(uint64_t nnz);
+cudaError_t run_compress(uint64_t nnz, const uint64_t* keys, uint64_t n_major, uint64_t n_minor,
+                         int doubly, uint64_t* ptr, uint64_t* ids, uint64_t* minor,
+                         uint64_t* n_nonempty, void* ctrl, const Launch& L);
 // index-matched addition (add.cu)
 uint64_t merge_tiles(uint64_t na, uint64_t nb);
 size_t merge_ctrl_bytes(uint64_t na, uint64_t nb);

@@ -12,6 +12,7 @@ Names follow the C ABI: ``permute`` (lco_permute), ``sort`` (lco_sort),
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import threading
 
@@ -91,6 +92,12 @@ _SIGS = {
                                      _P, _P, _P, ctypes.c_size_t, _P]),
     "lco_key_histogram": (ctypes.c_int, [_P, _U64, _P, ctypes.c_int, _P, _P]),
     "lco_add_workspace_size": (ctypes.c_int, [_P, _U64, _U64, ctypes.POINTER(ctypes.c_size_t)]),
+    "lco_compress_workspace_size": (ctypes.c_int, [_U64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+    "lco_compress": (ctypes.c_int, [_U64, _P, _U64, _U64, ctypes.c_int, _P, _P, _P, _P, _P,
+                                    ctypes.c_size_t, _P]),
+    "lco_sparsity_class": (ctypes.c_int, [_U64, _U64, _U64, ctypes.c_double]),
+    "lco_mdt_choice": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "lco_mdt_name": (ctypes.c_char_p, [ctypes.c_int]),
     "lco_add": (ctypes.c_int, [_P, _U64, _P, _P, _U64, _P, _P, ctypes.c_double, _P, _P, _P, _P,
                                ctypes.c_size_t, _P]),
     "lco_plan_query": (ctypes.c_int, [_P, _U64, ctypes.c_int, ctypes.POINTER(PlanInfo)]),
@@ -436,3 +443,66 @@ def fastdiv_host(d: int, xs) -> list:
     qa = (ctypes.c_uint64 * max(n, 1))()
     _check(lib().lco_fastdiv_host(int(d), n, ctypes.cast(xa, _P), ctypes.cast(qa, _P)))
     return [int(qa[i]) for i in range(n)]
+
+
+# ------------------------------------------------------------ matrix datatypes (§5.2)
+SPARSITY = ("sparse", "row-sparse", "column-sparse", "index-sparse")
+
+
+def flatten(keys, vals, dims, rows, cols, major="row", stream=None):
+    """Flatten (matricize) a sorted LCO tensor (§5.2 step 1): `rows` / `cols`
+    are the modes mapped to the matrix rows / columns (disjoint, covering all modes, in
+    the order wanted).  The permutation into (rows, cols) (row-major) or (cols, rows)
+    (column-major) order runs on the GPU (lco_permute; the identity is a copy); the LIV
+    of the result is row * n + col, resp. col * m + row.  Returns (keys, vals, m, n)."""
+    rows, cols = tuple(int(x) for x in rows), tuple(int(x) for x in cols)
+    if sorted(rows + cols) != list(range(len(dims))):
+        raise ValueError("rows and cols must partition the modes")
+    m = math.prod(int(dims[r]) for r in rows)
+    n = math.prod(int(dims[c]) for c in cols)
+    perm = rows + cols if major == "row" else cols + rows
+    ko, vo, _ = plan(dims, perm).permute(keys, vals, return_perm=False, stream=stream)
+    return ko, vo, m, n
+
+
+def compress(keys, n_major, n_minor, doubly=False, stream=None):
+    """Compress a major-first LCO matrix (lco_compress): CSR/CSC (doubly=False) returns
+    {"ptr": [n_major+1], "minor": [nnz]}; DCSR/DCSC returns {"ids", "ptr", "minor", "nz"}
+    with ids / ptr trimmed to the nz non-empty majors (one count read back)."""
+    if not keys.is_cuda:
+        raise ValueError("keys must be a CUDA tensor (no CPU fallback)")
+    keys = keys.contiguous()
+    dev, nnz = keys.device, keys.numel()
+    minor = torch.empty(nnz, dtype=torch.int64, device=dev)
+    b = ctypes.c_size_t()
+    _check(lib().lco_compress_workspace_size(nnz, 1 if doubly else 0, ctypes.byref(b)))
+    ws, off = _workspace(b.value, dev) if b.value else (None, 0)
+    wptr = None if ws is None else ctypes.c_void_p(ws.data_ptr() + off)
+    wlen = 0 if ws is None else ws.numel() - off
+    if doubly:
+        ids = torch.empty(max(nnz, 1), dtype=torch.int64, device=dev)
+        ptr = torch.empty(nnz + 1, dtype=torch.int64, device=dev)
+        nz = torch.zeros(1, dtype=torch.int64, device=dev)
+    else:
+        ids = nz = None
+        ptr = torch.empty(int(n_major) + 1, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        _check(lib().lco_compress(nnz, _ptr(keys), int(n_major), int(n_minor), 1 if doubly else 0,
+                                  _ptr(ptr), _ptr(ids), _ptr(minor), _ptr(nz), wptr, wlen,
+                                  _stream_ptr(stream, dev)))
+    if not doubly:
+        return {"ptr": ptr, "minor": minor}
+    k = int(nz.item())
+    return {"ids": ids[:k], "ptr": ptr[:k + 1], "minor": minor, "nz": k}
+
+
+def sparsity_class(m, n, nnz, threshold=3.0) -> str:
+    """Hyper-sparsity of an m x n matrix (LibNT's ratio test)."""
+    return SPARSITY[lib().lco_sparsity_class(int(m), int(n), int(nnz), float(threshold))]
+
+
+def mdt_choice(class_a: str, class_b: str) -> str:
+    """The poly-algorithm's MDT / algorithm for A (class_a) times B (class_b), PAPER.md
+    Table "Multiplication possibilities"."""
+    c = lib().lco_mdt_choice(SPARSITY.index(class_a), SPARSITY.index(class_b))
+    return lib().lco_mdt_name(c).decode()

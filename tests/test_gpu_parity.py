@@ -532,3 +532,57 @@ def test_add_eq23_assembly(cuda_device):
     kc, vc, m = lco.add(k.cuda(), v.cuda(), k.cuda(), v.cuda(), (n,) * 4, (1, 0, 3, 2))
     ek, ev = workloads.combinatorial_laplacian(n)
     assert torch.equal(kc.cpu(), ek) and torch.equal(vc.cpu(), ev)
+
+
+# ------------------------------------------------------------------ matrix datatypes
+@pytest.mark.parametrize("m,n,nnz", [(3000, 2000, 200_000), (1 << 30, 64, 300_000),
+                                     (5, 7, 35), (1000, 1000, 1), (100, 100, 0)])
+def test_compress_vs_oracle(m, n, nnz, cuda_device):
+    """CSR and DCSR of row-major LCO matrices (tile boundaries, empty majors, a
+    row-sparse matrix with 2^30 rows in DCSR form) vs the oracle, bit-exact."""
+    rng = np.random.default_rng(m % 97 + nnz)
+    if nnz > m * n // 2:
+        keys = np.sort(rng.choice(m * n, nnz, replace=False)).astype(np.uint64)
+    else:
+        keys = np.unique(rng.integers(0, m * n, nnz + nnz // 10 + 2, dtype=np.int64))[:nnz]
+        keys = keys.astype(np.uint64)
+    k = torch.as_tensor(keys.view(np.int64)).cuda()
+    ids, ptr, minor = oracle.compress(keys, m, n, doubly=True)
+    d = lco.compress(k, m, n, doubly=True)
+    assert d["nz"] == len(ids)
+    assert np.array_equal(_np_u64(d["ids"]), ids) and np.array_equal(_np_u64(d["ptr"]), ptr)
+    assert np.array_equal(_np_u64(d["minor"]), minor)
+    if m <= 1 << 20:
+        ptr1, minor1 = oracle.compress(keys, m, n)
+        s = lco.compress(k, m, n)
+        assert np.array_equal(_np_u64(s["ptr"]), ptr1) and np.array_equal(_np_u64(s["minor"]), minor1)
+
+
+def test_flatten_to_csc_and_roundtrip(cuda_device):
+    """Flatten a 4th-order tensor (rows {2, 0}, cols {3, 1}) column-major on the GPU and
+    compress it to CSC / DCSC: equals scipy's CSC of the same matrix; flattening back
+    (unflatten = the inverse permutation) returns the tensor."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(90)
+    dims = (30, 20, 40, 25)
+    keys, vals = _rand_sorted(rng, dims, 150_000)
+    kt = torch.as_tensor(keys.view(np.int64)).cuda()
+    vt = torch.as_tensor(vals).cuda()
+    rows, cols = (2, 0), (3, 1)
+    km, vm, m, n = lco.flatten(kt, vt, dims, rows, cols, major="col")
+    assert (m, n) == (40 * 30, 25 * 20)
+    c = np.array(np.unravel_index(keys.astype(np.int64), dims))
+    r_idx = c[2] * 30 + c[0]
+    c_idx = c[3] * 20 + c[1]
+    ref = sp.csc_matrix((vals, (r_idx, c_idx)), shape=(m, n))
+    ref.sort_indices()
+    s = lco.compress(km, n, m)
+    assert np.array_equal(_np_u64(s["ptr"]), ref.indptr)
+    assert np.array_equal(_np_u64(s["minor"]), ref.indices)
+    assert np.array_equal(vm.cpu().numpy(), ref.data)
+    d = lco.compress(km, n, m, doubly=True)
+    assert d["nz"] == int((np.diff(ref.indptr) > 0).sum())
+    # unflatten: the column-major matrix is the tensor in mode order (3, 1, 2, 0)
+    inv = tuple(int(x) for x in np.argsort((3, 1, 2, 0)))
+    back, bv, _ = lco.permute(km, vm, (25, 20, 40, 30), inv, return_perm=False)
+    assert torch.equal(back, kt) and torch.equal(bv, vt)

@@ -303,3 +303,53 @@ def test_add_eq23_assembly():
         ek, ev = workloads.combinatorial_laplacian(n)
         assert np.array_equal(kc, ek.numpy().astype(np.uint64))
         assert np.array_equal(vc, ev.numpy())
+
+
+# ------------------------------------------------------------------ matrix datatypes
+def test_compress_matches_scipy():
+    """CSR / DCSR of a row-major LCO matrix vs scipy.sparse (library routine)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(5)
+    for m, n, nnz in ((50, 70, 400), (1000, 30, 200), (7, 9, 0), (1, 1, 1)):
+        keys = np.sort(rng.choice(m * n, nnz, replace=False)).astype(np.uint64)
+        rows, cols = keys // n, keys % n
+        ref = sp.csr_matrix((np.ones(nnz), (rows, cols)), shape=(m, n))
+        ptr, minor = oracle.compress(keys, m, n)
+        assert np.array_equal(ptr, ref.indptr) and np.array_equal(minor, ref.indices)
+        ids, dptr, dminor = oracle.compress(keys, m, n, doubly=True)
+        nonempty = np.flatnonzero(np.diff(ref.indptr))
+        assert np.array_equal(ids, nonempty) and np.array_equal(dminor, ref.indices)
+        assert np.array_equal(dptr, np.append(ref.indptr[nonempty], nnz))
+
+
+def test_compress_fig5a_diagonal():
+    """PAPER.md Fig 5(a): a 10^4 diagonal tensor flattened with rows {i, j}, cols {k, l} is
+    a 100 x 100 matrix with 10 nonzeros on a stride-11 diagonal (index-sparse); its DCSR
+    holds the 10 present rows only."""
+    keys = np.array([i * 1111 for i in range(10)], dtype=np.uint64)  # (i, i, i, i)
+    ids, ptr, minor = oracle.compress(keys, 100, 100, doubly=True)
+    assert list(ids) == [11 * i for i in range(10)] and list(minor) == [11 * i for i in range(10)]
+    assert list(ptr) == list(range(11))
+    ptr1, _ = oracle.compress(keys, 100, 100)
+    assert len(ptr1) == 101 and ptr1[-1] == 10
+
+
+def test_sparsity_classes_and_mdt_table():
+    """SPEC classify examples and the paper's multiplication table (PAPER.md :340-352,
+    transcribed here cell by cell) through the library's host functions."""
+    import paper_1802_02619_b200 as lco
+    assert lco.sparsity_class(100, 100, 10) == "index-sparse"
+    assert lco.sparsity_class(10 ** 4, 10, 10 ** 3) == "row-sparse"
+    assert lco.sparsity_class(100, 100, 5000) == "sparse"
+    assert lco.sparsity_class(10, 10 ** 4, 10 ** 3) == "column-sparse"
+    assert lco.sparsity_class(5, 5, 0) == "sparse"
+    paper = {  # A \\ B: sparse, row-sparse, column-sparse, index-sparse
+        "sparse": ["CSC/CSR", "CSC", "CSC", "CSC"],
+        "column-sparse": ["CSR", "DCSC/DCSR", "DCSC", "DCSC"],
+        "row-sparse": ["CSR", "DCSR", "CSCNA/CSRNA", "CSCNA"],
+        "index-sparse": ["CSR", "DCSR", "CSRNA", "SOP"],
+    }
+    cols = ["sparse", "row-sparse", "column-sparse", "index-sparse"]
+    for a, row in paper.items():
+        for b, want in zip(cols, row):
+            assert lco.mdt_choice(a, b) == want, (a, b)
