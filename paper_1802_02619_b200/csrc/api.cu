@@ -126,15 +126,15 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     m.cta = (nnz >> (m.b1 + m.b2)) > wt;
     mcost = 8 + 36 + 8 + 40 + 40;
   }
-  if (getenv("LCO_MSD_B1")) m.b1 = atoi(getenv("LCO_MSD_B1"));  // experiment hooks
+  // schedule overrides for tests and A/B measurements (the defaults above otherwise)
+  if (getenv("LCO_MSD_B1")) m.b1 = atoi(getenv("LCO_MSD_B1"));
   if (getenv("LCO_MSD_B2") && m.levels == 2) m.b2 = atoi(getenv("LCO_MSD_B2"));
   if (getenv("LCO_MSD_CTA")) m.cta = atoi(getenv("LCO_MSD_CTA"));
   m.rb = B - m.b1 - m.b2;
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
   // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
   // and with a clear modelled win.
-  const bool seg_ok = op.segments == 1 || getenv("LCO_MSD_SEG");
-  if (seg_ok && mcost < 0.75 * c.cost) {
+  if (op.segments == 1 && mcost < 0.75 * c.cost) {
     c.path = kPathMsd;
     c.msd = m;
     c.cost = mcost;

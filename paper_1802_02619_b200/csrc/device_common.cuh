@@ -129,7 +129,6 @@ struct PassParams {
   int world;
   const TileEntry* ttab;      // segmented mode: tile table (else tiles are t * kTile)
   const uint32_t* ntiles;     // segmented mode: number of valid table entries
-  int ablate;                 // experiment hook (0 in production)
   uint32_t pf_dist;           // L2 prefetch distance in tiles (resident CTAs), 0 = off
 };
 

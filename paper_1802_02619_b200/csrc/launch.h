@@ -62,6 +62,7 @@ struct PassParams;
 struct ScatterIO;
 
 uint64_t pass_tiles(uint64_t nnz);
+uint32_t prefetch_distance();  // L2 prefetch distance of the pass kernels (tiles)
 int pass_tile();
 int pass_rb(int bits);
 size_t pass_ctrl_bytes(int rb, uint64_t nnz);

@@ -23,7 +23,6 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <vector>
 
 #include "device_common.cuh"
 #include "launch.h"
@@ -953,11 +952,9 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
       s_min = ~0ull;
       s_max = 0ull;
       s_big = 0;
-      if (L.a.ablate != 5) {
-        prefetch_l2(sk + start, (size_t)n * 8);  // the write phase gathers from L2
-        if (VALS) prefetch_l2(sv + start, (size_t)n * 8);
-        if (want_pos) prefetch_l2(sp + start, (size_t)n * 4);
-      }
+      prefetch_l2(sk + start, (size_t)n * 8);  // the write phase gathers from L2
+      if (VALS) prefetch_l2(sv + start, (size_t)n * 8);
+      if (want_pos) prefetch_l2(sp + start, (size_t)n * 4);
     }
     uint64_t lk[kRItems];
     uint64_t mn = ~0ull, mx = 0ull;
@@ -1336,10 +1333,7 @@ static cudaError_t launch_leafr_t(const LeafArgs& L, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   k_leafr<VALS><<<sms * per_sm, kCThreads, kRSmem, s>>>(L);
-  const cudaError_t e = cudaGetLastError();
-  if (getenv("LCO_DEBUG"))
-    fprintf(stderr, "k_leafr grid %d smem %zu: %s\n", sms * per_sm, kRSmem, cudaGetErrorString(e));
-  return e;
+  return cudaGetLastError();
 }
 
 template <bool VALS>
@@ -1365,9 +1359,6 @@ static cudaError_t launch_leafs_t(const LeafArgs& L, cudaStream_t s) {
 // SM; the single-leaf call: 64-bit keys and the in-smem radix fallback.
 static cudaError_t launch_leafc(const LeafArgs& L, bool vals, bool single, uint32_t grid_cap,
                                 cudaStream_t s) {
-  if (getenv("LCO_DEBUG"))
-    fprintf(stderr, "launch_leafc: single %d rb %d level %d vals %d\n", (int)single, L.rb,
-            L.only_level, (int)vals);
   if (!single && L.rb <= 32 && getenv("LCO_LEAFS"))
     return vals ? launch_leafs_t<true>(L, s) : launch_leafs_t<false>(L, s);
   if (!single && L.rb <= 32 && !getenv("LCO_NO_LEAFR"))
@@ -1473,16 +1464,6 @@ cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int
   e = vals ? launch_leafc_t<true, true, kTileCap>(L, 1u << 30, Lc.stream)
            : launch_leafc_t<false, true, kTileCap>(L, 1u << 30, Lc.stream);
   if (e != cudaSuccess) return e;
-  if (getenv("LCO_DEBUG")) {  // debug: deferred tiles and the largest tile
-    uint32_t nd = 0;
-    cudaMemcpyAsync(&nd, ndefer, 4, cudaMemcpyDeviceToHost, Lc.stream);
-    std::vector<uint32_t> ts(nt + 1);
-    cudaMemcpyAsync(ts.data(), tstart, (nt + 1) * 4, cudaMemcpyDeviceToHost, Lc.stream);
-    cudaStreamSynchronize(Lc.stream);
-    uint32_t mx = 0;
-    for (uint32_t c = 0; c < nt; ++c) mx = ts[c + 1] - ts[c] > mx ? ts[c + 1] - ts[c] : mx;
-    fprintf(stderr, "run_tiles: T %u tiles %u deferred %u largest %u\n", T, nt, nd, mx);
-  }
   if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf_deferred");
   LeafArgs LD = L;
   LD.dlist = defer;
@@ -1589,8 +1570,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   a.kp = kp;
   a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
   a.nnz = nnz;
-  a.ablate = getenv("LCO_ABLATE") ? atoi(getenv("LCO_ABLATE")) : 0;
-  a.pf_dist = getenv("LCO_PF") ? (uint32_t)atoi(getenv("LCO_PF")) : 0;
+  a.pf_dist = prefetch_distance();
   LeafArgs L;
   memset(&L, 0, sizeof L);
   L.a = a;
