@@ -46,6 +46,11 @@ KERNEL_BYTES = {
     "k_scatter_last": 40,
     "k_leafw": 40,            # read K', V, position; write K', V, perm (final)
     "k_leafw_l1": 40,
+    "k_leafr": 40,            # CTA leaves, 32-bit sort keys (read K', V, pos; write)
+    "k_leafs": 40,            # CTA leaves, fully staged
+    "k_leafc": 40,            # CTA leaves, 64-bit sort keys
+    "k_leaf_l1": 40,
+    "k_leafc_tiles": 36,      # segment-local tiles: read K, V; write K', V, perm
     "k_leaf": 36,
     "k_leaf_deferred": 40,
     "k_copy": 36,             # read K, V; write K, V, perm

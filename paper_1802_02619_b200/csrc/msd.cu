@@ -1355,6 +1355,13 @@ static cudaError_t launch_leafs_t(const LeafArgs& L, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// The CTA-leaf kernel launch_leafc picks (also the measurement marker's name).
+static const char* leafc_kernel(const LeafArgs& L, bool single) {
+  if (!single && L.rb <= 32 && getenv("LCO_LEAFS")) return "k_leafs";
+  if (!single && L.rb <= 32 && !getenv("LCO_NO_LEAFR")) return "k_leafr";
+  return "k_leafc";
+}
+
 // Leaf levels (defer list present): 32-bit keys when the leaf bits allow, two CTAs per
 // SM; the single-leaf call: 64-bit keys and the in-smem radix fallback.
 static cudaError_t launch_leafc(const LeafArgs& L, bool vals, bool single, uint32_t grid_cap,
@@ -1667,7 +1674,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     L2.only_level = 2;
     L2.rb = mp.rb;
     if (mp.cta) {
-      if (Lc.mark) Lc.mark(Lc.ctx, "k_leafc");
+      if (Lc.mark) Lc.mark(Lc.ctx, leafc_kernel(L2, false));
       e = launch_leafc(L2, vals, false, 1u << 30, Lc.stream);
     } else {
       if (Lc.mark) Lc.mark(Lc.ctx, "k_leafw");
@@ -1680,7 +1687,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   L1.only_level = 1;
   L1.rb = mp.rb + (mp.levels == 2 ? mp.b2 : 0);
   if (mp.cta) {
-    if (Lc.mark) Lc.mark(Lc.ctx, mp.levels == 2 ? "k_leafc_l1" : "k_leafc");
+    if (Lc.mark) Lc.mark(Lc.ctx, mp.levels == 2 ? "k_leaf_l1" : leafc_kernel(L1, false));
     e = launch_leafc(L1, vals, false, 1u << 30, Lc.stream);
   } else {
     if (Lc.mark) Lc.mark(Lc.ctx, mp.levels == 2 ? "k_leafw_l1" : "k_leafw");
