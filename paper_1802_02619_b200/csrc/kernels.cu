@@ -285,16 +285,25 @@ __global__ void __launch_bounds__(NT, 2)
   uint64_t base;
   uint32_t n, seg;
   if (!tile_range(a, t, &base, &n, &seg)) return;
-  if (tid == 0 && a.pf_dist && !a.ttab) {
+  if (tid == 0 && a.pf_dist) {
     // the tile the CTA launched pf_dist later will load: bring it into L2 now, so its
     // loads see L2 latency while HBM streams in the background
-    const uint64_t b2 = (uint64_t)(t + a.pf_dist) * kTile;
-    if (b2 < a.nnz) {
-      const size_t m = (size_t)umin64(kTile, a.nnz - b2);
-      prefetch_l2((FIRST ? io.keys_in : io.kin) + b2, m * 8);
-      if (VALS) prefetch_l2((FIRST ? io.vals_in : io.vin) + b2, m * 8);
-      if (!FIRST && io.pout) prefetch_l2(io.pin + b2, m * 4);
-      prefetch_l2(io.toff + (size_t)(t + a.pf_dist) * BINS, (size_t)BINS * 4);
+    const uint32_t t2 = t + a.pf_dist;
+    uint64_t b2 = 0;
+    uint32_t m = 0;
+    if (!a.ttab) {
+      b2 = (uint64_t)t2 * kTile;
+      m = b2 < a.nnz ? (uint32_t)umin64(kTile, a.nnz - b2) : 0u;
+    } else if (t2 < *a.ntiles) {
+      const TileEntry e2 = a.ttab[t2];
+      b2 = e2.start;
+      m = e2.n;
+    }
+    if (m) {
+      prefetch_l2((FIRST ? io.keys_in : io.kin) + b2, (size_t)m * 8);
+      if (VALS) prefetch_l2((FIRST ? io.vals_in : io.vin) + b2, (size_t)m * 8);
+      if (!FIRST && io.pout) prefetch_l2(io.pin + b2, (size_t)m * 4);
+      prefetch_l2(io.toff + (size_t)t2 * BINS, (size_t)BINS * 4);
     }
   }
   for (int i = tid; i < W * BINS / 2; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
