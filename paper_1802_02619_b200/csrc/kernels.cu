@@ -356,13 +356,20 @@ __global__ void __launch_bounds__(NT, 2)
   for (int it = 0; it < IT; ++it) {
     const uint32_t d = meta[it];
     const bool ok = d != kInvalid;
-    // lanes holding the same digit: one ballot per digit bit (ALU pipe; match.any goes
-    // through the MIO queue and its latency dominated the ranking loop, ncu)
-    uint32_t peers = __ballot_sync(0xffffffffu, ok);
+    // lanes holding the same digit: for <= 10-bit digits one ballot per digit bit (ALU
+    // pipe; match.any goes through the MIO queue and its latency dominated the 8-bit
+    // ranking loop, ncu: +25 % on C5); for 11-bit digits match.any (12 ballots cost
+    // more: -6 % on C4)
+    uint32_t peers;
+    if (RB >= 11) {
+      peers = __match_any_sync(0xffffffffu, d) & (ok ? 0xffffffffu : 0u);
+    } else {
+      peers = __ballot_sync(0xffffffffu, ok);
 #pragma unroll
-    for (int b = 0; b < RB; ++b) {
-      const uint32_t bit = (d >> b) & 1u;
-      peers &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
+      for (int b = 0; b < RB; ++b) {
+        const uint32_t bit = (d >> b) & 1u;
+        peers &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
+      }
     }
     const uint32_t below = __popc(peers & ltm);
     const uint32_t before = ok ? (uint32_t)wh[d] : 0u;  // every peer reads the same counter
