@@ -178,7 +178,7 @@ typedef struct lco_plan_info {
   int path;                            /* 0 copy, 1 LSD passes, 2 one on-chip leaf,
                                           3 MSD passes + on-chip leaf sorts, 4 segment-
                                           local tiles, 5 segmented single pass,
-                                          6 hierarchical stages */
+                                          6 hierarchical stages, 7 block transpose */
   int launches;                        /* kernels this library launches per call */
   int tile;                            /* nonzeros per tile (CTA) */
   int msd_levels;                      /* path 3: MSD passes before the leaves */

@@ -43,6 +43,8 @@ struct CallPlan {
   KeyPlan kp;
   double cost;  // modelled bytes per nonzero
   uint64_t segdiv, segments;  // tile path: identity-prefix segments
+  uint64_t nblocks, bfree;    // block path
+  KeyPlan kb;
 };
 
 CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
@@ -79,6 +81,22 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   c.passes = op.passes;
   c.rb = op.radix_bits;
   c.cost = 4 + 48.0 * op.passes;
+  // All rearranged modes in a small old-order prefix: a transpose of runs, no sorting
+  // (block.cu): one read of the keys for the run bounds, O(blocks) tables, one scatter.
+  // Opt-in (LCO_BLOCK=1): measured on C4 1.18 ms vs 0.97 ms for the LSD pass (its
+  // scatter is latency-bound on the key -> delta -> store chain).
+  if (op.nblocks && op.nblocks * 4 <= nnz && op.nblocks < (1ull << 31) && getenv("LCO_BLOCK")) {
+    const double bcost = 8 + 36 + 16.0 * (double)op.nblocks / (double)nnz;
+    if (bcost < c.cost) {
+      c.path = kPathBlock;
+      c.nblocks = op.nblocks;
+      c.bfree = op.bfree;
+      c.kb = op.kb;
+      c.passes = 0;
+      c.cost = bcost;
+      return c;
+    }
+  }
   // Identity prefix with large segments and a power-of-two middle of <= 11 bits: one
   // stable pass of the middle digit inside every segment (segment starts from a count of
   // the prefix digit), straight from the input to the outputs.
@@ -158,12 +176,13 @@ WsLayout layout_for(const CallPlan& c, uint64_t nnz) {
   memset(&w, 0, sizeof w);
   size_t off = 0;
   const bool lsd = c.path == kPathOnesweep, msd = c.path == kPathMsd, tile = c.path == kPathTile;
-  const bool seg = c.path == kPathSeg;
-  if ((lsd || msd || tile || seg) && nnz > 0) {
+  const bool seg = c.path == kPathSeg, blk = c.path == kPathBlock;
+  if ((lsd || msd || tile || seg || blk) && nnz > 0) {
     w.ctrl = off;
     off += align_up(lsd ? pass_ctrl_bytes(c.rb, nnz)
                         : ((msd || seg) ? msd_ctrl_bytes(c.msd.b1, c.msd.b2, nnz)
-                                        : tile_ctrl_bytes(nnz, c.segments)));
+                                        : (blk ? block_ctrl_bytes(c.nblocks)
+                                               : tile_ctrl_bytes(nnz, c.segments))));
     // the tile path needs both buffers only as scratch of the rare streaming fallback
     if (msd || tile || c.passes >= 2) {
       w.kA = off;
@@ -282,6 +301,7 @@ cudaError_t execute(lco_plan_s* h, const OpPlan& op, uint64_t nnz, const uint64_
   if (cp.path == kPathOnesweep) return run_passes(cp.rb, cp.kp, io, L);
   if (cp.path == kPathTile) return run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
   if (cp.path == kPathSeg) return run_seg(cp.msd.b1, cp.msd.b2, cp.kp, io, L);
+  if (cp.path == kPathBlock) return run_block(cp.kp, cp.kb, cp.nblocks, cp.bfree, io, L);
   return run_msd(cp.msd, cp.kp, io, L);
 }
 
@@ -838,6 +858,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
       const CallPlan sc = choose_plan(h->stages[j].op, nnz);
       launches_h += sc.path == kPathCopy || sc.path == kPathLocal ? 1
                     : sc.path == kPathTile ? 3
+                    : sc.path == kPathBlock ? 7
                     : sc.path == kPathSeg ? 6
                     : sc.path == kPathOnesweep ? 4 * sc.passes
                     : 4 + (sc.msd.levels == 2 ? 5 : 0) + 2;
@@ -851,6 +872,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
     if (cp.path == kPathCopy || cp.path == kPathLocal) launches = 1;
     else if (cp.path == kPathTile) launches = 3;  // bounds, tile sorts, deferred tiles
     else if (cp.path == kPathSeg) launches = 6;   // count, scan, tiles, count, offsets, scatter
+    else if (cp.path == kPathBlock) launches = 7; // bounds, counts, 3 scan, delta, scatter
     else if (cp.path == kPathOnesweep) launches = 4 * cp.passes;
     else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 2;  // passes, leaves, deferred
   }

@@ -198,7 +198,7 @@ LCO_HD uint32_t digit_of(const KeyPlan& p, uint64_t q, int pass) {
 }
 
 enum Path { kPathCopy = 0, kPathOnesweep = 1, kPathLocal = 2, kPathMsd = 3, kPathTile = 4,
-            kPathSeg = 5 };
+            kPathSeg = 5, kPathBlock = 7 };
 
 // Host plan for one operation (permute or sort) of a handle.
 struct OpPlan {
@@ -209,6 +209,10 @@ struct OpPlan {
   int tile;         // nonzeros per tile
   KeyPlan kp;
   uint64_t trailing, middle, segments, segdiv;
+  // block-transpose schedule: old modes 0..k (k = last old position of a prefix / middle
+  // mode) form the block id K div bfree; kb maps a block id to its new-order id
+  uint64_t nblocks, bfree;
+  KeyPlan kb;
 };
 
 // One stage of a hierarchical plan: the flat plan of a relative permutation.

@@ -244,6 +244,22 @@ static void flat_permute(const FlatInfo& fi, OpPlan* op) {
     op->path = kPathOnesweep;
     choose_passes(op, ceil_log2(G * S));
   }
+  // block-transpose schedule (block.cu): blocks = old modes 0..k
+  op->nblocks = 0;
+  if (n >= 2 && b > 0) {
+    int k = 0;
+    for (int t = 0; t < b; ++t) k = np[t] > k ? np[t] : k;
+    uint64_t nb = 1, F = 1;
+    for (int m = 0; m <= k; ++m) nb *= nd[m];
+    for (int m = k + 1; m < n; ++m) F *= nd[m];
+    int32_t bp[LCO_MAX_ORDER];
+    int j = 0;
+    for (int t = 0; t < n; ++t)
+      if (np[t] <= k) bp[j++] = np[t];
+    op->nblocks = nb;
+    op->bfree = F;
+    op->kb = make_keyplan(k + 1, nd, bp, 1);
+  }
 }
 
 // Hierarchical plan ("the rearrangement procedure is recursively applied

@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "liblco.so")
 FLAG_VALIDATE = 1
 FLAG_HIERARCHICAL = 2
 MAX_ORDER = 16
-PATHS = {0: "copy", 1: "lsd", 2: "leaf", 3: "msd", 4: "tile", 5: "seg", 6: "hier"}
+PATHS = {0: "copy", 1: "lsd", 2: "leaf", 3: "msd", 4: "tile", 5: "seg", 6: "hier", 7: "block"}
 
 _STATUS = {
     0: "LCO_OK", 1: "LCO_ERR_NULL", 2: "LCO_ERR_ORDER", 3: "LCO_ERR_DIM", 4: "LCO_ERR_PERM",

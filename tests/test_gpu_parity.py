@@ -586,3 +586,26 @@ def test_flatten_to_csc_and_roundtrip(cuda_device):
     inv = tuple(int(x) for x in np.argsort((3, 1, 2, 0)))
     back, bv, _ = lco.permute(km, vm, (25, 20, 40, 30), inv, return_perm=False)
     assert torch.equal(back, kt) and torch.equal(bv, vt)
+
+
+# ------------------------------------------------------------------ block transpose
+@pytest.mark.parametrize("dims,perm", [((37, 41, 1000), (1, 0, 2)),
+                                       ((64, 32, 16, 300), (2, 0, 1, 3)),
+                                       ((50, 60, 7, 90), (1, 0, 2, 3)),
+                                       ((16, 8, 12, 10, 200), (1, 2, 0, 3, 4))])
+def test_block_path(dims, perm, cuda_device, monkeypatch):
+    """Permutations whose rearranged modes lie in a small old-order prefix: a transpose of
+    runs without sorting (run bounds, block counts in new order, scan, one scatter) - non-
+    power-of-two dims, empty blocks, runs spanning thread boundaries (opt-in schedule)."""
+    monkeypatch.setenv("LCO_BLOCK", "1")
+    rng = np.random.default_rng(sum(dims))
+    keys, vals = _rand_sorted(rng, dims, 250_000)
+    info = lco.plan(dims, perm).info(len(keys))
+    assert info["path"] == "block", info["path"]
+    check(dims, perm, keys, vals)
+    check(dims, perm, keys, None, return_perm=False)
+    idx = rng.permutation(len(keys)).astype(np.uint32)
+    check(dims, perm, keys, vals, idx=idx)
+    w = workloads.config("C4", scale=300)
+    assert lco.plan(w.dims, w.perms[0]).info(w.keys.numel())["path"] == "block"
+    check(w.dims, w.perms[0], _np_u64(w.keys), w.vals.numpy())

@@ -111,7 +111,7 @@ def test_baseline_config_plans():
     for (name, dims, perm, nnz), (bits, path) in cases.items():
         info = lco.Plan(dims, perm).info(nnz)
         assert (info["sort_bits"], info["path"]) == (bits, path), (name, info)
-        if path not in ("tile", "hier"):  # tiles sort on K' on chip; hier: per stage
+        if path not in ("tile", "hier", "block"):  # no radix digits on these paths
             assert sum(info["digit_bits"]) + info["leaf_bits"] == bits
     # C3b: interior resting modes -> two stages: the c3 digit inside
     # the 128 c0 segments (one segmented pass), then c4 inside (c0, c3, c1) regions
