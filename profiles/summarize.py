@@ -15,7 +15,8 @@ import subprocess
 import sys
 
 OURS = ("k_count", "k_scan", "k_offsets", "k_scatter", "k_msd_tiles", "k_offsets_seg",
-        "k_leaf", "k_copy", "k_keyhist", "k_validate", "k_tile_bounds")
+        "k_leaf", "k_copy", "k_keyhist", "k_validate", "k_tile_bounds", "k_block", "k_merge",
+        "k_compress")
 
 
 def short(name):
@@ -59,6 +60,30 @@ def launches(path, out, traffic_key=None):
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     return {k: (a[2] + a[3]) / a[0] for k, a in agg.items()}
+
+
+def marker_traffic(path, markers):
+    """DRAM bytes (read + write) per launch of each bench marker: the launch list's kernels
+    of this library, in launch order, zipped cyclically with the marker names of one call
+    (bench.py kernels_ms keys; one launch per marker), averaged over the calls."""
+    rows = list(csv.reader(l for l in open(path) if not l.startswith("==")))
+    hdr = rows[0]
+    ki, mi, vi = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value"))
+    idi = hdr.index("ID")
+    per = collections.OrderedDict()
+    for r in rows[1:]:
+        if len(r) != len(hdr):
+            continue
+        k = short(r[ki])
+        if not any(k.startswith(o) for o in OURS) and not k.startswith("k_"):
+            continue
+        per.setdefault(r[idi], {"name": k})[r[mi]] = float(r[vi].replace(",", ""))
+    launches = list(per.values())
+    out = collections.defaultdict(list)
+    for j, l in enumerate(launches):
+        out[markers[j % len(markers)]].append(l.get("dram__bytes_read.sum", 0.0)
+                                              + l.get("dram__bytes_write.sum", 0.0))
+    return {m: sum(v) / len(v) for m, v in out.items()}
 
 
 WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",

@@ -16,7 +16,15 @@ echo "launches rc=$?"
 ncu --set full --clock-control none --import-source on -k regex:"k_leaf|k_scatter" -s 4 -c 3 \
     -o gpurun_out/m_c5_full -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_c5.log 2>&1
 echo "c5 full rc=$?"
-python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain4.log 2>&1 && \
+python bench.py --config C4 --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain4.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file gpurun_out/m_c4_launches.csv python bench.py --config C4 --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_launch4.log 2>&1
+echo "c4 launches rc=$?"
+python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain4b.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_count" -s 2 -c 2 \
     -o gpurun_out/m_c4_full -f python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_c4.log 2>&1
 echo "c4 full rc=$?"
+python benchmarks/table2.py --reps 5 --out gpurun_out/m_table2.md > gpurun_out/m_table2.log 2>&1; echo "table2 rc=$?"
+python benchmarks/addition.py --out gpurun_out/m_addition.json > gpurun_out/m_addition.log 2>&1; echo "addition rc=$?"
+python benchmarks/addition.py --hierarchical --n 2896 --out gpurun_out/m_addition_hier.json > gpurun_out/m_addition_hier.log 2>&1; echo "addition hier rc=$?"
+python benchmarks/mdt.py --out gpurun_out/m_mdt.json > gpurun_out/m_mdt.log 2>&1; echo "mdt rc=$?"

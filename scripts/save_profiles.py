@@ -21,7 +21,21 @@ if os.path.exists(os.path.join(G, "m_c5_launches.csv")):
     shutil.copy(os.path.join(G, "m_c5_launches.csv"), os.path.join(P, f"{tag}_c5_launches.csv"))
     subprocess.check_call([sys.executable, summ, "launches", os.path.join(G, "m_c5_launches.csv"),
                            os.path.join(P, f"{tag}_c5_launches.md")])
+sys.path.insert(0, P)
+import summarize  # noqa: E402
+
 traffic = {}
+# per bench marker (what bench.py's roofline.traffic looks up), from the launch lists
+for c in ("C5", "C4"):
+    lpath = os.path.join(G, f"m_{c.lower()}_launches.csv")
+    bpath = os.path.join(G, f"m_bench_{c}.json")
+    if os.path.exists(lpath) and os.path.exists(bpath):
+        markers = [m for m in json.load(open(bpath))["kernels_ms"]]
+        traffic.setdefault(c, {}).update(summarize.marker_traffic(lpath, markers))
+        if c == "C4":
+            shutil.copy(lpath, os.path.join(P, f"{tag}_c4_launches.csv"))
+            subprocess.check_call([sys.executable, summ, "launches", lpath,
+                                   os.path.join(P, f"{tag}_c4_launches.md")])
 for c, rep in (("C5", "m_c5_full.ncu-rep"), ("C4", "m_c4_full.ncu-rep")):
     path = os.path.join(G, rep)
     if not os.path.exists(path):
@@ -41,9 +55,14 @@ for c, rep in (("C5", "m_c5_full.ncu-rep"), ("C4", "m_c4_full.ncu-rep")):
         name = row[ki].split("(")[0].replace("void ", "").replace("lco::", "")
         b = float(row[r]) * scale.get(units[r], 1) + float(row[w]) * scale.get(units[w], 1)
         per.setdefault(name, []).append(b)
-    traffic[c] = {k: sum(v) / len(v) for k, v in per.items()}
+    traffic.setdefault(c, {}).update({k: sum(v) / len(v) for k, v in per.items()})
 tp = os.path.join(P, "traffic.json")
 old = json.load(open(tp)) if os.path.exists(tp) else {}
 old.update(traffic)
 json.dump(old, open(tp, "w"), indent=1)
+for src, dst in (("m_table2.md", "table2.md"), ("m_table2.json", "table2.json"),
+                 ("m_addition.json", "addition.json"), ("m_addition_hier.json", "addition_hier.json"),
+                 ("m_mdt.json", "mdt.json")):
+    if os.path.exists(os.path.join(G, src)):
+        shutil.copy(os.path.join(G, src), os.path.join(P, f"{tag}_{dst}"))
 print("saved", tag, sorted(traffic))
