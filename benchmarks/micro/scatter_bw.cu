@@ -53,12 +53,14 @@ __global__ void __launch_bounds__(256) k_direct(uint64_t N, int B, const uint64_
 // Reads are coalesced tile loads (kept alive through a checksum); writes go to the
 // bucketed destinations in output-slot order (runs of TILE/B records), no shared
 // memory, so only the HBM write pattern differs from a copy.
-__global__ void __launch_bounds__(256, 2) k_pattern(uint64_t N, int B, const uint64_t* __restrict__ k,
+template <bool P3>
+__global__ void __launch_bounds__(256, 2) k_pattern(uint64_t N, int per, const uint64_t* __restrict__ k,
                                                     const double* __restrict__ v, uint64_t* __restrict__ ko,
-                                                    double* __restrict__ vo, uint64_t pad) {
+                                                    double* __restrict__ vo, uint32_t* __restrict__ po,
+                                                    uint64_t nb) {
+  // runs of `per` records per bucket per tile, nb buckets, bucket regions N/nb apart
   const uint64_t tile = blockIdx.x;
   const uint64_t base = tile * TILE;
-  const int per = TILE / B;
   uint64_t acc = 0;
   double vacc = 0;
 #pragma unroll
@@ -66,11 +68,14 @@ __global__ void __launch_bounds__(256, 2) k_pattern(uint64_t N, int B, const uin
     acc += __ldcs(k + base + r * 256 + threadIdx.x);
     vacc += __ldcs(v + base + r * 256 + threadIdx.x);
   }
+  const uint64_t stride = N / nb;
 #pragma unroll 4
   for (int p = threadIdx.x; p < TILE; p += 256) {
-    const uint64_t d = (uint64_t)(p / per) * (N / B + pad) + tile * per + p % per;
+    const uint64_t bk = (uint64_t)(p / per) % nb;
+    const uint64_t d = bk * stride + (tile * per + p % per) % stride;
     ko[d] = acc + p;
     vo[d] = vacc + p;
+    if (P3) po[d] = (uint32_t)(acc + p);
   }
 }
 
@@ -98,15 +103,16 @@ int main() {
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= R;
-    printf("%-10s B=%6d  %8.3f ms  %7.1f GB/s  err=%s\n", name, B, ms, 32.0 * N / ms / 1e6,
+    printf("%-10s run=%4d  %8.3f ms  %7.1f GB/s(r16+w16)  err=%s\n", name, B, ms, 32.0 * N / ms / 1e6,
            cudaGetErrorString(cudaGetLastError()));
   };
   time("copy", 0, [&] { k_copy<<<148 * 8, 512>>>(N, k, v, ko, vo); });
-  for (uint64_t pad : {0ull, 40ull}) {
-    printf("pad %llu records between buckets\n", (unsigned long long)pad);
-    for (int B : {1, 4, 16, 64, 256, 1024, 2048, 4096}) {
-      time("pattern", B, [&] { k_pattern<<<N / TILE, 256>>>(N, B, k, v, ko, vo, pad); });
-    }
+  uint32_t* po;
+  cudaMalloc(&po, N * 4 + (64ull << 20));
+  for (int per : {64, 16, 13, 8, 4}) {
+    const uint64_t nb = TILE / per;
+    time(per == 13 ? "2arr r13" : "2arr", per, [&] { k_pattern<false><<<N / TILE, 256>>>(N, per, k, v, ko, vo, po, nb); });
+    time(per == 13 ? "3arr r13" : "3arr", per, [&] { k_pattern<true><<<N / TILE, 256>>>(N, per, k, v, ko, vo, po, nb); });
   }
   return 0;
 }

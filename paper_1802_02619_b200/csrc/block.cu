@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "device_common.cuh"
@@ -133,7 +134,11 @@ __global__ void __launch_bounds__(256) k_block_scatter(uint64_t nnz, const __gri
                                                        uint64_t* __restrict__ keys_out,
                                                        double* __restrict__ vals_out,
                                                        uint32_t* __restrict__ perm_out) {
-  const uint64_t base = (uint64_t)blockIdx.x * 256 * kBkU + threadIdx.x;
+  // grid-stride over chunks in launch order with a small grid: the concurrently written
+  // output window (one run per block per active chunk) stays small enough for L2 to
+  // complete the partial lines before they are evicted
+  for (uint64_t base = (uint64_t)blockIdx.x * 256 * kBkU + threadIdx.x; base < nnz;
+       base += (uint64_t)gridDim.x * 256 * kBkU) {
   uint64_t k[kBkU];
   double v[kBkU];
   uint32_t o[kBkU];
@@ -157,6 +162,7 @@ __global__ void __launch_bounds__(256) k_block_scatter(uint64_t nnz, const __gri
       if (VALS) vals_out[o[u]] = v[u];
       if (perm_out) perm_out[o[u]] = idx_in ? __ldg(idx_in + i) : (uint32_t)i;
     }
+  }
   }
 }
 
@@ -199,11 +205,12 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   k_block_delta<<<gb, 256, 0, L.stream>>>(nblocks, kb, bstart, cnew, bend);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.mark) L.mark(L.ctx, "k_block_scatter");
+  static const unsigned gsc = getenv("LCO_BLK_GRID") ? (unsigned)atoi(getenv("LCO_BLK_GRID")) : 148 * 4;
   if (io.vals_out)
-    k_block_scatter<true><<<gn, 256, 0, L.stream>>>(nnz, kp, fF, io.keys_in, io.vals_in, io.idx_in,
+    k_block_scatter<true><<<gsc, 256, 0, L.stream>>>(nnz, kp, fF, io.keys_in, io.vals_in, io.idx_in,
                                                    bend, io.keys_out, io.vals_out, io.perm_out);
   else
-    k_block_scatter<false><<<gn, 256, 0, L.stream>>>(nnz, kp, fF, io.keys_in, io.vals_in, io.idx_in,
+    k_block_scatter<false><<<gsc, 256, 0, L.stream>>>(nnz, kp, fF, io.keys_in, io.vals_in, io.idx_in,
                                                     bend, io.keys_out, io.vals_out, io.perm_out);
   return cudaGetLastError();
 }
