@@ -205,7 +205,7 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   k_block_delta<<<gb, 256, 0, L.stream>>>(nblocks, kb, bstart, cnew, bend);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.mark) L.mark(L.ctx, "k_block_scatter");
-  static const unsigned gsc = getenv("LCO_BLK_GRID") ? (unsigned)atoi(getenv("LCO_BLK_GRID")) : 148 * 4;
+  const unsigned gsc = (unsigned)umin64(gn, 148 * 32);
   if (io.vals_out)
     k_block_scatter<true><<<gsc, 256, 0, L.stream>>>(nnz, kp, fF, io.keys_in, io.vals_in, io.idx_in,
                                                    bend, io.keys_out, io.vals_out, io.perm_out);
