@@ -124,26 +124,33 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   // per digit, which the HBM write path sustains; 10-11-bit digits write runs of 2-4 and
   // ran at half the bandwidth, benchmarks/micro/scatter_bw.cu), then one on-chip sort per
   // leaf: by a warp when the expected leaf is <= leaf_target(), else by a CTA (<= 8K).
+  // Two-level plans size the second digit for the fully staged CTA leaves (k_leafs,
+  // ~1.9K nonzeros, three CTAs per SM): measured on C5 8+10 bits + k_leafs 22.5 ms vs
+  // 8+8 + k_leafr (7.6K-nonzero leaves, L2 gathers) 23.3 ms.
   MsdPlan m;
   memset(&m, 0, sizeof m);
   const uint64_t wt = leaf_target();
   const uint64_t ct = cta_leaf_cap() * 15 / 16;  // expected size, ~4 sigma below the cap
+  const uint64_t st = staged_leaf_target();
   double mcost;
   if ((nnz >> 8) <= ct) {
     m.levels = 1;
     m.b1 = B < 8 ? B : 8;
     m.b2 = 0;
     m.cta = (nnz >> m.b1) > wt;
+    m.staged = m.cta && (nnz >> m.b1) <= st;
     mcost = 8 + 36 + 40;
   } else {
     m.levels = 2;
     m.b1 = 8;
     m.b2 = 8;
-    while (m.b2 < 11 && (nnz >> (m.b1 + m.b2)) > ct) ++m.b2;
+    while (m.b2 < 11 && (nnz >> (m.b1 + m.b2)) > st) ++m.b2;
     if (m.b1 + m.b2 > B) m.b2 = B - m.b1;  // B >= 12 here, so b2 >= 4
     m.cta = (nnz >> (m.b1 + m.b2)) > wt;
+    m.staged = m.cta && (nnz >> (m.b1 + m.b2)) <= st;
     mcost = 8 + 36 + 8 + 40 + 40;
   }
+  if (getenv("LCO_LEAFS")) m.staged = 1;
   // schedule overrides for tests and A/B measurements (the defaults above otherwise)
   if (getenv("LCO_MSD_B1")) m.b1 = atoi(getenv("LCO_MSD_B1"));
   if (getenv("LCO_MSD_B2") && m.levels == 2) m.b2 = atoi(getenv("LCO_MSD_B2"));

@@ -55,7 +55,8 @@ struct MsdPlan {
   int levels;
   int b1, b2;
   int rb;
-  int cta;  // leaves sorted by k_leafc (one CTA per leaf) instead of k_leafw (one warp)
+  int cta;     // leaves sorted by one CTA per leaf instead of k_leafw (one warp)
+  int staged;  // CTA leaves of <= ~2K nonzeros: the fully staged k_leafs
 };
 
 struct PassParams;
@@ -78,6 +79,7 @@ cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch
 uint32_t leaf_cap();      // largest leaf one CTA sorts in shared memory
 uint32_t leaf_target();   // expected leaf size the MSD digits aim for (warp leaves)
 uint32_t cta_leaf_cap();  // largest leaf k_leafc sorts
+uint32_t staged_leaf_target();  // expected leaf size for k_leafs
 size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
 cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
 uint32_t tile_nominal(uint64_t nnz, uint64_t segments);  // segment-local path (msd.cu)

@@ -145,6 +145,7 @@ struct LeafArgs {
   const uint32_t* tstart;
   uint32_t ntiles;
   int keymode;             // 0: sort on q = K' div T (rb low bits); 1: on K' (rb bits)
+  int staged;              // CTA leaves: fully staged k_leafs (<= kSCap nonzeros)
 };
 
 // A readable (K', V, position) array set.
@@ -1295,6 +1296,7 @@ static cudaError_t launch_leafw(const LeafArgs& L, cudaStream_t s) {
 
 uint32_t leaf_cap() { return kCCap; }
 uint32_t cta_leaf_cap() { return kCCap; }
+uint32_t staged_leaf_target() { return kSCap * 27 / 32; }  // ~1.94K: ~8 sigma below the cap
 
 template <bool VALS, bool BIG, int CAP = kCCap>
 static cudaError_t launch_leafc_t(const LeafArgs& L, uint32_t grid_cap, cudaStream_t s) {
@@ -1356,9 +1358,16 @@ static cudaError_t launch_leafs_t(const LeafArgs& L, cudaStream_t s) {
 }
 
 // The CTA-leaf kernel launch_leafc picks (also the measurement marker's name).
+static bool use_leafs(const LeafArgs& L, bool single) {
+  return !single && L.rb <= 32 && L.staged && !getenv("LCO_NO_LEAFS") && !getenv("LCO_NO_LEAFR");
+}
+static bool use_leafr(const LeafArgs& L, bool single) {
+  return !single && L.rb <= 32 && !getenv("LCO_NO_LEAFR");
+}
+
 static const char* leafc_kernel(const LeafArgs& L, bool single) {
-  if (!single && L.rb <= 32 && getenv("LCO_LEAFS")) return "k_leafs";
-  if (!single && L.rb <= 32 && !getenv("LCO_NO_LEAFR")) return "k_leafr";
+  if (use_leafs(L, single)) return "k_leafs";
+  if (use_leafr(L, single)) return "k_leafr";
   return "k_leafc";
 }
 
@@ -1366,9 +1375,9 @@ static const char* leafc_kernel(const LeafArgs& L, bool single) {
 // SM; the single-leaf call: 64-bit keys and the in-smem radix fallback.
 static cudaError_t launch_leafc(const LeafArgs& L, bool vals, bool single, uint32_t grid_cap,
                                 cudaStream_t s) {
-  if (!single && L.rb <= 32 && getenv("LCO_LEAFS"))
+  if (use_leafs(L, single))
     return vals ? launch_leafs_t<true>(L, s) : launch_leafs_t<false>(L, s);
-  if (!single && L.rb <= 32 && !getenv("LCO_NO_LEAFR"))
+  if (use_leafr(L, single))
     return vals ? launch_leafr_t<true>(L, s) : launch_leafr_t<false>(L, s);
   if (single) return vals ? launch_leafc_t<true, true>(L, grid_cap, s) : launch_leafc_t<false, true>(L, grid_cap, s);
   return vals ? launch_leafc_t<true, false>(L, grid_cap, s) : launch_leafc_t<false, false>(L, grid_cap, s);
@@ -1585,6 +1594,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   L.b1 = mp.b1;
   L.rb = mp.rb;
   L.cap = kLeafCap;
+  L.staged = mp.staged;
   L.keys_in = io.keys_in;
   L.vals_in = io.vals_in;
   L.idx_in = io.idx_in;

@@ -394,11 +394,12 @@ def test_tile_path_clustered_q(cuda_device):
     check(dims, perm, _np_u64(w.keys), w.vals.numpy(), return_perm=False)
 
 
-@pytest.mark.parametrize("env", [{}, {"LCO_LEAFS": "1", "LCO_MSD_B1": "9", "LCO_MSD_B2": "9"},
+@pytest.mark.parametrize("env", [{}, {"LCO_NO_LEAFS": "1"}, {"LCO_MSD_B1": "9", "LCO_MSD_B2": "9"},
                                  {"LCO_NO_LEAFR": "1"}])
 def test_msd_leaf_variants(env, cuda_device, monkeypatch):
-    """8+8 MSD levels with 32-bit-key CTA leaves (default), 9+9 levels with fully staged
-    leaves, and 64-bit-key CTA leaves: all bit-exact."""
+    """MSD levels with fully staged CTA leaves (default at 14M), 32-bit-key CTA leaves
+    with L2 gathers (default for 1-level ~4K leaves, forced at 14M), 9+9 levels, and
+    64-bit-key CTA leaves: all bit-exact."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     rng = np.random.default_rng(43)

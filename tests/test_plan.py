@@ -138,8 +138,9 @@ def test_call_schedules():
     i = p.info(500_000_000)
     assert i["path"] == "msd" and i["msd_levels"] == 2
     assert sum(i["digit_bits"]) + i["leaf_bits"] == 48
-    # 8-bit MSD digits (runs of ~16 per tile), ~7.6K-nonzero leaves sorted by one CTA
-    assert i["digit_bits"] == [8, 8] and i["leaf_kind"] == "cta"
+    # 8-bit first MSD digit (runs of ~16 per tile), second digit sized for ~1.9K-nonzero
+    # leaves sorted fully staged by one CTA
+    assert i["digit_bits"] == [8, 10] and i["leaf_kind"] == "cta"
     assert p.info(8192)["path"] == "leaf" and p.info(8193)["path"] == "msd"
     assert p.info(40_000)["msd_levels"] == 1
     assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54_484_996)["path"] == "lsd"
