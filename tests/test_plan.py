@@ -217,3 +217,33 @@ def test_hierarchical_stages_compose_to_oracle(order):
         ek, ev, ep = oracle.permute(dims, perm, keys, vals)
         assert np.array_equal(k, ek) and np.array_equal(v.view(np.uint64), ev.view(np.uint64))
         assert np.array_equal(pos, ep), (dims, perm)
+
+
+def test_new_entry_points_reject_bad_arguments_before_any_launch():
+    """lco_add / lco_compress / lco_plan_stage: argument errors are detected on the host
+    (no device memory touched, no GPU needed) and reported as status codes."""
+    import ctypes
+    lib = lco.lib()
+    h = lco.Plan((4, 5, 6), (2, 0, 1))
+    nc = ctypes.c_size_t()
+    assert lib.lco_add_workspace_size(h._h, 10, 20, ctypes.byref(nc)) == 0 and nc.value > 0
+    # lco_add: NULL count / outputs -> LCO_ERR_NULL (1)
+    assert lib.lco_add(h._h, 0, None, None, 0, None, None, 1.0, None, None, None, None, 0, None) == 1
+    # lco_add: operand at or above 2^32 nonzeros -> LCO_ERR_CAPACITY (6)
+    dummy = ctypes.c_void_p(256)
+    assert lib.lco_add(h._h, 2 ** 32, dummy, dummy, 0, None, None, 1.0, dummy, dummy, dummy,
+                       None, 0, None) == 6
+    # lco_compress: zero dims -> LCO_ERR_DIM (3); missing outputs -> LCO_ERR_NULL (1)
+    assert lib.lco_compress(0, None, 0, 5, 0, dummy, None, None, None, None, 0, None) == 3
+    assert lib.lco_compress(10, None, 5, 5, 1, dummy, None, None, None, None, 0, None) == 1
+    b = ctypes.c_size_t()
+    assert lib.lco_compress_workspace_size(1000, 1, ctypes.byref(b)) == 0 and b.value > 0
+    assert lib.lco_compress_workspace_size(1000, 0, ctypes.byref(b)) == 0 and b.value == 0
+    # lco_plan_stage: out-of-range stage -> LCO_ERR_ARG
+    n_st, order = ctypes.c_int(), ctypes.c_int()
+    dims = (ctypes.c_uint64 * 16)()
+    perm = (ctypes.c_int32 * 16)()
+    assert lib.lco_plan_stage(h._h, 5, ctypes.byref(n_st), ctypes.byref(order), dims, perm) != 0
+    assert n_st.value == 1
+    # the MDT table rejects unknown classes
+    assert lib.lco_mdt_choice(4, 0) == -1 and lib.lco_mdt_name(-1) == b"invalid"
