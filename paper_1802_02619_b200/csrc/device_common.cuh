@@ -24,7 +24,7 @@ __host__ __device__ __forceinline__ uint32_t chunk_tiles(uint32_t tiles) {
   uint32_t c = tiles / 512;
   return c < 4 ? 4u : (c > (uint32_t)kChunkTiles ? (uint32_t)kChunkTiles : c);
 }
-constexpr int kScanThreads = 256;
+constexpr int kScanThreads = 1024;  // k_scan: 32 bins x 32 chunk groups per CTA
 constexpr uint32_t kInvalid = 0xFFFFu;
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

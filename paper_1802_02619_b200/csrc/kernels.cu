@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ cs
                                                        uint64_t* __restrict__ counts64,
                                                        int ncounts) {
   constexpr int BINS = 1 << RB;
-  constexpr int LANES = BINS >= 64 ? 64 : BINS;  // bins per CTA
+  constexpr int LANES = BINS >= 32 ? 32 : BINS;  // bins per CTA (one warp-wide row)
   constexpr int SPLIT = kScanThreads / LANES;    // chunk groups per bin
   __shared__ uint32_t part[kScanThreads];
   __shared__ uint32_t s_warp[32];
@@ -644,7 +644,7 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
   if ((e = launch_count(rb, first, a, in_keys, c.thist, c.csum, c.tiles, L.stream)) != cudaSuccess)
     return e;
   if (L.mark) L.mark(L.ctx, "k_scan");
-  const int scan_grid = BINS >= 64 ? BINS / 64 : 1;
+  const int scan_grid = BINS >= 32 ? BINS / 32 : 1;
   switch (rb) {
     case 8:
       k_scan<8><<<scan_grid, kScanThreads, 0, L.stream>>>(c.csum, c.nchunks, c.totals, c.bucket,
