@@ -54,6 +54,8 @@ KERNEL_BYTES = {
     "k_leaf": 36,
     "k_leaf_deferred": 40,
     "k_copy": 36,             # read K, V; write K, V, perm
+    "k_block_bounds": 8,      # read K (run bounds of the blocks)
+    "k_block_tiles": 36,      # read K, V; write K', V, perm (tiled transpose of runs)
     "k_partition": 36,
 }
 STEP_BYTES = 36  # read K+V, write K'+V (32) + the uint32 perm (4)

@@ -44,6 +44,7 @@ struct CallPlan {
   double cost;  // modelled bytes per nonzero
   uint64_t segdiv, segments;  // tile path: identity-prefix segments
   uint64_t nblocks, bfree;    // block path
+  BlockGrid bg;
   KeyPlan kb;
 };
 
@@ -82,15 +83,15 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   c.rb = op.radix_bits;
   c.cost = 4 + 48.0 * op.passes;
   // All rearranged modes in a small old-order prefix: a transpose of runs, no sorting
-  // (block.cu): one read of the keys for the run bounds, O(blocks) tables, one scatter.
-  // Opt-in (LCO_BLOCK=1): measured on C4 1.18 ms vs 0.97 ms for the LSD pass (its
-  // scatter is latency-bound on the key -> delta -> store chain).
-  if (op.nblocks && op.nblocks * 4 <= nnz && op.nblocks < (1ull << 31) && getenv("LCO_BLOCK")) {
-    const double bcost = 8 + 36 + 16.0 * (double)op.nblocks / (double)nnz;
+  // (block.cu): one read of the keys for the run bounds, O(blocks) tables, one tiled
+  // copy that reads and writes long runs.
+  if (op.nblocks && op.nblocks * 4 <= nnz && op.nblocks < (1ull << 31) && !getenv("LCO_NO_BLOCK")) {
+    const double bcost = 8 + 36 + 24.0 * (double)op.nblocks / (double)nnz;
     if (bcost < c.cost) {
       c.path = kPathBlock;
       c.nblocks = op.nblocks;
       c.bfree = op.bfree;
+      c.bg = BlockGrid{op.bdA, op.bdB, op.bmid, op.bhi};
       c.kb = op.kb;
       c.passes = 0;
       c.cost = bcost;
@@ -308,7 +309,7 @@ cudaError_t execute(lco_plan_s* h, const OpPlan& op, uint64_t nnz, const uint64_
   if (cp.path == kPathOnesweep) return run_passes(cp.rb, cp.kp, io, L);
   if (cp.path == kPathTile) return run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
   if (cp.path == kPathSeg) return run_seg(cp.msd.b1, cp.msd.b2, cp.kp, io, L);
-  if (cp.path == kPathBlock) return run_block(cp.kp, cp.kb, cp.nblocks, cp.bfree, io, L);
+  if (cp.path == kPathBlock) return run_block(cp.kp, cp.kb, cp.nblocks, cp.bfree, cp.bg, io, L);
   return run_msd(cp.msd, cp.kp, io, L);
 }
 

@@ -12,11 +12,11 @@
 //   k_block_bounds    run starts / ends of the blocks present (one read of the keys);
 //   k_block_counts    counts moved to the blocks' NEW-order ids (a dense grid transpose);
 //   k_scan_tiles x2   exclusive scan of the counts in new order -> output starts;
-//   k_block_delta     delta[b] = output start - input start (mod 2^32);
-//   k_block_scatter   out = i + delta[b]: K' (LIV shuffle), V, position, one coalesced
-//                     read and one run-coalesced write per nonzero.
+//   k_block_tiles     a tiled transpose of the runs: per tile of blocks, long input runs
+//                     -> LIV shuffle -> shared memory in output order -> long output
+//                     runs (K', V, position).
 // Taken when the block grid is small (<= nnz / 4 blocks): BASELINE C4 (2048 x 2048 blocks
-// of ~13 nonzeros), Table 2's {0,1,3,2}-type permutations.
+// of ~13 nonzeros).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -33,32 +33,41 @@ constexpr int kBkTile = 4096;  // scan tile (counts)
 
 __device__ __forceinline__ uint64_t block_of(uint64_t k, const FastDiv& f) { return fdiv(f, k); }
 
-// One tile of kBkU x 256 consecutive nonzeros per CTA, lane-consecutive: the key loads of
-// a thread are independent (8 in flight), the neighbours come from the same warp's loads
-// or one extra load at the warp's edges.
+// 256 consecutive nonzeros per warp (8 per lane, lane-consecutive): all key loads are
+// issued before any block id is computed; a nonzero's neighbours come from the warp's
+// own registers, plus one key on each side of the warp's range.
 constexpr int kBkU = 8;
 
 __global__ void __launch_bounds__(256) k_block_bounds(uint64_t nnz, const uint64_t* __restrict__ keys,
                                                       FastDiv fF, uint32_t* __restrict__ bstart,
                                                       uint32_t* __restrict__ bend) {
-  const uint64_t base = (uint64_t)blockIdx.x * 256 * kBkU + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint64_t wbase = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * (32 * kBkU);
   uint64_t b[kBkU];
 #pragma unroll
   for (int u = 0; u < kBkU; ++u) {
-    const uint64_t i = base + (uint64_t)u * 256;
-    b[u] = i < nnz ? block_of(__ldcs(keys + i), fF) : ~0ull;
+    const uint64_t i = wbase + u * 32 + lane;
+    b[u] = i < nnz ? __ldcs(keys + i) : 0ull;
   }
-  const int lane = threadIdx.x & 31;
+  uint64_t bp = 0, bn = 0;
+  if (lane == 0 && wbase > 0) bp = __ldg(keys + wbase - 1);
+  if (lane == 31 && wbase + 32 * kBkU < nnz) bn = __ldg(keys + wbase + 32 * kBkU);
+#pragma unroll
+  for (int u = 0; u < kBkU; ++u) b[u] = wbase + u * 32 + lane < nnz ? block_of(b[u], fF) : ~0ull;
+  bp = (lane == 0 && wbase > 0) ? block_of(bp, fF) : ~0ull;
+  bn = (lane == 31 && wbase + 32 * kBkU < nnz) ? block_of(bn, fF) : ~0ull;
 #pragma unroll
   for (int u = 0; u < kBkU; ++u) {
-    const uint64_t i = base + (uint64_t)u * 256;
-    uint64_t prev = __shfl_up_sync(0xffffffffu, b[u], 1);
-    uint64_t next = __shfl_down_sync(0xffffffffu, b[u], 1);
+    const uint64_t i = wbase + u * 32 + lane;
+    const uint64_t up = __shfl_up_sync(0xffffffffu, b[u], 1);
+    const uint64_t dn = __shfl_down_sync(0xffffffffu, b[u], 1);
+    const uint64_t pl = __shfl_sync(0xffffffffu, u > 0 ? b[u > 0 ? u - 1 : 0] : bp, u > 0 ? 31 : 0);
+    const uint64_t nf = __shfl_sync(0xffffffffu, u < kBkU - 1 ? b[u < kBkU - 1 ? u + 1 : 0] : bn,
+                                    u < kBkU - 1 ? 0 : 31);
+    const uint64_t prev = lane == 0 ? pl : up, next = lane == 31 ? nf : dn;
     if (i < nnz) {
-      if (lane == 0) prev = i > 0 ? block_of(__ldg(keys + i - 1), fF) : ~0ull;
-      if (lane == 31 || i + 1 >= nnz) next = i + 1 < nnz ? block_of(__ldg(keys + i + 1), fF) : ~0ull;
-      if (i == 0 || prev != b[u]) bstart[b[u]] = (uint32_t)i;
-      if (i == nnz - 1 || next != b[u]) bend[b[u]] = (uint32_t)(i + 1);
+      if (prev != b[u]) bstart[b[u]] = (uint32_t)i;
+      if (next != b[u]) bend[b[u]] = (uint32_t)(i + 1);
     }
   }
 }
@@ -115,54 +124,175 @@ __global__ void __launch_bounds__(256) k_scan_tiles(uint64_t n, uint32_t* __rest
   }
 }
 
-__global__ void k_block_delta(uint64_t nblocks, const __grid_constant__ KeyPlan kb,
-                              const uint32_t* __restrict__ bstart,
-                              const uint32_t* __restrict__ outstart, uint32_t* __restrict__ delta) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += stride)
-    delta[b] = __ldg(outstart + reencode(kb, b)) - __ldg(bstart + b);
-}
+// ---------------------------------------------------------------------------------
+// k_block_tiles: one tile of TB x TA blocks per CTA (TB consecutive values of the new-
+// innermost block mode B, TA of the old-innermost A, the other block coordinates fixed).
+// Its TB input rows (fixed c_B, c_A in the tile) are contiguous runs of the input and its
+// TA output runs (fixed c_A, c_B in the tile) contiguous runs of the output, so the CTA
+// reads TB long runs, LIV-shuffles the keys and stages K', V and the
+// source position in shared memory in OUTPUT order, then writes TA long runs: the
+// output of a ~13-nonzero block is no longer written by itself (unaligned short runs cap
+// a scatter at ~3 TB/s).  A tile larger than the stage (big blocks) is
+// written straight from registers: its runs are long anyway.
+// ---------------------------------------------------------------------------------
+constexpr int kBtThreads = 256;
+constexpr int kBtLgWarps = 3;
+constexpr int kBtCap = 2048;  // staged nonzeros per tile: 20 B each -> 40 KB, 4 CTAs / SM
+constexpr int kBtU = 4;       // nonzeros per thread per round
+constexpr int kBtTarget = 1700;  // expected nonzeros per tile the host sizes tiles for
 
-// kBkU nonzeros per thread, lane-consecutive (coalesced reads; a block's nonzeros are
-// consecutive in the output too, so the writes come in runs); all loads issued first.
+struct BlockTiling {
+  uint64_t dA, dB, mid, ntA, ntB;
+  int lgTA, lgTB;
+};
+
 template <bool VALS>
-__global__ void __launch_bounds__(256) k_block_scatter(uint64_t nnz, const __grid_constant__ KeyPlan kp,
-                                                       FastDiv fF, const uint64_t* __restrict__ keys_in,
-                                                       const double* __restrict__ vals_in,
-                                                       const uint32_t* __restrict__ idx_in,
-                                                       const uint32_t* __restrict__ delta,
-                                                       uint64_t* __restrict__ keys_out,
-                                                       double* __restrict__ vals_out,
-                                                       uint32_t* __restrict__ perm_out) {
-  // grid-stride over chunks in launch order with a small grid: the concurrently written
-  // output window (one run per block per active chunk) stays small enough for L2 to
-  // complete the partial lines before they are evicted
-  for (uint64_t base = (uint64_t)blockIdx.x * 256 * kBkU + threadIdx.x; base < nnz;
-       base += (uint64_t)gridDim.x * 256 * kBkU) {
-  uint64_t k[kBkU];
-  double v[kBkU];
-  uint32_t o[kBkU];
-#pragma unroll
-  for (int u = 0; u < kBkU; ++u) {
-    const uint64_t i = base + (uint64_t)u * 256;
-    k[u] = i < nnz ? __ldcs(keys_in + i) : 0ull;
-    if (VALS) v[u] = i < nnz ? __ldcs(vals_in + i) : 0.0;
-  }
-#pragma unroll
-  for (int u = 0; u < kBkU; ++u) {
-    const uint64_t i = base + (uint64_t)u * 256;
-    o[u] = i < nnz ? (uint32_t)i + __ldg(delta + block_of(k[u], fF)) : 0u;
-  }
-  reencode_keys<kBkU>(kp, k);
-#pragma unroll
-  for (int u = 0; u < kBkU; ++u) {
-    const uint64_t i = base + (uint64_t)u * 256;
-    if (i < nnz) {
-      keys_out[o[u]] = k[u];
-      if (VALS) vals_out[o[u]] = v[u];
-      if (perm_out) perm_out[o[u]] = idx_in ? __ldg(idx_in + i) : (uint32_t)i;
+__global__ void __launch_bounds__(kBtThreads, 4) k_block_tiles(
+    const __grid_constant__ BlockTiling g, const __grid_constant__ KeyPlan kp,
+    const __grid_constant__ KeyPlan kb, FastDiv fF, const uint64_t* __restrict__ keys_in,
+    const double* __restrict__ vals_in, const uint32_t* __restrict__ idx_in,
+    const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ bend,
+    const uint32_t* __restrict__ outstart, uint64_t* __restrict__ keys_out,
+    double* __restrict__ vals_out, uint32_t* __restrict__ perm_out) {
+  extern __shared__ __align__(16) unsigned char bt_smem[];
+  uint64_t* sK = reinterpret_cast<uint64_t*>(bt_smem);
+  double* sV = reinterpret_cast<double*>(sK + kBtCap);
+  uint32_t* sP = reinterpret_cast<uint32_t*>(sV + kBtCap);
+  __shared__ uint32_t s_cnt[kBtThreads], s_ipre[kBtThreads], s_opre[kBtThreads];  // TA * TB <= threads
+  __shared__ uint32_t s_rowlen[32], s_runlen[32], s_runpre[33], s_rs[32], s_ost[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lgTA = g.lgTA, lgTB = g.lgTB, TA = 1 << lgTA, TB = 1 << lgTB, nblk = TA * TB;
+  // tile -> (hi, B tile, mid, A tile), B tiles fastest: consecutive CTAs extend the same
+  // output runs, so partial sectors at run ends meet in L2
+  uint64_t t = blockIdx.x;
+  const uint64_t bT = t % g.ntB;
+  t /= g.ntB;
+  const uint64_t aT = t % g.ntA;
+  t /= g.ntA;
+  const uint64_t m = t % g.mid, h = t / g.mid;
+  const uint64_t b0 = bT << lgTB, a0 = aT << lgTA;
+  const uint64_t strideB = g.mid * g.dA;
+  const uint64_t base = (h * g.dB * g.mid + m) * g.dA;  // old block id at c_B = c_A = 0
+
+  // 1. counts and starts of the tile's blocks; row-wise (over A) exclusive scan
+  {
+    const int b = tid >> lgTA, a = tid & (TA - 1);
+    uint32_t c = 0, s = 0;
+    if (tid < nblk && b0 + b < g.dB && a0 + a < g.dA) {
+      const uint64_t id = base + (b0 + b) * strideB + a0 + a;
+      s = __ldg(bstart + id);
+      c = __ldg(bend + id) - s;
+      // the output start of run a = the new-order start of its first block (b = 0)
+      if (b == 0) s_ost[a] = __ldg(outstart + reencode(kb, id));
+    }
+    uint32_t incl = c;
+    for (int o = 1; o < TA; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, TA);
+      if (a >= o) incl += y;
+    }
+    if (tid < nblk) {
+      s_cnt[tid] = c;
+      s_ipre[tid] = incl - c;
+      if (a == TA - 1) s_rowlen[b] = incl;
+      if (c) s_rs[b] = s - (incl - c);  // every present block of a row agrees
     }
   }
+  __syncthreads();
+  // 2. column-wise (over B) exclusive scan: offsets of the blocks in their output run
+  {
+    const int a = tid >> lgTB, b = tid & (TB - 1);
+    const uint32_t c = tid < nblk ? s_cnt[(b << lgTA) + a] : 0u;
+    uint32_t incl = c;
+    for (int o = 1; o < TB; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o, TB);
+      if (b >= o) incl += y;
+    }
+    if (tid < nblk) {
+      s_opre[(a << lgTB) + b] = incl - c;
+      if (b == TB - 1) s_runlen[a] = incl;
+    }
+  }
+  __syncthreads();
+  // 3. run prefixes (the output-ordered stage) and the output start of every run
+  if (warp == 0) {
+    const uint32_t v = lane < TA ? s_runlen[lane] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane < TA) s_runpre[lane] = incl - v;
+    if (lane == TA - 1) s_runpre[TA] = incl;
+  }
+  __syncthreads();
+  const uint32_t E = s_runpre[TA];
+  const bool staged = E <= (uint32_t)kBtCap;
+  // 4. per block: destination = position in its row + delta (stage or output index)
+  if (tid < nblk) {
+    const int b = tid >> lgTA, a = tid & (TA - 1);
+    s_cnt[tid] = (staged ? s_runpre[a] : s_ost[a]) + s_opre[(a << lgTB) + b] - s_ipre[tid];
+  }
+  __syncthreads();
+
+  // 5. read the rows (2^lgW warps per row, coalesced), LIV shuffle, place in output
+  //    order; a nonzero's block within its row is its own old block id minus the row's
+  {
+    const int lgW = lgTB >= kBtLgWarps ? 0 : kBtLgWarps - lgTB;
+    const uint32_t gw = 32u << lgW, g0 = ((warp & ((1 << lgW) - 1)) << 5) + lane;
+    for (int b = warp >> lgW; b < TB; b += (kBtThreads / 32) >> lgW) {
+      const uint32_t len = s_rowlen[b];
+      const uint32_t rs = s_rs[b];
+      const uint64_t id0 = base + (b0 + b) * strideB + a0;
+      const uint32_t* dl = s_cnt + (b << lgTA);
+      for (uint32_t r0 = 0; r0 < len; r0 += gw * kBtU) {
+        uint64_t k[kBtU];
+        double v[kBtU];
+        uint32_t blk[kBtU];
+#pragma unroll
+        for (int u = 0; u < kBtU; ++u) {
+          const uint32_t r = r0 + g0 + u * gw;
+          k[u] = r < len ? __ldcs(keys_in + rs + r) : 0ull;
+          if (VALS) v[u] = r < len ? __ldcs(vals_in + rs + r) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kBtU; ++u) blk[u] = (uint32_t)(fdiv(fF, k[u]) - id0);
+        reencode_keys<kBtU>(kp, k);
+#pragma unroll
+        for (int u = 0; u < kBtU; ++u) {
+          const uint32_t r = r0 + g0 + u * gw;
+          if (r >= len) continue;
+          const uint32_t d = r + dl[blk[u]];
+          const uint32_t p = idx_in ? __ldg(idx_in + rs + r) : rs + r;
+          if (staged) {
+            sK[d] = k[u];
+            if (VALS) sV[d] = v[u];
+            sP[d] = p;
+          } else {
+            keys_out[d] = k[u];
+            if (VALS) vals_out[d] = v[u];
+            if (perm_out) perm_out[d] = p;
+          }
+        }
+      }
+    }
+  }
+  if (!staged) return;
+  __syncthreads();
+  // 6. write the TA output runs (2^lgW warps per run)
+  {
+    const int lgW = lgTA >= kBtLgWarps ? 0 : kBtLgWarps - lgTA;
+    const uint32_t gw = 32u << lgW, g0 = ((warp & ((1 << lgW) - 1)) << 5) + lane;
+    for (int a = warp >> lgW; a < TA; a += (kBtThreads / 32) >> lgW) {
+      const uint32_t s0 = s_runpre[a], n = s_runpre[a + 1] - s0;
+      const uint32_t o = s_ost[a];
+#pragma unroll 2
+      for (uint32_t j = g0; j < n; j += gw) {
+        keys_out[o + j] = sK[s0 + j];
+        if (VALS) vals_out[o + j] = sV[s0 + j];
+        if (perm_out) perm_out[o + j] = sP[s0 + j];
+      }
+    }
   }
 }
 
@@ -172,13 +302,13 @@ size_t block_ctrl_bytes(uint64_t nblocks) {
 }
 
 cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, uint64_t F,
-                      const PassIO& io, const Launch& L) {
+                      const BlockGrid& bg, const PassIO& io, const Launch& L) {
   cudaError_t e;
   const uint64_t nnz = io.nnz;
   const size_t tb = (nblocks * 4 + 255) / 256 * 256;
   char* cb = reinterpret_cast<char*>(io.ctrl);
   uint32_t* bstart = reinterpret_cast<uint32_t*>(cb);
-  uint32_t* bend = reinterpret_cast<uint32_t*>(cb + tb);  // later: delta
+  uint32_t* bend = reinterpret_cast<uint32_t*>(cb + tb);
   uint32_t* cnew = reinterpret_cast<uint32_t*>(cb + 2 * tb);  // later: output starts
   const uint64_t nt = (nblocks + kBkTile - 1) / kBkTile;
   uint32_t* sums = reinterpret_cast<uint32_t*>(cb + 3 * tb);
@@ -186,7 +316,7 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   uint64_t* total = toff + nt;
   const FastDiv fF = make_fastdiv(F);
   if ((e = cudaMemsetAsync(bstart, 0, 2 * tb, L.stream)) != cudaSuccess) return e;
-  const unsigned gn = (unsigned)((nnz + 256 * kBkU - 1) / (256 * kBkU));
+  const unsigned gn = (unsigned)((nnz + 256 * kBkU - 1) / (256 * kBkU));  // 8 warps x 256
   const unsigned gb = (unsigned)umin64((nblocks + 255) / 256, 148 * 16);
   if (L.mark) L.mark(L.ctx, "k_block_bounds");
   k_block_bounds<<<gn, 256, 0, L.stream>>>(nnz, io.keys_in, fF, bstart, bend);
@@ -201,17 +331,50 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
     return e;
   k_scan_tiles<false><<<(unsigned)nt, 256, 0, L.stream>>>(nblocks, cnew, nullptr, toff);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (L.mark) L.mark(L.ctx, "k_block_delta");
-  k_block_delta<<<gb, 256, 0, L.stream>>>(nblocks, kb, bstart, cnew, bend);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (L.mark) L.mark(L.ctx, "k_block_scatter");
-  const unsigned gsc = (unsigned)umin64(gn, 148 * 32);
-  if (io.vals_out)
-    k_block_scatter<true><<<gsc, 256, 0, L.stream>>>(nnz, kp, fF, io.keys_in, io.vals_in, io.idx_in,
-                                                   bend, io.keys_out, io.vals_out, io.perm_out);
-  else
-    k_block_scatter<false><<<gsc, 256, 0, L.stream>>>(nnz, kp, fF, io.keys_in, io.vals_in, io.idx_in,
-                                                    bend, io.keys_out, io.vals_out, io.perm_out);
+  // tile shape: about kBtTarget expected nonzeros, at most 32 x 32 blocks and 256 in all,
+  // the longer side along B (the output runs)
+  BlockTiling g;
+  g.dA = bg.dA;
+  g.dB = bg.dB;
+  g.mid = bg.mid;
+  int lg = 0;
+  const double avg = (double)nnz / (double)nblocks;
+  while (lg < 8 && avg * (double)(2ull << lg) <= kBtTarget) ++lg;
+  const int capA = umin64(ceil_log2(bg.dA), 5), capB = umin64(ceil_log2(bg.dB), 5);
+  int lgB = umin64((lg + 1) / 2, capB);
+  int lgA = umin64(lg - lgB, capA);
+  lgB = umin64(lg - lgA, capB);
+  g.lgTA = lgA;
+  g.lgTB = lgB;
+  g.ntA = (bg.dA + (1ull << lgA) - 1) >> lgA;
+  g.ntB = (bg.dB + (1ull << lgB) - 1) >> lgB;
+  const uint64_t ntiles = g.ntA * g.ntB * bg.mid * bg.hi;
+  if (ntiles >= (1ull << 31)) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)kBtCap * 20;
+  if (L.mark) L.mark(L.ctx, "k_block_tiles");
+  if (io.vals_out) {
+    static bool attr = false;
+    if (!attr) {
+      if ((e = cudaFuncSetAttribute(k_block_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      attr = true;
+    }
+    k_block_tiles<true><<<(unsigned)ntiles, kBtThreads, smem, L.stream>>>(
+        g, kp, kb, fF, io.keys_in, io.vals_in, io.idx_in, bstart, bend, cnew, io.keys_out,
+        io.vals_out, io.perm_out);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      if ((e = cudaFuncSetAttribute(k_block_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      attr = true;
+    }
+    k_block_tiles<false><<<(unsigned)ntiles, kBtThreads, smem, L.stream>>>(
+        g, kp, kb, fF, io.keys_in, io.vals_in, io.idx_in, bstart, bend, cnew, io.keys_out,
+        io.vals_out, io.perm_out);
+  }
   return cudaGetLastError();
 }
 

@@ -88,9 +88,14 @@ cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const L
 cudaError_t run_count_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, uint64_t* total,
                            const Launch& L);
 // block-transpose schedule (block.cu)
+// grid of blocks as (hi, B, mid, A): dims of the old-innermost block mode A and the
+// new-innermost block mode B, products of the block modes before B / between B and A
+struct BlockGrid {
+  uint64_t dA, dB, mid, hi;
+};
 size_t block_ctrl_bytes(uint64_t nblocks);
 cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, uint64_t F,
-                      const PassIO& io, const Launch& L);
+                      const BlockGrid& bg, const PassIO& io, const Launch& L);
 // compressed matrix datatypes (mdt.cu)
 size_t compress_ctrl_bytes(uint64_t nnz);
 cudaError_t run_compress(uint64_t nnz, const uint64_t* keys, uint64_t n_major, uint64_t n_minor,

@@ -210,8 +210,12 @@ struct OpPlan {
   KeyPlan kp;
   uint64_t trailing, middle, segments, segdiv;
   // block-transpose schedule: old modes 0..k (k = last old position of a prefix / middle
-  // mode) form the block id K div bfree; kb maps a block id to its new-order id
+  // mode) form the block id K div bfree; kb maps a block id to its new-order id.  The
+  // block grid as (hi, B, mid, A): A = old mode k (innermost old), B = the innermost
+  // block mode of the new order, hi / mid = products of the block modes before B and
+  // between B and A (the tile decomposition of k_block_tiles)
   uint64_t nblocks, bfree;
+  uint64_t bdA, bdB, bmid, bhi;
   KeyPlan kb;
 };
 

@@ -259,6 +259,13 @@ static void flat_permute(const FlatInfo& fi, OpPlan* op) {
     op->nblocks = nb;
     op->bfree = F;
     op->kb = make_keyplan(k + 1, nd, bp, 1);
+    const int B = bp[k];  // != k: the old-innermost block mode never stays innermost
+    op->bdA = nd[k];
+    op->bdB = nd[B];
+    op->bmid = 1;
+    op->bhi = 1;
+    for (int m = B + 1; m < k; ++m) op->bmid *= nd[m];
+    for (int m = 0; m < B; ++m) op->bhi *= nd[m];
   }
 }
 

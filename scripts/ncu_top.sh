@@ -4,6 +4,6 @@
 mkdir -p gpurun_out
 name=$1; kre=$2; skip=$3; shift 3
 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu "$@" > gpurun_out/ncu_${name}_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"$kre" -s $skip -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"$kre" -s $skip -c ${COUNT:-1} \
     -o gpurun_out/prof_${name} -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu "$@" > gpurun_out/ncu_${name}.log 2>&1
 echo "ncu rc=$?"

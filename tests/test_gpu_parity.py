@@ -593,12 +593,15 @@ def test_flatten_to_csc_and_roundtrip(cuda_device):
 @pytest.mark.parametrize("dims,perm", [((37, 41, 1000), (1, 0, 2)),
                                        ((64, 32, 16, 300), (2, 0, 1, 3)),
                                        ((50, 60, 7, 90), (1, 0, 2, 3)),
-                                       ((16, 8, 12, 10, 200), (1, 2, 0, 3, 4))])
-def test_block_path(dims, perm, cuda_device, monkeypatch):
+                                       ((16, 8, 12, 10, 200), (1, 2, 0, 3, 4)),
+                                       ((5, 6, 1 << 20), (1, 0, 2)),
+                                       ((3, 700, 9, 400), (0, 2, 1, 3))])
+def test_block_path(dims, perm, cuda_device):
     """Permutations whose rearranged modes lie in a small old-order prefix: a transpose of
-    runs without sorting (run bounds, block counts in new order, scan, one scatter) - non-
-    power-of-two dims, empty blocks, runs spanning thread boundaries (opt-in schedule)."""
-    monkeypatch.setenv("LCO_BLOCK", "1")
+    runs without sorting (run bounds, block counts in new order, scan, one tiled copy) -
+    non-power-of-two dims, empty blocks, ragged tiles at the grid edges, modes between
+    and before the tile modes, blocks larger than the on-chip stage ((5, 6, 2^20): ~8K
+    nonzeros per block, written straight from registers)."""
     rng = np.random.default_rng(sum(dims))
     keys, vals = _rand_sorted(rng, dims, 250_000)
     info = lco.plan(dims, perm).info(len(keys))

@@ -105,7 +105,7 @@ def test_baseline_config_plans():
         ("C2b", (512,) * 4, (0, 2, 1, 3), 1308672): (18, "tile"),
         ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2), 14581760): (21, "lsd"),
         ("C3b", (128,) * 6, (0, 3, 1, 4, 2, 5), 14581760): (28, "lsd"),
-        ("C4", (2048,) * 4, (1, 0, 2, 3), 54484996): (11, "lsd"),
+        ("C4", (2048,) * 4, (1, 0, 2, 3), 54484996): (11, "block"),
         ("C5", (4096,) * 5, (4, 3, 2, 1, 0), 500_000_000): (48, "msd"),
     }
     for (name, dims, perm, nnz), (bits, path) in cases.items():
@@ -127,7 +127,7 @@ def test_baseline_config_plans():
     assert c2b["num_segments"] == 512 and c2b["leaf_kind"] == "cta" and c2b["launches"] == 3
     c4 = lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54484996)
     assert c4["norm_dims"] == [2048, 2048, 2 ** 22] and c4["norm_perm"] == [1, 0, 2]
-    assert c4["trailing"] == 2048 * 2 ** 22 and c4["passes"] == 1
+    assert c4["trailing"] == 2048 * 2 ** 22 and c4["path"] == "block" and c4["passes"] == 0
 
 
 def test_call_schedules():
@@ -143,6 +143,13 @@ def test_call_schedules():
     assert i["digit_bits"] == [8, 10] and i["leaf_kind"] == "cta"
     assert p.info(8192)["path"] == "leaf" and p.info(8193)["path"] == "msd"
     assert p.info(40_000)["msd_levels"] == 1
+    # C4: the rearranged modes (x, y) lie before the free (x', y') modes -> a tiled
+    # transpose of the 2048 x 2048 grid of runs; without it, one 11-bit LSD pass
+    assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54_484_996)["path"] == "block"
+
+
+def test_block_schedule_opt_out(monkeypatch):
+    monkeypatch.setenv("LCO_NO_BLOCK", "1")
     assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(54_484_996)["path"] == "lsd"
 
 
