@@ -34,8 +34,9 @@ constexpr int kBkTile = 4096;  // scan tile (counts)
 __device__ __forceinline__ uint64_t block_of(uint64_t k, const FastDiv& f) { return fdiv(f, k); }
 
 // 256 consecutive nonzeros per warp (8 per lane, lane-consecutive): all key loads are
-// issued before any block id is computed; a nonzero's neighbours come from the warp's
-// own registers, plus one key on each side of the warp's range.
+// issued before any block id is computed; block ids are 32-bit (nblocks < 2^31); each
+// nonzero's neighbours come from one lane rotation per direction (lane 0's predecessor is
+// the previous item's rotated value at lane 0), plus one key on each side of the warp.
 constexpr int kBkU = 8;
 
 __global__ void __launch_bounds__(256) k_block_bounds(uint64_t nnz, const uint64_t* __restrict__ keys,
@@ -43,28 +44,36 @@ __global__ void __launch_bounds__(256) k_block_bounds(uint64_t nnz, const uint64
                                                       uint32_t* __restrict__ bend) {
   const int lane = threadIdx.x & 31;
   const uint64_t wbase = ((uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * (32 * kBkU);
-  uint64_t b[kBkU];
+  uint64_t k[kBkU];
 #pragma unroll
   for (int u = 0; u < kBkU; ++u) {
     const uint64_t i = wbase + u * 32 + lane;
-    b[u] = i < nnz ? __ldcs(keys + i) : 0ull;
+    k[u] = i < nnz ? __ldcs(keys + i) : 0ull;
   }
-  uint64_t bp = 0, bn = 0;
-  if (lane == 0 && wbase > 0) bp = __ldg(keys + wbase - 1);
-  if (lane == 31 && wbase + 32 * kBkU < nnz) bn = __ldg(keys + wbase + 32 * kBkU);
+  const bool has_p = wbase > 0, has_n = wbase + 32 * kBkU < nnz;
+  const uint64_t kp = (lane == 31 && has_p) ? __ldg(keys + wbase - 1) : 0ull;
+  const uint64_t kn = (lane == 0 && has_n) ? __ldg(keys + wbase + 32 * kBkU) : 0ull;
+  constexpr uint32_t kNone = 0xffffffffu;
+  uint32_t b[kBkU];
 #pragma unroll
-  for (int u = 0; u < kBkU; ++u) b[u] = wbase + u * 32 + lane < nnz ? block_of(b[u], fF) : ~0ull;
-  bp = (lane == 0 && wbase > 0) ? block_of(bp, fF) : ~0ull;
-  bn = (lane == 31 && wbase + 32 * kBkU < nnz) ? block_of(bn, fF) : ~0ull;
+  for (int u = 0; u < kBkU; ++u)
+    b[u] = wbase + u * 32 + lane < nnz ? (uint32_t)block_of(k[u], fF) : kNone;
+  // rotations: up[u] at lane l = b[u] at lane l-1 (lane 0: lane 31), dn[u] at lane l =
+  // b[u] at lane l+1 (lane 31: lane 0)
+  uint32_t up_prev = __shfl_sync(0xffffffffu, (lane == 31 && has_p) ? (uint32_t)block_of(kp, fF) : kNone,
+                                 (lane + 31) & 31);
+  uint32_t dn[kBkU + 1];
+#pragma unroll
+  for (int u = 0; u < kBkU; ++u) dn[u] = __shfl_sync(0xffffffffu, b[u], (lane + 1) & 31);
+  dn[kBkU] = __shfl_sync(0xffffffffu, (lane == 0 && has_n) ? (uint32_t)block_of(kn, fF) : kNone,
+                         (lane + 1) & 31);
 #pragma unroll
   for (int u = 0; u < kBkU; ++u) {
     const uint64_t i = wbase + u * 32 + lane;
-    const uint64_t up = __shfl_up_sync(0xffffffffu, b[u], 1);
-    const uint64_t dn = __shfl_down_sync(0xffffffffu, b[u], 1);
-    const uint64_t pl = __shfl_sync(0xffffffffu, u > 0 ? b[u > 0 ? u - 1 : 0] : bp, u > 0 ? 31 : 0);
-    const uint64_t nf = __shfl_sync(0xffffffffu, u < kBkU - 1 ? b[u < kBkU - 1 ? u + 1 : 0] : bn,
-                                    u < kBkU - 1 ? 0 : 31);
-    const uint64_t prev = lane == 0 ? pl : up, next = lane == 31 ? nf : dn;
+    const uint32_t up = __shfl_sync(0xffffffffu, b[u], (lane + 31) & 31);
+    const uint32_t prev = lane == 0 ? up_prev : up;  // lane 0: item u-1 at lane 31
+    const uint32_t next = lane == 31 ? dn[u + 1] : dn[u];  // lane 31: item u+1 at lane 0
+    up_prev = up;
     if (i < nnz) {
       if (prev != b[u]) bstart[b[u]] = (uint32_t)i;
       if (next != b[u]) bend[b[u]] = (uint32_t)(i + 1);
@@ -142,9 +151,22 @@ constexpr int kBtU = 4;       // nonzeros per thread per round
 constexpr int kBtTarget = 1700;  // expected nonzeros per tile the host sizes tiles for
 
 struct BlockTiling {
-  uint64_t dA, dB, mid, ntA, ntB;
+  uint64_t dA, dB;
+  uint32_t mid, ntA, ntB;  // tile counts < 2^31: 32-bit index arithmetic
   int lgTA, lgTB;
 };
+
+__device__ __forceinline__ uint64_t tile_base(const BlockTiling& g, uint32_t t, uint64_t* b0,
+                                              uint64_t* a0) {
+  const uint32_t bT = t % g.ntB;
+  t /= g.ntB;
+  const uint32_t aT = t % g.ntA;
+  t /= g.ntA;
+  *b0 = (uint64_t)bT << g.lgTB;
+  *a0 = (uint64_t)aT << g.lgTA;
+  // old block id at c_B = c_A = 0
+  return ((uint64_t)(t / g.mid) * g.dB * g.mid + t % g.mid) * g.dA;
+}
 
 template <bool VALS>
 __global__ void __launch_bounds__(kBtThreads, 4) k_block_tiles(
@@ -164,16 +186,9 @@ __global__ void __launch_bounds__(kBtThreads, 4) k_block_tiles(
   const int lgTA = g.lgTA, lgTB = g.lgTB, TA = 1 << lgTA, TB = 1 << lgTB, nblk = TA * TB;
   // tile -> (hi, B tile, mid, A tile), B tiles fastest: consecutive CTAs extend the same
   // output runs, so partial sectors at run ends meet in L2
-  uint64_t t = blockIdx.x;
-  const uint64_t bT = t % g.ntB;
-  t /= g.ntB;
-  const uint64_t aT = t % g.ntA;
-  t /= g.ntA;
-  const uint64_t m = t % g.mid, h = t / g.mid;
-  const uint64_t b0 = bT << lgTB, a0 = aT << lgTA;
-  const uint64_t strideB = g.mid * g.dA;
-  const uint64_t base = (h * g.dB * g.mid + m) * g.dA;  // old block id at c_B = c_A = 0
-
+  uint64_t b0, a0;
+  const uint64_t base = tile_base(g, blockIdx.x, &b0, &a0);
+  const uint64_t strideB = (uint64_t)g.mid * g.dA;
   // 1. counts and starts of the tile's blocks; row-wise (over A) exclusive scan
   {
     const int b = tid >> lgTA, a = tid & (TA - 1);
@@ -336,7 +351,6 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   BlockTiling g;
   g.dA = bg.dA;
   g.dB = bg.dB;
-  g.mid = bg.mid;
   int lg = 0;
   const double avg = (double)nnz / (double)nblocks;
   while (lg < 8 && avg * (double)(2ull << lg) <= kBtTarget) ++lg;
@@ -346,10 +360,12 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   lgB = umin64(lg - lgA, capB);
   g.lgTA = lgA;
   g.lgTB = lgB;
-  g.ntA = (bg.dA + (1ull << lgA) - 1) >> lgA;
-  g.ntB = (bg.dB + (1ull << lgB) - 1) >> lgB;
-  const uint64_t ntiles = g.ntA * g.ntB * bg.mid * bg.hi;
+  const uint64_t ntA = (bg.dA + (1ull << lgA) - 1) >> lgA, ntB = (bg.dB + (1ull << lgB) - 1) >> lgB;
+  const uint64_t ntiles = ntA * ntB * bg.mid * bg.hi;
   if (ntiles >= (1ull << 31)) return cudaErrorInvalidValue;
+  g.ntA = (uint32_t)ntA;
+  g.ntB = (uint32_t)ntB;
+  g.mid = (uint32_t)bg.mid;
   const size_t smem = (size_t)kBtCap * 20;
   if (L.mark) L.mark(L.ctx, "k_block_tiles");
   if (io.vals_out) {
