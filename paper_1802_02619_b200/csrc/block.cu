@@ -146,9 +146,17 @@ __global__ void __launch_bounds__(256) k_scan_tiles(uint64_t n, uint32_t* __rest
 // ---------------------------------------------------------------------------------
 constexpr int kBtThreads = 256;
 constexpr int kBtLgWarps = 3;
-constexpr int kBtCap = 2048;  // staged nonzeros per tile: 20 B each -> 40 KB, 4 CTAs / SM
-constexpr int kBtU = 4;       // nonzeros per thread per round
-constexpr int kBtTarget = 1700;  // expected nonzeros per tile the host sizes tiles for
+#ifndef LCO_BT_CAP
+#define LCO_BT_CAP 2048
+#define LCO_BT_MINB 4
+#define LCO_BT_TARGET 1700
+#endif
+constexpr int kBtCap = LCO_BT_CAP;  // staged nonzeros per tile: 17 B each
+#ifndef LCO_BT_U
+#define LCO_BT_U 2
+#endif
+constexpr int kBtU = LCO_BT_U;  // nonzeros per thread per round
+constexpr int kBtTarget = LCO_BT_TARGET;  // expected nonzeros per tile the host sizes tiles for
 
 struct BlockTiling {
   uint64_t dA, dB;
@@ -169,19 +177,21 @@ __device__ __forceinline__ uint64_t tile_base(const BlockTiling& g, uint32_t t, 
 }
 
 template <bool VALS>
-__global__ void __launch_bounds__(kBtThreads, 4) k_block_tiles(
+__global__ void __launch_bounds__(kBtThreads, LCO_BT_MINB) k_block_tiles(
     const __grid_constant__ BlockTiling g, const __grid_constant__ KeyPlan kp,
     const __grid_constant__ KeyPlan kb, FastDiv fF, const uint64_t* __restrict__ keys_in,
     const double* __restrict__ vals_in, const uint32_t* __restrict__ idx_in,
     const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ bend,
     const uint32_t* __restrict__ outstart, uint64_t* __restrict__ keys_out,
     double* __restrict__ vals_out, uint32_t* __restrict__ perm_out) {
+  // input-ordered stage of the rows (K, V) and, per output slot, the row it comes from
   extern __shared__ __align__(16) unsigned char bt_smem[];
   uint64_t* sK = reinterpret_cast<uint64_t*>(bt_smem);
   double* sV = reinterpret_cast<double*>(sK + kBtCap);
-  uint32_t* sP = reinterpret_cast<uint32_t*>(sV + kBtCap);
+  uint8_t* sB = reinterpret_cast<uint8_t*>(sV + kBtCap);
   __shared__ uint32_t s_cnt[kBtThreads], s_ipre[kBtThreads], s_opre[kBtThreads];  // TA * TB <= threads
-  __shared__ uint32_t s_rowlen[32], s_runlen[32], s_runpre[33], s_rs[32], s_ost[32];
+  __shared__ uint32_t s_rowlen[32], s_runlen[32], s_runpre[33], s_rowoff[33], s_rs[32], s_ost[32],
+      s_pdel[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lgTA = g.lgTA, lgTB = g.lgTB, TA = 1 << lgTA, TB = 1 << lgTB, nblk = TA * TB;
   // tile -> (hi, B tile, mid, A tile), B tiles fastest: consecutive CTAs extend the same
@@ -228,84 +238,120 @@ __global__ void __launch_bounds__(kBtThreads, 4) k_block_tiles(
     }
   }
   __syncthreads();
-  // 3. run prefixes (the output-ordered stage) and the output start of every run
-  if (warp == 0) {
-    const uint32_t v = lane < TA ? s_runlen[lane] : 0u;
+  // 3. run prefixes (output slots) and row offsets (input stage)
+  if (warp < 2) {
+    const int nr = warp == 0 ? TA : TB;
+    const uint32_t v = lane < nr ? (warp == 0 ? s_runlen[lane] : s_rowlen[lane]) : 0u;
     uint32_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += y;
     }
-    if (lane < TA) s_runpre[lane] = incl - v;
-    if (lane == TA - 1) s_runpre[TA] = incl;
+    uint32_t* pre = warp == 0 ? s_runpre : s_rowoff;
+    if (lane < nr) pre[lane] = incl - v;
+    if (lane == nr - 1) pre[nr] = incl;
   }
   __syncthreads();
   const uint32_t E = s_runpre[TA];
-  const bool staged = E <= (uint32_t)kBtCap;
-  // 4. per block: destination = position in its row + delta (stage or output index)
-  if (tid < nblk) {
-    const int b = tid >> lgTA, a = tid & (TA - 1);
-    s_cnt[tid] = (staged ? s_runpre[a] : s_ost[a]) + s_opre[(a << lgTB) + b] - s_ipre[tid];
-  }
-  __syncthreads();
-
-  // 5. read the rows (2^lgW warps per row, coalesced), LIV shuffle, place in output
-  //    order; a nonzero's block within its row is its own old block id minus the row's
-  {
-    const int lgW = lgTB >= kBtLgWarps ? 0 : kBtLgWarps - lgTB;
+  if (E <= (uint32_t)kBtCap) {
+    // 4. rows -> input stage with cp.async (no registers held, every row in flight at
+    //    once; measured faster than one TMA bulk copy per row, whose ~1 KB copies of
+    //    16-byte aligned row interiors ran C4's tiles at 0.50 vs 0.45 ms)
+    {
+      const int lgW = lgTB >= kBtLgWarps ? 0 : kBtLgWarps - lgTB;
+      const uint32_t gw = 32u << lgW, g0 = ((warp & ((1 << lgW) - 1)) << 5) + lane;
+      for (int b = warp >> lgW; b < TB; b += (kBtThreads / 32) >> lgW) {
+        const uint32_t len = s_rowlen[b], rs = s_rs[b], ro = s_rowoff[b];
+        for (uint32_t r = g0; r < len; r += gw) {
+          cp_async8(sK + ro + r, keys_in + rs + r);
+          if (VALS) cp_async8(sV + ro + r, vals_in + rs + r);
+        }
+      }
+      cp_async_commit();
+    }
+    // 5. while they fly: per block, stage offset of its slots; per slot, its row
+    if (tid < nblk) {
+      const int b = tid >> lgTA, a = tid & (TA - 1);
+      const uint32_t c = s_cnt[tid], first = s_runpre[a] + s_opre[(a << lgTB) + b];
+      for (uint32_t w = 0; w < c; ++w) sB[first + w] = (uint8_t)b;
+      s_opre[(a << lgTB) + b] = s_rowoff[b] + s_ipre[tid] - first;  // stage index - slot
+      if (a == 0) s_pdel[b] = s_rs[b] - s_rowoff[b];               // input index - stage
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // 6. write the TA output runs (2^lgW warps per run): gather from the stage, LIV
+    //    shuffle, long coalesced runs of K', V and the source position
+    const int lgW = lgTA >= kBtLgWarps ? 0 : kBtLgWarps - lgTA;
     const uint32_t gw = 32u << lgW, g0 = ((warp & ((1 << lgW) - 1)) << 5) + lane;
-    for (int b = warp >> lgW; b < TB; b += (kBtThreads / 32) >> lgW) {
-      const uint32_t len = s_rowlen[b];
-      const uint32_t rs = s_rs[b];
-      const uint64_t id0 = base + (b0 + b) * strideB + a0;
-      const uint32_t* dl = s_cnt + (b << lgTA);
-      for (uint32_t r0 = 0; r0 < len; r0 += gw * kBtU) {
+    for (int a = warp >> lgW; a < TA; a += (kBtThreads / 32) >> lgW) {
+      const uint32_t s0 = s_runpre[a], n = s_runpre[a + 1] - s0, o = s_ost[a];
+      const uint32_t* so = s_opre + (a << lgTB);
+      for (uint32_t j0 = g0; j0 < n; j0 += gw * kBtU) {
         uint64_t k[kBtU];
-        double v[kBtU];
-        uint32_t blk[kBtU];
+        uint32_t src[kBtU];
 #pragma unroll
         for (int u = 0; u < kBtU; ++u) {
-          const uint32_t r = r0 + g0 + u * gw;
-          k[u] = r < len ? __ldcs(keys_in + rs + r) : 0ull;
-          if (VALS) v[u] = r < len ? __ldcs(vals_in + rs + r) : 0.0;
+          const uint32_t j = j0 + u * gw;
+          src[u] = 0;
+          if (j < n) {
+            const uint32_t jj = s0 + j;
+            src[u] = jj + so[sB[jj]];
+          }
+          k[u] = sK[src[u]];
         }
-#pragma unroll
-        for (int u = 0; u < kBtU; ++u) blk[u] = (uint32_t)(fdiv(fF, k[u]) - id0);
         reencode_keys<kBtU>(kp, k);
 #pragma unroll
         for (int u = 0; u < kBtU; ++u) {
-          const uint32_t r = r0 + g0 + u * gw;
-          if (r >= len) continue;
-          const uint32_t d = r + dl[blk[u]];
-          const uint32_t p = idx_in ? __ldg(idx_in + rs + r) : rs + r;
-          if (staged) {
-            sK[d] = k[u];
-            if (VALS) sV[d] = v[u];
-            sP[d] = p;
-          } else {
-            keys_out[d] = k[u];
-            if (VALS) vals_out[d] = v[u];
-            if (perm_out) perm_out[d] = p;
+          const uint32_t j = j0 + u * gw;
+          if (j >= n) continue;
+          keys_out[o + j] = k[u];
+          if (VALS) vals_out[o + j] = sV[src[u]];
+          if (perm_out) {
+            const uint32_t p = src[u] + s_pdel[sB[s0 + j]];
+            perm_out[o + j] = idx_in ? __ldg(idx_in + p) : p;
           }
         }
       }
     }
+    return;
   }
-  if (!staged) return;
+  // Tile larger than the stage (blocks of thousands of nonzeros: long runs anyway): per
+  // nonzero, destination = position in its row + delta, written from registers; a
+  // nonzero's block within its row is its own old block id minus the row's.
+  if (tid < nblk) {
+    const int b = tid >> lgTA, a = tid & (TA - 1);
+    s_cnt[tid] = s_ost[a] + s_opre[(a << lgTB) + b] - s_ipre[tid];
+  }
   __syncthreads();
-  // 6. write the TA output runs (2^lgW warps per run)
-  {
-    const int lgW = lgTA >= kBtLgWarps ? 0 : kBtLgWarps - lgTA;
-    const uint32_t gw = 32u << lgW, g0 = ((warp & ((1 << lgW) - 1)) << 5) + lane;
-    for (int a = warp >> lgW; a < TA; a += (kBtThreads / 32) >> lgW) {
-      const uint32_t s0 = s_runpre[a], n = s_runpre[a + 1] - s0;
-      const uint32_t o = s_ost[a];
-#pragma unroll 2
-      for (uint32_t j = g0; j < n; j += gw) {
-        keys_out[o + j] = sK[s0 + j];
-        if (VALS) vals_out[o + j] = sV[s0 + j];
-        if (perm_out) perm_out[o + j] = sP[s0 + j];
+  const int lgW = lgTB >= kBtLgWarps ? 0 : kBtLgWarps - lgTB;
+  const uint32_t gw = 32u << lgW, g0 = ((warp & ((1 << lgW) - 1)) << 5) + lane;
+  for (int b = warp >> lgW; b < TB; b += (kBtThreads / 32) >> lgW) {
+    const uint32_t len = s_rowlen[b];
+    const uint32_t rs = s_rs[b];
+    const uint64_t id0 = base + (b0 + b) * strideB + a0;
+    const uint32_t* dl = s_cnt + (b << lgTA);
+    for (uint32_t r0 = 0; r0 < len; r0 += gw * kBtU) {
+      uint64_t k[kBtU];
+      double v[kBtU];
+      uint32_t blk[kBtU];
+#pragma unroll
+      for (int u = 0; u < kBtU; ++u) {
+        const uint32_t r = r0 + g0 + u * gw;
+        k[u] = r < len ? __ldcs(keys_in + rs + r) : 0ull;
+        if (VALS) v[u] = r < len ? __ldcs(vals_in + rs + r) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kBtU; ++u) blk[u] = (uint32_t)(fdiv(fF, k[u]) - id0);
+      reencode_keys<kBtU>(kp, k);
+#pragma unroll
+      for (int u = 0; u < kBtU; ++u) {
+        const uint32_t r = r0 + g0 + u * gw;
+        if (r >= len) continue;
+        const uint32_t d = r + dl[blk[u]];
+        keys_out[d] = k[u];
+        if (VALS) vals_out[d] = v[u];
+        if (perm_out) perm_out[d] = idx_in ? __ldg(idx_in + rs + r) : rs + r;
       }
     }
   }
@@ -366,7 +412,7 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   g.ntA = (uint32_t)ntA;
   g.ntB = (uint32_t)ntB;
   g.mid = (uint32_t)bg.mid;
-  const size_t smem = (size_t)kBtCap * 20;
+  const size_t smem = (size_t)kBtCap * 17;
   if (L.mark) L.mark(L.ctx, "k_block_tiles");
   if (io.vals_out) {
     static bool attr = false;

@@ -28,11 +28,22 @@ def _np_u64(t):
         t.detach().cpu().numpy().astype(np.uint64)
 
 
+def _dev(a, dev, shift):
+    """Device copy of a; shift=1 puts it one element into a larger buffer (8-byte but not
+    16-byte aligned data pointer)."""
+    t = torch.as_tensor(a)
+    if not shift:
+        return t.to(dev)
+    buf = torch.empty(len(t) + 1, dtype=t.dtype, device=dev)
+    buf[1:] = t.to(dev)
+    return buf[1:]
+
+
 def check(dims, perm, keys, vals, idx=None, sort=False, dev="cuda:0", return_perm=True,
-          hierarchical=False):
+          hierarchical=False, shift=0):
     """Run the CUDA path and the oracle on the same inputs; compare bit-exactly."""
-    k = torch.as_tensor(np.asarray(keys, dtype=np.uint64).view(np.int64)).to(dev)
-    v = None if vals is None else torch.as_tensor(np.asarray(vals, dtype=np.float64)).to(dev)
+    k = _dev(np.asarray(keys, dtype=np.uint64).view(np.int64), dev, shift)
+    v = None if vals is None else _dev(np.asarray(vals, dtype=np.float64), dev, shift)
     ix = None if idx is None else torch.as_tensor(np.asarray(idx, dtype=np.uint32).view(np.int32)).to(dev)
     p = lco.plan(dims, perm, hierarchical=hierarchical)
     fn = p.sort if sort else p.permute
@@ -610,6 +621,7 @@ def test_block_path(dims, perm, cuda_device):
     check(dims, perm, keys, None, return_perm=False)
     idx = rng.permutation(len(keys)).astype(np.uint32)
     check(dims, perm, keys, vals, idx=idx)
+    check(dims, perm, keys, vals, shift=1)  # inputs not 16-byte aligned: no TMA row copies
     w = workloads.config("C4", scale=300)
     assert lco.plan(w.dims, w.perms[0]).info(w.keys.numel())["path"] == "block"
     check(w.dims, w.perms[0], _np_u64(w.keys), w.vals.numpy())
