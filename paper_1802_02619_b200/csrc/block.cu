@@ -10,8 +10,9 @@
 // data is "already sorted").  The permutation is then a transpose of a ragged grid of
 // runs, with no sorting at all:
 //   k_block_bounds    run starts / ends of the blocks present (one read of the keys);
-//   k_block_counts    counts moved to the blocks' NEW-order ids (a dense grid transpose);
-//   k_scan_tiles x2   exclusive scan of the counts in new order -> output starts;
+//   k_block_counts    counts moved to the blocks' NEW-order ids (a tiled grid transpose)
+//                     and the sums of the scan tiles;
+//   k_scan_tiles      exclusive scan of the counts in new order -> output starts;
 //   k_block_tiles     a tiled transpose of the runs: per tile of blocks, long input runs
 //                     -> LIV shuffle -> shared memory in output order -> long output
 //                     runs (K', V, position).
@@ -81,55 +82,41 @@ __global__ void __launch_bounds__(256) k_block_bounds(uint64_t nnz, const uint64
   }
 }
 
-__global__ void k_block_counts(uint64_t nblocks, const __grid_constant__ KeyPlan kb,
-                               const uint32_t* __restrict__ bstart,
-                               const uint32_t* __restrict__ bend, uint32_t* __restrict__ cnew) {
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks; b += stride)
-    cnew[reencode(kb, b)] = __ldg(bend + b) - __ldg(bstart + b);
-}
-
-// Tile sums (SUMS) / tile-local exclusive scan plus the tile's offset (!SUMS), in place.
-template <bool SUMS>
+// Exclusive scan of the new-order counts, in place, plus the tile's offset: one tile of
+// kBkTile counts per CTA, 512 per warp read lane-consecutively (coalesced), warp scans
+// with a running carry.
 __global__ void __launch_bounds__(256) k_scan_tiles(uint64_t n, uint32_t* __restrict__ a,
-                                                    uint32_t* __restrict__ sums,
                                                     const uint64_t* __restrict__ toff) {
-  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_warp[8];
   constexpr int PER = kBkTile / 256;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t base = (uint64_t)blockIdx.x * kBkTile + (uint64_t)tid * PER;
-  uint32_t v[PER], sum = 0;
+  const uint64_t wbase = (uint64_t)blockIdx.x * kBkTile + (uint64_t)warp * 32 * PER;
+  uint32_t v[PER], carry = 0;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    v[i] = base + i < n ? a[base + i] : 0u;
-    sum += v[i];
+    const uint64_t x = wbase + i * 32 + lane;
+    v[i] = x < n ? a[x] : 0u;
   }
-  uint32_t incl = sum;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const uint32_t w = lane < 8 ? s_warp[lane] : 0u;
-    uint32_t wi = w;
+  for (int i = 0; i < PER; ++i) {
+    uint32_t incl = v[i];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += y;
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
     }
-    if (lane < 8) s_warp[lane] = wi - w;
-    if (SUMS && lane == 7) sums[blockIdx.x] = wi;
+    const uint32_t ex = carry + incl - v[i];
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+    v[i] = ex;
   }
+  if (lane == 0) s_warp[warp] = carry;
   __syncthreads();
-  if (SUMS) return;
-  uint32_t run = (uint32_t)toff[blockIdx.x] + s_warp[warp] + incl - sum;
+  uint32_t off = (uint32_t)toff[blockIdx.x];
+  for (int w = 0; w < warp; ++w) off += s_warp[w];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    if (base + i < n) a[base + i] = run;
-    run += v[i];
+    const uint64_t x = wbase + i * 32 + lane;
+    if (x < n) a[x] = off + v[i];
   }
 }
 
@@ -174,6 +161,50 @@ __device__ __forceinline__ uint64_t tile_base(const BlockTiling& g, uint32_t t, 
   *a0 = (uint64_t)aT << g.lgTA;
   // old block id at c_B = c_A = 0
   return ((uint64_t)(t / g.mid) * g.dB * g.mid + t % g.mid) * g.dA;
+}
+
+// Block counts moved to NEW-order positions: a 32 x 32 (A x B) tile transpose through
+// shared memory (reads along the old-innermost mode A, writes along the new-innermost
+// mode B, both coalesced), plus each scan tile's sum (atomics per written run).
+__global__ void __launch_bounds__(256) k_block_counts(const __grid_constant__ BlockTiling g,
+                                                      const __grid_constant__ KeyPlan kb,
+                                                      const uint32_t* __restrict__ bstart,
+                                                      const uint32_t* __restrict__ bend,
+                                                      uint32_t* __restrict__ cnew,
+                                                      uint32_t* __restrict__ sums) {
+  __shared__ uint32_t t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
+  uint64_t b0, a0;
+  const uint64_t base = tile_base(g, blockIdx.x, &b0, &a0);
+  const uint64_t strideB = (uint64_t)g.mid * g.dA;
+  // new id of (b0, a0 + r) = nid0 + r * sA (the new stride of mode A)
+  const uint64_t nid0 = reencode(kb, base + b0 * strideB + a0);
+  const uint64_t sA = a0 + 1 < g.dA ? reencode(kb, base + b0 * strideB + a0 + 1) - nid0 : 0;
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {  // r: B offset, tx: A offset
+    uint32_t c = 0;
+    if (b0 + r < g.dB && a0 + tx < g.dA) {
+      const uint64_t id = base + (b0 + r) * strideB + a0 + tx;
+      c = __ldg(bend + id) - __ldg(bstart + id);
+    }
+    t[r][tx] = c;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = ty; r < 32; r += 8) {  // r: A offset, tx: B offset
+    if (a0 + r >= g.dA) continue;  // warp-uniform
+    const uint64_t nid = nid0 + r * sA;
+    const bool ok = b0 + tx < g.dB;
+    const uint32_t c = ok ? t[tx][r] : 0u;
+    if (ok) cnew[nid + tx] = c;
+    // scan-tile sums: the run [nid, nid + 32) meets at most two scan tiles
+    const uint64_t tile0 = nid / kBkTile;
+    const bool second = (nid + tx) / kBkTile != tile0;
+    const uint32_t s0 = __reduce_add_sync(0xffffffffu, second ? 0u : c);
+    const uint32_t s1 = __reduce_add_sync(0xffffffffu, second ? c : 0u);
+    if (tx == 0 && s0) atomicAdd(sums + tile0, s0);
+    if (tx == 0 && s1) atomicAdd(sums + tile0 + 1, s1);
+  }
 }
 
 template <bool VALS>
@@ -377,20 +408,29 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   uint64_t* total = toff + nt;
   const FastDiv fF = make_fastdiv(F);
   if ((e = cudaMemsetAsync(bstart, 0, 2 * tb, L.stream)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(sums, 0, nt * 4, L.stream)) != cudaSuccess) return e;
   const unsigned gn = (unsigned)((nnz + 256 * kBkU - 1) / (256 * kBkU));  // 8 warps x 256
-  const unsigned gb = (unsigned)umin64((nblocks + 255) / 256, 148 * 16);
   if (L.mark) L.mark(L.ctx, "k_block_bounds");
   k_block_bounds<<<gn, 256, 0, L.stream>>>(nnz, io.keys_in, fF, bstart, bend);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // counts in new order (32 x 32 transpose tiles) and the scan-tile sums
+  BlockTiling gc;
+  gc.dA = bg.dA;
+  gc.dB = bg.dB;
+  gc.lgTA = gc.lgTB = 5;
+  const uint64_t ncA = (bg.dA + 31) >> 5, ncB = (bg.dB + 31) >> 5;
+  const uint64_t nct = ncA * ncB * bg.mid * bg.hi;
+  if (nct >= (1ull << 31)) return cudaErrorInvalidValue;
+  gc.ntA = (uint32_t)ncA;
+  gc.ntB = (uint32_t)ncB;
+  gc.mid = (uint32_t)bg.mid;
   if (L.mark) L.mark(L.ctx, "k_block_counts");
-  k_block_counts<<<gb, 256, 0, L.stream>>>(nblocks, kb, bstart, bend, cnew);
+  k_block_counts<<<(unsigned)nct, 256, 0, L.stream>>>(gc, kb, bstart, bend, cnew, sums);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (L.mark) L.mark(L.ctx, "k_block_scan");
-  k_scan_tiles<true><<<(unsigned)nt, 256, 0, L.stream>>>(nblocks, cnew, sums, nullptr);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = run_count_scan(sums, nt, toff, total, Launch{L.stream, nullptr, nullptr})) != cudaSuccess)
     return e;
-  k_scan_tiles<false><<<(unsigned)nt, 256, 0, L.stream>>>(nblocks, cnew, nullptr, toff);
+  k_scan_tiles<<<(unsigned)nt, 256, 0, L.stream>>>(nblocks, cnew, toff);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // tile shape: about kBtTarget expected nonzeros, at most 32 x 32 blocks and 256 in all,
   // the longer side along B (the output runs)
