@@ -142,7 +142,8 @@ constexpr int kBtCap = LCO_BT_CAP;  // staged nonzeros per tile: 17 B each
 #ifndef LCO_BT_U
 #define LCO_BT_U 2
 #endif
-constexpr int kBtU = LCO_BT_U;  // nonzeros per thread per round
+constexpr int kBtU = LCO_BT_U;  // nonzeros per thread per round (register path)
+constexpr int kBtWU = 4;        // nonzeros per thread per round (stage -> output)
 constexpr int kBtTarget = LCO_BT_TARGET;  // expected nonzeros per tile the host sizes tiles for
 
 struct BlockTiling {
@@ -221,8 +222,10 @@ __global__ void __launch_bounds__(kBtThreads, LCO_BT_MINB) k_block_tiles(
   double* sV = reinterpret_cast<double*>(sK + kBtCap);
   uint8_t* sB = reinterpret_cast<uint8_t*>(sV + kBtCap);
   __shared__ uint32_t s_cnt[kBtThreads], s_ipre[kBtThreads], s_opre[kBtThreads];  // TA * TB <= threads
-  __shared__ uint32_t s_rowlen[32], s_runlen[32], s_runpre[33], s_rowoff[33], s_rs[32], s_ost[32],
-      s_pdel[32];
+  __shared__ uint32_t s_rowlen[32], s_runlen[32], s_runpre[33], s_rowoff[33], s_rs[32], s_ost[32];
+  __shared__ uint64_t s_nid[32];  // new block id of (b0, a0 + a)
+  // per block (a, b): stage index - slot, input index - stage index, K' - K
+  __shared__ uint4 s_blk[kBtThreads];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lgTA = g.lgTA, lgTB = g.lgTB, TA = 1 << lgTA, TB = 1 << lgTB, nblk = TA * TB;
   // tile -> (hi, B tile, mid, A tile), B tiles fastest: consecutive CTAs extend the same
@@ -239,7 +242,11 @@ __global__ void __launch_bounds__(kBtThreads, LCO_BT_MINB) k_block_tiles(
       s = __ldg(bstart + id);
       c = __ldg(bend + id) - s;
       // the output start of run a = the new-order start of its first block (b = 0)
-      if (b == 0) s_ost[a] = __ldg(outstart + reencode(kb, id));
+      if (b == 0) {
+        const uint64_t nid = reencode(kb, id);
+        s_nid[a] = nid;
+        s_ost[a] = __ldg(outstart + nid);
+      }
     }
     uint32_t incl = c;
     for (int o = 1; o < TA; o <<= 1) {
@@ -306,8 +313,12 @@ __global__ void __launch_bounds__(kBtThreads, LCO_BT_MINB) k_block_tiles(
       const int b = tid >> lgTA, a = tid & (TA - 1);
       const uint32_t c = s_cnt[tid], first = s_runpre[a] + s_opre[(a << lgTB) + b];
       for (uint32_t w = 0; w < c; ++w) sB[first + w] = (uint8_t)b;
-      s_opre[(a << lgTB) + b] = s_rowoff[b] + s_ipre[tid] - first;  // stage index - slot
-      if (a == 0) s_pdel[b] = s_rs[b] - s_rowoff[b];               // input index - stage
+      // the free modes follow the block modes unchanged in both orders, so the LIV
+      // shuffle of a key of block (b, a) is K + (new id - old id) * F
+      const uint64_t oid = base + (b0 + b) * strideB + a0 + a;
+      const uint64_t kd = (s_nid[a] + b - oid) * fF.d;
+      s_blk[(a << lgTB) + b] = make_uint4(s_rowoff[b] + s_ipre[tid] - first, s_rs[b] - s_rowoff[b],
+                                          (uint32_t)kd, (uint32_t)(kd >> 32));
     }
     cp_async_wait<0>();
     __syncthreads();
@@ -317,29 +328,33 @@ __global__ void __launch_bounds__(kBtThreads, LCO_BT_MINB) k_block_tiles(
     const uint32_t gw = 32u << lgW, g0 = ((warp & ((1 << lgW) - 1)) << 5) + lane;
     for (int a = warp >> lgW; a < TA; a += (kBtThreads / 32) >> lgW) {
       const uint32_t s0 = s_runpre[a], n = s_runpre[a + 1] - s0, o = s_ost[a];
-      const uint32_t* so = s_opre + (a << lgTB);
-      for (uint32_t j0 = g0; j0 < n; j0 += gw * kBtU) {
-        uint64_t k[kBtU];
-        uint32_t src[kBtU];
+      const uint4* blk = s_blk + (a << lgTB);
+      for (uint32_t j0 = g0; j0 < n; j0 += gw * kBtWU) {
+        uint32_t bb[kBtWU];
+        uint4 r[kBtWU];
+        uint64_t k[kBtWU];
+        double v[kBtWU];
 #pragma unroll
-        for (int u = 0; u < kBtU; ++u) {
+        for (int u = 0; u < kBtWU; ++u) {
           const uint32_t j = j0 + u * gw;
-          src[u] = 0;
-          if (j < n) {
-            const uint32_t jj = s0 + j;
-            src[u] = jj + so[sB[jj]];
-          }
-          k[u] = sK[src[u]];
+          bb[u] = j < n ? sB[s0 + j] : 0u;
         }
-        reencode_keys<kBtU>(kp, k);
 #pragma unroll
-        for (int u = 0; u < kBtU; ++u) {
+        for (int u = 0; u < kBtWU; ++u) r[u] = blk[bb[u]];
+#pragma unroll
+        for (int u = 0; u < kBtWU; ++u) {
+          const uint32_t src = s0 + j0 + u * gw + r[u].x;
+          k[u] = sK[src] + (((uint64_t)r[u].w << 32) | r[u].z);
+          if (VALS) v[u] = sV[src];
+        }
+#pragma unroll
+        for (int u = 0; u < kBtWU; ++u) {
           const uint32_t j = j0 + u * gw;
           if (j >= n) continue;
           keys_out[o + j] = k[u];
-          if (VALS) vals_out[o + j] = sV[src[u]];
+          if (VALS) vals_out[o + j] = v[u];
           if (perm_out) {
-            const uint32_t p = src[u] + s_pdel[sB[s0 + j]];
+            const uint32_t p = s0 + j + r[u].x + r[u].y;
             perm_out[o + j] = idx_in ? __ldg(idx_in + p) : p;
           }
         }
