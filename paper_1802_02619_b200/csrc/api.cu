@@ -160,7 +160,7 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
   // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
   // and with a clear modelled win.
-  if (op.segments == 1 && mcost < 0.75 * c.cost) {
+  if ((op.segments == 1 && mcost < 0.9 * c.cost) || getenv("LCO_MSD")) {
     c.path = kPathMsd;
     c.msd = m;
     c.cost = mcost;

@@ -101,7 +101,7 @@ def test_baseline_config_plans():
     schedule chosen at the config's nnz."""
     cases = {
         ("C1", (64, 48, 32), (2, 0, 1), 5000): (5, "leaf"),
-        ("C2a", (512,) * 4, (2, 3, 0, 1), 1308672): (18, "lsd"),
+        ("C2a", (512,) * 4, (2, 3, 0, 1), 1308672): (18, "msd"),
         ("C2b", (512,) * 4, (0, 2, 1, 3), 1308672): (18, "tile"),
         ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2), 14581760): (21, "lsd"),
         ("C3b", (128,) * 6, (0, 3, 1, 4, 2, 5), 14581760): (28, "lsd"),
