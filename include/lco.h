@@ -184,7 +184,8 @@ typedef struct lco_plan_info {
   int msd_levels;                      /* path 3: MSD passes before the leaves */
   int leaf_bits;                       /* paths 2/3: bits of q the leaf sorts handle */
   int leaf_kind;                       /* paths 2/3: 1 one warp per leaf (<= 384 nonzeros),
-                                          2 one CTA per leaf (<= 8192 nonzeros) */
+                                          2 one CTA per leaf (<= 8192 nonzeros), 3 one
+                                          cluster of 8 CTAs per leaf (<= 65536, DSMEM) */
   double model_bytes;                  /* modelled HBM bytes per nonzero of the plan */
   int stages;                          /* permute: stages of the hierarchical plan (one per
                                           maximal run of rearrangement indices, PAPER.md:

@@ -141,6 +141,17 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     m.cta = (nnz >> m.b1) > wt;
     m.staged = m.cta && (nnz >> m.b1) <= st;
     mcost = 8 + 36 + 40;
+  } else if ((nnz >> 8) <= cluster_leaf_cap() * 15 / 16 && B - 8 <= 35 && B - 8 >= 4 &&
+             getenv("LCO_CLUSTER")) {
+    // one 8-bit MSD pass, then every bucket (up to ~60K nonzeros) sorted inside a
+    // cluster of CTAs (k_leafx): the second digit moves over DSMEM, not through HBM
+    // (opt-in: measured slower than two LSD passes on C3a, msd.cu)
+    m.levels = 1;
+    m.b1 = 8;
+    m.b2 = 0;
+    m.cta = 1;
+    m.cluster = 1;
+    mcost = 8 + 36 + 40;
   } else {
     m.levels = 2;
     m.b1 = 8;
@@ -845,7 +856,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   info->msd_levels = cp.msd.levels;
   info->leaf_bits = cp.path == kPathMsd || cp.path == kPathLocal ? cp.msd.rb : 0;
   info->leaf_kind = (cp.path == kPathLocal || cp.path == kPathTile) ? 2
-                                                                     : (cp.path == kPathMsd ? (cp.msd.cta ? 2 : 1) : 0);
+                                                                     : (cp.path == kPathMsd ? (cp.msd.cluster ? 3 : (cp.msd.cta ? 2 : 1)) : 0);
   if (cp.path == kPathTile) info->leaf_bits = cp.msd.rb;
   info->model_bytes = cp.cost;
   info->flat_model_bytes = cp.cost;

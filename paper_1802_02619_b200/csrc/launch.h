@@ -57,6 +57,7 @@ struct MsdPlan {
   int rb;
   int cta;     // leaves sorted by one CTA per leaf instead of k_leafw (one warp)
   int staged;  // CTA leaves of <= ~2K nonzeros: the fully staged k_leafs
+  int cluster; // one-level plans: buckets sorted by a CTA cluster in DSMEM (k_leafx)
 };
 
 struct PassParams;
@@ -64,6 +65,7 @@ struct ScatterIO;
 
 uint64_t pass_tiles(uint64_t nnz);
 uint32_t prefetch_distance();  // L2 prefetch distance of the pass kernels (tiles)
+uint32_t cluster_leaf_cap();   // largest level-1 bucket a k_leafx cluster sorts
 int pass_tile();
 int pass_rb(int bits);
 size_t pass_ctrl_bytes(int rb, uint64_t nnz);

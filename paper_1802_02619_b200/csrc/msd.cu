@@ -17,6 +17,7 @@
 //             through global scratch.
 // Buckets keep their position ranges from level to level (the paper's "regions"), so
 // every leaf writes its final outputs in place.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -1247,6 +1248,256 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------------
+// k_leafx: one level-1 bucket (up to kXCS * kXChunk nonzeros, ~57K at C3a) per thread-
+// block cluster of kXCS CTAs, sorted in the cluster's distributed shared memory instead
+// of a second pass through HBM (the paper's recursion into regions, with
+// the next digit exchanged over DSMEM):
+//   1. CTA r reads the keys of its chunk of the bucket (K' only) and records (the bits
+//      of q below the bucket digit, position in the bucket); the top 3 of those bits
+//      choose the destination CTA;
+//   2. digit counts are exchanged through DSMEM; every record is stored straight into
+//      its destination CTA's shared memory;
+//   3. each CTA sorts its records on (key, position) -- unique, so the result is the
+//      stable order -- by buckets of the key's top bits plus comparisons
+//      inside a bucket, as k_leafs;
+//   4. it writes its slice of the bucket contiguously, gathering K', V and the source
+//      position of each record from buffer A (L2: the bucket was read moments before).
+// Buckets that do not fit, or whose records crowd a CTA or a key bucket, are deferred
+// whole (a cluster-uniform decision) to the block-level kernel.
+// Opt-in (LCO_CLUSTER=1): measured on C3a 0.69 ms vs 0.66 ms for two LSD passes; the
+// phases take 138 us (load + DSMEM exchange), 144 us (local sorts, latency-bound at two
+// CTAs per SM) and 189 us (the final gathers of K', V and position from L2 are 8-byte
+// random reads that waste 3/4 of every sector) -- DESIGN.md §12.
+// ---------------------------------------------------------------------------------
+#ifndef LCO_XLG
+#define LCO_XLG 4
+#endif
+constexpr int kXLg = LCO_XLG;                    // log2 CTAs per cluster
+constexpr int kXCS = 1 << kXLg;                  // 16: non-portable size, two CTAs per SM
+constexpr int kXThreads = 512;
+constexpr int kXChunk = 65536 >> kXLg;           // records sent per CTA (bucket <= 64K)
+constexpr int kXRecv = kXChunk * 3 / 2;          // records received per CTA
+constexpr int kXBBits = kXLg == 4 ? 12 : 13;     // local key buckets
+constexpr size_t kXSmem = (size_t)kXChunk * 8 + (size_t)kXRecv * 8 + ((size_t)1 << kXBBits) * 4;
+static_assert((size_t)kXRecv * 4 <= (size_t)kXChunk * 8, "X / F live in the send buffer");
+
+template <bool VALS>
+__global__ void __launch_bounds__(kXThreads, kXLg == 4 ? 2 : 1)
+    k_leafx(const __grid_constant__ LeafArgs L) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem[];
+  // [chunk] sent records (key, position | (destination | local rank << 3) << 16)
+  uint2* S = reinterpret_cast<uint2*>(smem);
+  uint2* Rv = S + kXChunk;                                     // [recv] (key, pos)
+  uint32_t* Bk = reinterpret_cast<uint32_t*>(Rv + kXRecv);    // [2^kXBBits] key buckets
+  uint16_t* X = reinterpret_cast<uint16_t*>(S);               // after the exchange
+  uint16_t* F = X + kXRecv;
+  __shared__ uint32_t s_hist[kXCS], s_all[kXCS * kXCS], s_tot[kXCS], s_off[kXCS], s_warp[32],
+      s_flag;
+  __shared__ unsigned long long s_min, s_max;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t r = cl.block_rank(), slot = blockIdx.x / kXCS;
+  LeafDesc d;
+  if (!leaf_at(L, 1, slot, &d)) return;  // uniform: empty bucket
+  const uint32_t n = d.n, start = d.start;
+  if (n > (uint32_t)(kXCS * kXChunk)) {
+    if (r == 0 && tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = (1u << 30) | slot;
+    return;
+  }
+  const bool want_pos = L.perm_out != nullptr;
+  const int rb = L.rb;  // bits of q below the bucket digit, 4..35
+  const uint64_t mask = rb >= 64 ? ~0ull : ((1ull << rb) - 1ull);
+  const int ds = rb - kXLg;  // destination = top kXLg of the rb bits
+  const uint32_t per = (n + kXCS - 1) / kXCS, c0 = min(n, r * per), c1 = min(n, c0 + per);
+  if (r == 0 && tid == 0) {  // the gathers of step 4 then hit L2
+    if (VALS) prefetch_l2(L.vA + start, (size_t)n * 8);
+    if (want_pos) prefetch_l2(L.pA + start, (size_t)n * 4);
+  }
+  if (tid < kXCS) s_hist[tid] = 0;
+  if (tid == 0) s_flag = 0;
+  __syncthreads();
+  // 1. the chunk's K' into the send buffer (cp.async), then in place into records;
+  //    local rank per destination (warp-aggregated)
+  uint64_t* SK = reinterpret_cast<uint64_t*>(S);
+  for (uint32_t i = c0 + tid; i < c1; i += kXThreads) cp_async8(SK + (i - c0), L.kA + (uint64_t)start + i);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  for (uint32_t i0 = c0; i0 < c1; i0 += kXThreads) {
+    const uint32_t i = i0 + tid;
+    const bool ok = i < c1;
+    const uint64_t key = ok ? leaf_key(L, SK[i - c0], mask) : 0ull;
+    const uint32_t dst = (uint32_t)(key >> ds);
+    const uint32_t peers = __match_any_sync(0xffffffffu, ok ? dst : 0xffffffffu);
+    const uint32_t leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (ok && lane == (int)leader) base = atomicAdd(&s_hist[dst], (uint32_t)__popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (ok) {
+      const uint32_t lr = base + __popc(peers & ((1u << lane) - 1u));
+      S[i - c0] = make_uint2((uint32_t)(key & ((1ull << ds) - 1ull)), i | ((dst | (lr << kXLg)) << 16));
+    }
+  }
+  cl.sync();
+  // 2. counts of every CTA -> where this CTA's records go, and every CTA's total
+  if (tid < kXCS * kXCS) s_all[tid] = *cl.map_shared_rank(&s_hist[tid & (kXCS - 1)], tid / kXCS);
+  __syncthreads();
+  if (tid < kXCS) {
+    uint32_t t = 0, o = 0;
+    for (uint32_t rr = 0; rr < (uint32_t)kXCS; ++rr) {
+      const uint32_t h = s_all[rr * kXCS + tid];
+      t += h;
+      o += rr < r ? h : 0u;
+    }
+    s_tot[tid] = t;
+    s_off[tid] = o;
+  }
+  __syncthreads();
+  bool crowded = false;
+  uint32_t m = 0, obase = start;
+  for (uint32_t q = 0; q < (uint32_t)kXCS; ++q) {
+    const uint32_t t = s_tot[q];
+    crowded |= t > (uint32_t)kXRecv;
+    if (q == r) m = t;
+    if (q < r) obase += t;
+  }
+  if (crowded) {  // uniform: every CTA sees the same totals
+    if (r == 0 && tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = (1u << 30) | slot;
+    cl.sync();  // s_hist stays readable until every CTA has read it
+    return;
+  }
+  for (uint32_t j = tid; j < c1 - c0; j += kXThreads) {
+    const uint2 rec = S[j];
+    const uint32_t lr = rec.y >> 16, q = lr & (kXCS - 1);
+    uint2* dstbuf = cl.map_shared_rank(Rv, q);
+    dstbuf[s_off[q] + (lr >> kXLg)] = make_uint2(rec.x, rec.y & 0xffffu);
+  }
+  cl.sync();  // every record delivered; S is free
+  // 3. sort this CTA's records on (key, position)
+  if (tid == 0) {
+    s_min = ~0ull;
+    s_max = 0ull;
+  }
+  const int lg = m > 1 ? 32 - __clz((int)(m - 1)) : 0;
+  const int tb = min(max(lg, 1), kXBBits);
+  const uint32_t nbk = 1u << tb;
+  for (uint32_t b = tid; b < nbk; b += kXThreads) Bk[b] = 0;
+  __syncthreads();
+  uint32_t mn = 0xffffffffu, mx = 0;
+  for (uint32_t j = tid; j < m; j += kXThreads) {
+    const uint32_t kk = Rv[j].x;
+    mn = kk < mn ? kk : mn;
+    mx = kk > mx ? kk : mx;
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0 && m) {
+    atomicMin(&s_min, (unsigned long long)mn);
+    atomicMax(&s_max, (unsigned long long)mx);
+  }
+  __syncthreads();
+  const uint32_t kmin = (uint32_t)s_min, range = m ? (uint32_t)(s_max - s_min) : 0u;
+  const int rbits = range ? 32 - __clz((int)range) : 0;
+  const int bshift = rbits > tb ? rbits - tb : 0;
+  for (uint32_t j = tid; j < m; j += kXThreads) atomicAdd(&Bk[(Rv[j].x - kmin) >> bshift], 1u);
+  __syncthreads();
+  block_scan_bins<kXThreads, (1 << kXBBits)>(Bk, Bk, s_warp);
+  for (uint32_t j = tid; j < m; j += kXThreads)
+    X[atomicAdd(&Bk[(Rv[j].x - kmin) >> bshift], 1u)] = (uint16_t)j;
+  __syncthreads();
+  bool big = false;
+  for (uint32_t p = tid; p < m; p += kXThreads) {
+    const uint16_t x = X[p];
+    const uint2 rx = Rv[x];
+    const uint32_t b = (rx.x - kmin) >> bshift;
+    const uint32_t lo = b ? Bk[b - 1] : 0u, hi = Bk[b];
+    if (hi - lo == 1u) {
+      F[lo] = x;
+      continue;
+    }
+    if (hi - lo > (uint32_t)kCBig) {
+      big = true;
+      continue;
+    }
+    uint32_t rk = lo;
+    for (uint32_t q = lo; q < hi; ++q) {
+      const uint2 ry = Rv[X[q]];
+      rk += (ry.x < rx.x || (ry.x == rx.x && ry.y < rx.y)) ? 1u : 0u;
+    }
+    F[rk] = x;
+  }
+  // a crowded key bucket anywhere defers the whole bucket: the flag is pushed to every
+  // CTA, so after the barrier each reads its own copy (no remote read can outlive a CTA)
+  big = __syncthreads_or(big);
+  if (big && tid < kXCS) atomicOr(cl.map_shared_rank(&s_flag, tid), 1u);
+  cl.sync();
+  if (s_flag) {
+    if (r == 0 && tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = (1u << 30) | slot;
+    return;
+  }
+  // 4. this CTA's slice of the bucket, in order (gathers batched for L2 parallelism)
+  constexpr int GU = 4;
+  for (uint32_t j0 = tid; j0 < m; j0 += kXThreads * GU) {
+    uint32_t src[GU];
+    uint64_t kk[GU];
+    double vv[GU];
+    uint32_t pp[GU];
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const uint32_t j = j0 + u * kXThreads;
+      src[u] = start + (j < m ? Rv[F[j]].y : 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      kk[u] = L.kA[src[u]];
+      if (VALS) vv[u] = L.vA[src[u]];
+      if (want_pos) pp[u] = L.pA[src[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < GU; ++u) {
+      const uint32_t j = j0 + u * kXThreads;
+      if (j >= m) continue;
+      const uint64_t g = (uint64_t)obase + j;
+      L.keys_out[g] = kk[u];
+      if (VALS) L.vals_out[g] = vv[u];
+      if (want_pos) L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pp[u]) : pp[u];
+    }
+  }
+}
+
+template <bool VALS>
+static cudaError_t launch_leafx_t(const LeafArgs& L, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_leafx<VALS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kXSmem);
+    if (e != cudaSuccess) return e;
+    if (kXCS > 8 && (e = cudaFuncSetAttribute(k_leafx<VALS>,
+                                              cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) !=
+                        cudaSuccess)
+      return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3((1u << L.b1) * kXCS);
+  cfg.blockDim = dim3(kXThreads);
+  cfg.dynamicSmemBytes = kXSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kXCS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_leafx<VALS>, L);
+}
+
+uint32_t cluster_leaf_cap() { return (uint32_t)(kXCS * kXChunk); }
+
+// ---------------------------------------------------------------------------------
 // Launchers
 // ---------------------------------------------------------------------------------
 template <int LB, bool VALS>
@@ -1710,7 +1961,10 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   LeafArgs L1 = L;
   L1.only_level = 1;
   L1.rb = mp.rb + (mp.levels == 2 ? mp.b2 : 0);
-  if (mp.cta) {
+  if (mp.cluster && mp.levels == 1) {
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_leafx");
+    e = vals ? launch_leafx_t<true>(L1, Lc.stream) : launch_leafx_t<false>(L1, Lc.stream);
+  } else if (mp.cta) {
     if (Lc.mark) Lc.mark(Lc.ctx, mp.levels == 2 ? "k_leaf_l1" : leafc_kernel(L1, false));
     e = launch_leafc(L1, vals, false, 1u << 30, Lc.stream);
   } else {

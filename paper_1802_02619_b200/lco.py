@@ -241,7 +241,7 @@ class Plan:
             "tile": pi.tile,
             "msd_levels": pi.msd_levels,
             "leaf_bits": pi.leaf_bits,
-            "leaf_kind": {0: None, 1: "warp", 2: "cta"}.get(pi.leaf_kind, pi.leaf_kind),
+            "leaf_kind": {0: None, 1: "warp", 2: "cta", 3: "cluster"}.get(pi.leaf_kind, pi.leaf_kind),
             "model_bytes": pi.model_bytes,
             "stages": pi.stages,
             "stage_paths": [PATHS.get(x, x) for x in pi.stage_path[:pi.stages]] if pi.stages > 1 else [],

@@ -424,6 +424,30 @@ def test_msd_leaf_variants(env, cuda_device, monkeypatch):
         check(dims, (1, 4, 0, 3, 2), keys, None)
 
 
+@pytest.mark.parametrize("dims,perm,nnz", [((4096, 4096, 16), (1, 0, 2), 3_000_000),
+                                           ((256,) * 4, (3, 2, 1, 0), 4_000_000),
+                                           ((3000, 3000, 50), (1, 0, 2), 5_000_000),
+                                           ((1 << 16, 4096), (1, 0), 3_000_000)])
+def test_cluster_leaves(dims, perm, nnz, cuda_device, monkeypatch):
+    """One 8-bit MSD pass, then every bucket sorted by a cluster of 16 CTAs in DSMEM
+    (k_leafx, opt-in): 4..16 remaining bits, a non-power-of-two middle, and (2^16 x 4096)
+    buckets whose ~700 nonzeros per key crowd one key bucket -> whole buckets deferred
+    to the block-level kernel; and C3a at full size."""
+    monkeypatch.setenv("LCO_CLUSTER", "1")
+    rng = np.random.default_rng(nnz + len(dims))
+    keys, vals = _rand_sorted(rng, dims, nnz)
+    info = lco.plan(dims, perm).info(len(keys))
+    assert info["path"] == "msd" and info["leaf_kind"] == "cluster", info
+    check(dims, perm, keys, vals)
+    check(dims, perm, keys, None, return_perm=False)
+    idx = rng.permutation(len(keys)).astype(np.uint32)
+    check(dims, perm, keys, vals, idx=idx)
+    if nnz == 3_000_000 and len(dims) == 3:
+        w = workloads.config("C3")
+        assert lco.plan(w.dims, w.perms[0]).info(w.keys.numel())["leaf_kind"] == "cluster"
+        check(w.dims, w.perms[0], _np_u64(w.keys), w.vals.numpy())
+
+
 # ------------------------------------------------------------------ segmented single pass
 @pytest.mark.parametrize("dims,perm,nnz", [((256, 16, 64, 32), (0, 2, 1, 3), 1_000_000),
                                            ((128, 16, 2048, 4), (0, 2, 1, 3), 1_000_000),
