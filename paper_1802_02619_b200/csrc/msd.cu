@@ -1165,31 +1165,38 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
     for (uint32_t b = tid; b < nbk; b += kSThreads) B[b] = 0;
     cp_async_wait<0>();
     __syncthreads();
-    uint64_t mn = ~0ull, mx = 0ull;
-    for (uint32_t i = tid; i < n; i += kSThreads) {
-      const uint64_t kk = leaf_key(L, K[i], mask);
-      mn = kk < mn ? kk : mn;
-      mx = kk > mx ? kk : mx;
-    }
+    // keys of <= 32 remaining bits are used as they are (the MSD levels leave uniform
+    // keys spread over the whole range); wider ones relative to the leaf's minimum
+    uint64_t kmin = 0;
+    int rbits = L.rb;
+    if (L.rb > 32) {
+      uint64_t mn = ~0ull, mx = 0ull;
+      for (uint32_t i = tid; i < n; i += kSThreads) {
+        const uint64_t kk = leaf_key(L, K[i], mask);
+        mn = kk < mn ? kk : mn;
+        mx = kk > mx ? kk : mx;
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o);
-      const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
-      mn = a < mn ? a : mn;
-      mx = b > mx ? b : mx;
-    }
-    if (lane == 0) {
-      atomicMin(&s_min, (unsigned long long)mn);
-      atomicMax(&s_max, (unsigned long long)mx);
-    }
-    __syncthreads();
-    const uint64_t kmin = s_min, range = s_max - s_min;
-    const int rbits = range ? 64 - __clzll((long long)range) : 0;
-    if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
-      k += gridDim.x;
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o);
+        const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+      }
+      if (lane == 0) {
+        atomicMin(&s_min, (unsigned long long)mn);
+        atomicMax(&s_max, (unsigned long long)mx);
+      }
       __syncthreads();
-      continue;
+      kmin = s_min;
+      const uint64_t range = s_max - s_min;
+      rbits = range ? 64 - __clzll((long long)range) : 0;
+      if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+        k += gridDim.x;
+        __syncthreads();
+        continue;
+      }
     }
     const int bshift = rbits > tb ? rbits - tb : 0;
     for (uint32_t i = tid; i < n; i += kSThreads) {
