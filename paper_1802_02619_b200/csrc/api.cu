@@ -171,7 +171,9 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
   // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
   // and with a clear modelled win.
-  if ((op.segments == 1 && mcost < 0.9 * c.cost) || getenv("LCO_MSD")) {
+  // (one level: below 0.9 of the LSD model, C2a 0.105 vs 0.127 ms; two levels: below
+  // 0.75 -- structured tensors (Table 2's Laplacian) fill two-level buckets unevenly)
+  if ((op.segments == 1 && mcost < (m.levels == 1 ? 0.9 : 0.75) * c.cost) || getenv("LCO_MSD")) {
     c.path = kPathMsd;
     c.msd = m;
     c.cost = mcost;

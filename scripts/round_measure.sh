@@ -21,7 +21,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --csv --log-file gpurun_out/m_c4_launches.csv python bench.py --config C4 --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_launch4.log 2>&1
 echo "c4 launches rc=$?"
 python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain4b.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_count" -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:"k_block_tiles|k_block_bounds" -s 2 -c 2 \
     -o gpurun_out/m_c4_full -f python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_c4.log 2>&1
 echo "c4 full rc=$?"
 python benchmarks/table2.py --reps 5 --out gpurun_out/m_table2.md > gpurun_out/m_table2.log 2>&1; echo "table2 rc=$?"
