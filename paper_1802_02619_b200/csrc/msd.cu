@@ -61,15 +61,27 @@ __global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__
     tfirst[b] = off[b];
     tcnt[b] = nt;
   }
-  if (b == 1023) *ntiles = off[1023] + nt;
-  const uint32_t start = b < nb1 ? bucket1[b] : 0u;
-  for (uint32_t j = 0; j < nt; ++j) {
+  __shared__ uint32_t s_start[1024], s_size[1024];
+  s_start[b] = b < nb1 ? bucket1[b] : 0u;
+  s_size[b] = size;
+  if (b == 1023) cnt[0] = off[1023] + nt;  // cnt is free after the scan
+  __syncthreads();
+  const uint32_t total = cnt[0];
+  if (b == 0) *ntiles = total;
+  // all threads write the table in order (coalesced): tile t belongs to the last bucket
+  // whose first tile is <= t (buckets without tiles share their successor's offset)
+  for (uint32_t t = b; t < total; t += 1024) {
+    int x = 0;
+#pragma unroll
+    for (int st = 512; st > 0; st >>= 1)
+      if (off[x + st] <= t) x += st;
+    const uint32_t j = t - off[x];
     TileEntry e;
-    e.start = start + j * kTile;
-    e.n = min((uint32_t)kTile, size - j * kTile);
-    e.seg = b;
+    e.start = s_start[x] + j * kTile;
+    e.n = min((uint32_t)kTile, s_size[x] - j * kTile);
+    e.seg = x;
     e.pad = 0;
-    ttab[off[b] + j] = e;
+    ttab[t] = e;
   }
 }
 
