@@ -132,6 +132,45 @@ struct PassParams {
   uint32_t pf_dist;           // L2 prefetch distance in tiles (resident CTAs), 0 = off
 };
 
+// PER consecutive uint16 tile-histogram entries in, PER uint32 offsets out (vector
+// loads / stores of one row slice; used by the offset kernels).
+template <int PER>
+struct RowVec;
+template <>
+struct RowVec<8> {
+  __device__ static void load(const uint16_t* p, uint32_t (&h)[8]) {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      h[2 * i] = w[i] & 0xFFFFu;
+      h[2 * i + 1] = w[i] >> 16;
+    }
+  }
+  __device__ static void store(uint32_t* p, const uint32_t (&r)[8]) {
+    reinterpret_cast<uint4*>(p)[0] = make_uint4(r[0], r[1], r[2], r[3]);
+    reinterpret_cast<uint4*>(p)[1] = make_uint4(r[4], r[5], r[6], r[7]);
+  }
+};
+template <>
+struct RowVec<4> {
+  __device__ static void load(const uint16_t* p, uint32_t (&h)[4]) {
+    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(p));
+    h[0] = v.x & 0xFFFFu;
+    h[1] = v.x >> 16;
+    h[2] = v.y & 0xFFFFu;
+    h[3] = v.y >> 16;
+  }
+  __device__ static void store(uint32_t* p, const uint32_t (&r)[4]) {
+    reinterpret_cast<uint4*>(p)[0] = make_uint4(r[0], r[1], r[2], r[3]);
+  }
+};
+template <>
+struct RowVec<1> {
+  __device__ static void load(const uint16_t* p, uint32_t (&h)[1]) { h[0] = __ldcg(p); }
+  __device__ static void store(uint32_t* p, const uint32_t (&r)[1]) { p[0] = r[0]; }
+};
+
 // Shaved key q = K' div T.
 __device__ __forceinline__ uint64_t q_of(const PassParams& a, uint64_t k2) {
   return a.qshift >= 0 ? (k2 >> a.qshift) : fdiv(a.kp.divT, k2);

@@ -108,13 +108,30 @@ __global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __rest
   __syncthreads();
   block_scan_bins<kThreads, BINS>(tot, ex, s_warp);
   const uint32_t t0 = tfirst[b], start = bucket1[b];
-  for (int d = threadIdx.x; d < BINS; d += kThreads) {
-    uint32_t run = start + ex[d];
-    base2[(size_t)b * BINS + d] = run;
-    for (uint32_t j = 0; j < nt; ++j) {
-      const size_t o = (size_t)(t0 + j) * BINS + d;
-      toff[o] = run;
-      run += thist[o];
+  // each thread owns PER consecutive digits: vector loads of the tile-histogram rows,
+  // U rows in flight
+  constexpr int PER = BINS >= kThreads ? BINS / kThreads : 1;
+  constexpr int U = 4;
+  const int d0 = threadIdx.x * PER;
+  if (d0 >= BINS) return;
+  uint32_t run[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    run[i] = start + ex[d0 + i];
+    base2[(size_t)b * BINS + d0 + i] = run[i];
+  }
+  for (uint32_t j = 0; j < nt; j += U) {
+    uint32_t h[U][PER];
+#pragma unroll
+    for (int r = 0; r < U; ++r)
+      if (j + r < nt) RowVec<PER>::load(thist + (size_t)(t0 + j + r) * BINS + d0, h[r]);
+#pragma unroll
+    for (int r = 0; r < U; ++r) {
+      if (j + r < nt) {
+        RowVec<PER>::store(toff + (size_t)(t0 + j + r) * BINS + d0, run);
+#pragma unroll
+        for (int i = 0; i < PER; ++i) run[i] += h[r][i];
+      }
     }
   }
 }
