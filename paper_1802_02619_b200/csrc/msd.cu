@@ -1146,8 +1146,8 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
 // ---------------------------------------------------------------------------------
 constexpr int kSCap = 2304;
 constexpr int kSThreads = 256;
-constexpr int kSBucketBits = 11;
-constexpr size_t kSSmem = (size_t)kSCap * (8 + 8 + 4 + 4 + 2 + 2) + ((size_t)1 << kSBucketBits) * 4;
+constexpr int kSBucketBits = 12;  // 4,096 buckets (~0.5 nonzero each), u16 counts packed in pairs
+constexpr size_t kSSmem = (size_t)kSCap * (8 + 8 + 4 + 4 + 2 + 2) + ((size_t)1 << kSBucketBits) * 2;
 
 template <bool VALS>
 __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ LeafArgs L) {
@@ -1189,9 +1189,8 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       s_big = 0;
     }
     const int lg = n > 1 ? 32 - __clz((int)(n - 1)) : 0;  // ceil(log2 n)
-    const int tb = min(max(lg, 1), kSBucketBits);          // ~1 nonzero per bucket
-    const uint32_t nbk = 1u << tb;
-    for (uint32_t b = tid; b < nbk; b += kSThreads) B[b] = 0;
+    const int tb = min(lg + 1, kSBucketBits);               // ~0.5 nonzero per bucket
+    for (uint32_t b = tid; b < (1u << kSBucketBits) / 2; b += kSThreads) B[b] = 0;
     cp_async_wait<0>();
     __syncthreads();
     // keys of <= 32 remaining bits are used as they are (the MSD levels leave uniform
@@ -1228,22 +1227,57 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       }
     }
     const int bshift = rbits > tb ? rbits - tb : 0;
+    // bucket b's u16 count / start lives in half (b & 1) of word b >> 1 (no carries: every
+    // value is <= n <= kSCap)
     for (uint32_t i = tid; i < n; i += kSThreads) {
       const uint32_t rel = (uint32_t)(leaf_key(L, K[i], mask) - kmin);
       R[i] = rel;
-      atomicAdd(&B[rel >> bshift], 1u);
+      const uint32_t bk = rel >> bshift;
+      atomicAdd(&B[bk >> 1], 1u << ((bk & 1u) << 4));
     }
     __syncthreads();
-    block_scan_bins<kSThreads, (1 << kSBucketBits)>(B, B, s_warp);  // nbk <= 2^11; rest 0
-    for (uint32_t i = tid; i < n; i += kSThreads) X[atomicAdd(&B[R[i] >> bshift], 1u)] = (uint16_t)i;
+    {  // exclusive scan of the 4,096 packed counts: 16 per thread, then warps, then block
+      constexpr int PW = (1 << kSBucketBits) / 2 / kSThreads;  // words per thread
+      uint32_t c[2 * PW], tsum = 0;
+#pragma unroll
+      for (int i = 0; i < PW; ++i) {
+        const uint32_t w = B[tid * PW + i];
+        c[2 * i] = w & 0xFFFFu;
+        c[2 * i + 1] = w >> 16;
+        tsum += c[2 * i] + c[2 * i + 1];
+      }
+      uint32_t incl = tsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) s_warp[warp] = incl;
+      __syncthreads();
+      uint32_t run = incl - tsum;
+      for (int w = 0; w < warp; ++w) run += s_warp[w];
+#pragma unroll
+      for (int i = 0; i < PW; ++i) {
+        const uint32_t lo = run;
+        run += c[2 * i];
+        B[tid * PW + i] = lo | (run << 16);
+        run += c[2 * i + 1];
+      }
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kSThreads) {
+      const uint32_t bk = R[i] >> bshift, sh = (bk & 1u) << 4;
+      X[(atomicAdd(&B[bk >> 1], 1u << sh) >> sh) & 0xFFFFu] = (uint16_t)i;
+    }
     __syncthreads();
     // B[b] is now the end of bucket b
+    auto bend16 = [&](uint32_t b) { return (B[b >> 1] >> ((b & 1u) << 4)) & 0xFFFFu; };
     bool big = false;
     for (uint32_t p = tid; p < n; p += kSThreads) {
       const uint16_t x = X[p];
       const uint32_t kx = R[x];
       const uint32_t b = kx >> bshift;
-      const uint32_t lo = b ? B[b - 1] : 0u, hi = B[b];
+      const uint32_t lo = b ? bend16(b - 1) : 0u, hi = bend16(b);
       if (hi - lo == 1u) {  // the common case: alone in its bucket
         F[lo] = x;
         continue;
