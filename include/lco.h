@@ -185,7 +185,7 @@ typedef struct lco_plan_info {
   int leaf_bits;                       /* paths 2/3: bits of q the leaf sorts handle */
   int leaf_kind;                       /* paths 2/3: 1 one warp per leaf (<= 384 nonzeros),
                                           2 one CTA per leaf (<= 8192 nonzeros), 3 one
-                                          cluster of 8 CTAs per leaf (<= 65536, DSMEM) */
+                                          cluster of 16 CTAs per leaf (<= 65536, DSMEM) */
   double model_bytes;                  /* modelled HBM bytes per nonzero of the plan */
   int stages;                          /* permute: stages of the hierarchical plan (one per
                                           maximal run of rearrangement indices, PAPER.md:
@@ -193,6 +193,10 @@ typedef struct lco_plan_info {
   int stage_path[8];                   /* path of each stage (0-5 as above) */
   int stage_sort_bits[8];              /* bits of q each stage sorts */
   double flat_model_bytes;             /* modelled bytes of the flat plan */
+  uint64_t block_grid[5];              /* path 7: blocks (runs of constant old modes 0..k),
+                                          dims of the old-innermost block mode A and of the
+                                          new-innermost block mode B, products of the block
+                                          modes between B and A and before B; else 0 */
 } lco_plan_info;
 LCO_API lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* info);
 

@@ -862,6 +862,13 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   if (cp.path == kPathTile) info->leaf_bits = cp.msd.rb;
   info->model_bytes = cp.cost;
   info->flat_model_bytes = cp.cost;
+  if (cp.path == kPathBlock) {
+    info->block_grid[0] = cp.nblocks;
+    info->block_grid[1] = cp.bg.dA;
+    info->block_grid[2] = cp.bg.dB;
+    info->block_grid[3] = cp.bg.mid;
+    info->block_grid[4] = cp.bg.hi;
+  }
   const Hier hp = hier_for(h, sort != 0, nnz);
   info->stages = sort ? 1 : (h->nstages >= 2 ? h->nstages : 1);
   for (int j = 0; j < h->nstages && j < 8 && !sort; ++j) {

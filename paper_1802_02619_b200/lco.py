@@ -71,6 +71,7 @@ class PlanInfo(ctypes.Structure):
         ("stage_path", ctypes.c_int * 8),
         ("stage_sort_bits", ctypes.c_int * 8),
         ("flat_model_bytes", ctypes.c_double),
+        ("block_grid", ctypes.c_uint64 * 5),
     ]
 
 
@@ -247,6 +248,7 @@ class Plan:
             "stage_paths": [PATHS.get(x, x) for x in pi.stage_path[:pi.stages]] if pi.stages > 1 else [],
             "stage_sort_bits": list(pi.stage_sort_bits[:pi.stages]) if pi.stages > 1 else [],
             "flat_model_bytes": pi.flat_model_bytes,
+            "block_grid": list(pi.block_grid) if pi.path == 7 else None,
         }
 
     # ---------------------------------------------------------------- device calls

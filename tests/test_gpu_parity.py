@@ -630,7 +630,8 @@ def test_flatten_to_csc_and_roundtrip(cuda_device):
                                        ((50, 60, 7, 90), (1, 0, 2, 3)),
                                        ((16, 8, 12, 10, 200), (1, 2, 0, 3, 4)),
                                        ((5, 6, 1 << 20), (1, 0, 2)),
-                                       ((3, 700, 9, 400), (0, 2, 1, 3))])
+                                       ((3, 700, 9, 400), (0, 2, 1, 3)),
+                                       ((20, 30, 40, 500), (2, 1, 0, 3))])
 def test_block_path(dims, perm, cuda_device):
     """Permutations whose rearranged modes lie in a small old-order prefix: a transpose of
     runs without sorting (run bounds, block counts in new order, scan, one tiled copy) -

@@ -254,3 +254,29 @@ def test_new_entry_points_reject_bad_arguments_before_any_launch():
     assert n_st.value == 1
     # the MDT table rejects unknown classes
     assert lib.lco_mdt_choice(4, 0) == -1 and lib.lco_mdt_name(-1) == b"invalid"
+
+
+def test_block_grid_decomposition():
+    """Block transpose (path 7): blocks = runs of constant old modes 0..k (k = last old
+    position of a prefix / middle mode) of the NORMALIZED plan; A = old mode k, B = the new
+    order's innermost block mode, the tiles span (B, A) with the block modes before B /
+    between B and A fixed (hand-derived values; their product is the block count)."""
+    cases = {
+        ((2048,) * 4, (1, 0, 2, 3), 54_484_996): [2048 * 2048, 2048, 2048, 1, 1],
+        # modes 1, 2 fuse: (16, 96, 2000) with perm (1, 0, 2)
+        ((16, 8, 12, 10, 200), (1, 2, 0, 3, 4), 250_000): [16 * 96, 96, 16, 1, 1],
+        # modes 0, 1 fuse: (2048, 16, 300) with perm (1, 0, 2)
+        ((64, 32, 16, 300), (2, 0, 1, 3), 250_000): [2048 * 16, 16, 2048, 1, 1],
+        # identity prefix c0 before B
+        ((3, 700, 9, 400), (0, 2, 1, 3), 250_000): [3 * 700 * 9, 9, 700, 1, 3],
+        # reversal of three modes: c1 sits between B = c0 and A = c2
+        ((20, 30, 40, 500), (2, 1, 0, 3), 250_000): [20 * 30 * 40, 40, 20, 30, 1],
+    }
+    for (dims, perm, nnz), grid in cases.items():
+        info = lco.Plan(dims, perm).info(nnz)
+        assert info["path"] == "block", (dims, perm, info["path"])
+        assert info["block_grid"] == grid, (dims, perm, info["block_grid"])
+        nb, da, db, mid, hi = grid
+        assert da * db * mid * hi == nb
+    # too few nonzeros per block (< 4 on average): sorted instead
+    assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(4_000_000)["path"] != "block"
