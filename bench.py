@@ -375,6 +375,9 @@ def main():
     ap.add_argument("--e2e-sequential", action="store_true",
                     help="e2e: one stream only (no overlap of consecutive steps)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "direct"],
+                    help="N > 1: NCCL all_to_all after the partition, or the partition storing "
+                         "straight into the peers' symmetric memory (lco_partition_direct)")
     ap.add_argument("--cpu-nnz", type=int, default=40_000_000)
     ap.add_argument("--ref-nnz", type=int, default=20_000_000)
     ap.add_argument("--scale", type=int, default=None,

@@ -149,6 +149,30 @@ LCO_API lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* key
                          uint32_t* send_idx, uint64_t* send_counts, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* The exchange fused into the partition ("the partition scatter IS the
+ * exchange"): the same stable multisplit as lco_partition, but every record is stored
+ * straight into its destination rank's receive buffer, at recv_*[d][recv_offsets[d] + w]
+ * (w = its index among this rank's records for d).  recv_keys / recv_vals / recv_idx
+ * are [host] arrays of `world` DEVICE pointers: peer-mapped buffers of the other GPUs
+ * (CUDA IPC / symmetric memory over NVLink), or plain local buffers.  recv_offsets
+ * [host]: where this rank's chunk starts in each receiver = the sum of the counts of the
+ * lower source ranks for that destination (from lco_partition_counts + an all-gather),
+ * so receivers see the chunks in source-rank order = global input order.  send_counts
+ * (device) as in lco_partition.  world in 1..16; the caller synchronizes the ranks
+ * before the receivers read.  Same workspace as lco_partition. */
+LCO_API lco_status lco_partition_direct(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
+                                const double* vals_in, uint32_t idx_base, int world,
+                                const uint64_t* splitters, uint64_t* const* recv_keys,
+                                double* const* recv_vals, uint32_t* const* recv_idx,
+                                const uint64_t* recv_offsets, uint64_t* send_counts,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
+/* Only the per-destination record counts of the partition (device send_counts[world]):
+ * the count and scan of the multisplit pass, no data movement.  world in 1..4096. */
+LCO_API lco_status lco_partition_counts(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
+                                int world, const uint64_t* splitters, uint64_t* send_counts,
+                                void* workspace, size_t workspace_bytes, void* stream);
+
 /* Histogram of the top `bits` bits of the re-encoded keys (new-key order), used to
  * choose balanced splitters: counts[b] += #{i : (K'_i >> (keybits - bits)) == b} where
  * keybits = ceil(log2(prod dims)).  counts: 2^bits uint64 on the device, ACCUMULATED

@@ -674,6 +674,106 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
   return LCO_OK;
 }
 
+// Shared argument checks / setup of lco_partition_counts and lco_partition_direct.
+static lco_status partition_setup(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
+                                  const double* vals_in, int world, const uint64_t* splitters,
+                                  uint64_t* send_counts, void* workspace, size_t workspace_bytes,
+                                  int max_world, PassIO* io, int* rb) {
+  lco_status st = check_handle(h);
+  if (st) return st;
+  if (world < 1 || world > max_world) {
+    set_error("world %d outside 1..%d", world, max_world);
+    return LCO_ERR_ARG;
+  }
+  if (nnz > h->max_nnz || nnz >= (1ull << 32)) {
+    set_error("nnz above max_nnz or 2^32-1");
+    return LCO_ERR_CAPACITY;
+  }
+  if (!send_counts || (world > 1 && !splitters) || (nnz && !keys_in)) {
+    set_error("keys_in, send_counts (and splitters when world > 1) are required");
+    return LCO_ERR_NULL;
+  }
+  *rb = partition_rb(world);
+  CallPlan pp;
+  memset(&pp, 0, sizeof pp);
+  pp.path = kPathOnesweep;
+  pp.passes = 1;
+  pp.rb = *rb;
+  const WsLayout w = layout_for(pp, nnz);
+  if (nnz && (!workspace || workspace_bytes < w.total ||
+              reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
+    set_error("workspace needs %zu bytes, 256-byte aligned", w.total);
+    return LCO_ERR_WORKSPACE;
+  }
+  memset(io, 0, sizeof *io);
+  io->nnz = nnz;
+  io->keys_in = keys_in;
+  io->vals_in = vals_in;
+  io->ctrl = reinterpret_cast<uint32_t*>(static_cast<char*>(workspace) + w.ctrl);
+  io->splitters = world > 1 ? splitters : reinterpret_cast<const uint64_t*>(send_counts);
+  io->world = world;
+  io->counts64 = send_counts;
+  return LCO_OK;
+}
+
+lco_status lco_partition_counts(lco_handle h, uint64_t nnz, const uint64_t* keys_in, int world,
+                                const uint64_t* splitters, uint64_t* send_counts,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  PassIO io;
+  int rb = 8;
+  lco_status st = partition_setup(h, nnz, keys_in, nullptr, world, splitters, send_counts,
+                                  workspace, workspace_bytes, 4096, &io, &rb);
+  if (st) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = nnz == 0 ? cudaMemsetAsync(send_counts, 0, (size_t)world * 8, s)
+                           : run_partition(rb, h->kp_full, io, Launch{s, nullptr, nullptr}, true);
+  return e == cudaSuccess ? LCO_OK : cuda_fail(e, "lco_partition_counts");
+}
+
+lco_status lco_partition_direct(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
+                                const double* vals_in, uint32_t idx_base, int world,
+                                const uint64_t* splitters, uint64_t* const* recv_keys,
+                                double* const* recv_vals, uint32_t* const* recv_idx,
+                                const uint64_t* recv_offsets, uint64_t* send_counts,
+                                void* workspace, size_t workspace_bytes, void* stream) {
+  PassIO io;
+  int rb = 8;
+  lco_status st = partition_setup(h, nnz, keys_in, vals_in, world, splitters, send_counts,
+                                  workspace, workspace_bytes, kMaxDirect, &io, &rb);
+  if (st) return st;
+  if (!recv_keys || !recv_idx || !recv_offsets || (vals_in && !recv_vals)) {
+    set_error("recv_keys, recv_idx, recv_offsets (and recv_vals with values) are required");
+    return LCO_ERR_NULL;
+  }
+  DirectOut d;
+  memset(&d, 0, sizeof d);
+  for (int r = 0; r < world; ++r) {
+    if (!recv_keys[r] || !recv_idx[r] || (vals_in && !recv_vals[r])) {
+      set_error("receive buffer of rank %d is NULL", r);
+      return LCO_ERR_NULL;
+    }
+    d.k[r] = recv_keys[r];
+    d.v[r] = vals_in ? recv_vals[r] : nullptr;
+    d.p[r] = recv_idx[r];
+    d.off[r] = recv_offsets[r];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (nnz == 0) {
+    cudaError_t e = cudaMemsetAsync(send_counts, 0, (size_t)world * 8, s);
+    return e == cudaSuccess ? LCO_OK : cuda_fail(e, "lco_partition_direct");
+  }
+  io.idx_base = idx_base;
+  io.direct = &d;
+  io.vals_out = vals_in ? reinterpret_cast<double*>(1) : nullptr;  // selects the VALS kernels
+  io.keys_out = recv_keys[0];
+  Launch L{s, nullptr, nullptr};
+  ProfCtx pc;
+  const bool prof = prof_begin(h, s, &pc, &L);
+  cudaError_t e = run_partition(rb, h->kp_full, io, L, false);
+  if (prof) prof_end(&pc);
+  return e == cudaSuccess ? LCO_OK : cuda_fail(e, "lco_partition_direct");
+}
+
 lco_status lco_compress_workspace_size(uint64_t nnz, int doubly, size_t* bytes) {
   if (!bytes) {
     set_error("bytes is NULL");

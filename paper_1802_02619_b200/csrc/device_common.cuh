@@ -257,6 +257,14 @@ struct ScatterIO {
   const uint32_t* toff;     // [tiles][BINS] from k_offsets
   int keep_old_key;         // partition: scatter the old key
   uint32_t idx_base;        // partition: added to single-pass source positions
+  // partition straight into the receivers (lco_partition_direct): record w of digit d
+  // (= destination rank) goes to dk[d][doff[d] + w], w = position - bucket[d]
+  int direct;
+  const uint32_t* bucket;
+  uint64_t* dk[16];
+  double* dv[16];
+  uint32_t* dp[16];
+  uint64_t doff[16];
 };
 
 }  // namespace lco

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(NT, 2)
   }
   __syncthreads();  // the warp counters (in sV) are dead from here on
   // ---- gather values / positions into their slots (cp.async, global -> shared) ----
-  const bool want_p = io.pout != nullptr;
+  const bool want_p = io.pout != nullptr || io.direct;
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     if ((meta[it] & 0xFFFFu) == kInvalid) continue;
@@ -392,12 +392,25 @@ __global__ void __launch_bounds__(NT, 2)
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int d = tid + b * NT;
-    if (d < BINS) gbase[d] -= loff[d];  // global position of local slot 0 of digit d
+    if (d < BINS) {
+      gbase[d] -= loff[d];  // global position of local slot 0 of digit d
+      if (io.direct) gbase[d] -= io.bucket[d];  // ... within its destination's chunk
+    }
   }
   cp_async_wait<0>();
   __syncthreads();
   // ---- one write loop: K', V, position of each slot ----
   const bool remap = !FIRST && LAST && io.idx_in != nullptr;
+  if (io.direct) {  // partition: the scatter IS the exchange (stores to peer memory)
+    for (uint32_t p = tid; p < n; p += NT) {
+      const uint32_t d = sdig[p];
+      const uint64_t w = io.doff[d] + (uint32_t)(gbase[d] + p);  // gbase wraps mod 2^32
+      io.dk[d][w] = sK[p];
+      if (VALS) io.dv[d][w] = sV[p];
+      io.dp[d][w] = sP[p];
+    }
+    return;
+  }
   for (uint32_t p = tid; p < n; p += NT) {
     const uint32_t g = gbase[sdig[p]] + p;
     io.kout[g] = sK[p];
@@ -634,7 +647,17 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
     case 11: k_offsets<11><<<c.nchunks, kThreads, 0, L.stream>>>(a, c.thist, c.csum, c.bucket, c.toff); break;
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const ScatterIO s = pass_buffers(io, j, last, c.toff);
+  ScatterIO s = pass_buffers(io, j, last, c.toff);
+  if (io.direct) {
+    s.direct = 1;
+    s.bucket = c.bucket;
+    for (int d = 0; d < kMaxDirect && d < BINS; ++d) {
+      s.dk[d] = io.direct->k[d];
+      s.dv[d] = io.direct->v[d];
+      s.dp[d] = io.direct->p[d];
+      s.doff[d] = io.direct->off[d];
+    }
+  }
   if (L.mark)
     L.mark(L.ctx, part ? "k_partition"
                        : (first && last ? "k_scatter_single"
@@ -661,6 +684,20 @@ cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t run_partition(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L,
+                          bool count_only) {
+  PassParams a;
+  memset(&a, 0, sizeof a);
+  a.kp = kp;
+  a.kp.passes = 1;
+  a.pf_dist = prefetch_distance();
+  a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
+  a.nnz = io.nnz;
+  a.splitters = io.splitters;
+  a.world = io.world;
+  return run_pass(rb, a, io, 0, true, true, L, count_only);
 }
 
 cudaError_t run_copy(uint64_t nnz, const uint64_t* keys_in, const double* vals_in,

@@ -16,6 +16,16 @@ struct Launch {
 constexpr uint32_t kMaxChunks = 1024;  // persistent CTAs (chunks) per pass, upper bound
 
 // All buffers of one multi-pass run.  Partition mode: splitters != null, single pass.
+// Partition straight into the receivers' buffers (peer-mapped device pointers): record
+// w of destination d goes to k[d][off[d] + w] (lco_partition_direct).
+constexpr int kMaxDirect = 16;
+struct DirectOut {
+  uint64_t* k[kMaxDirect];
+  double* v[kMaxDirect];
+  uint32_t* p[kMaxDirect];
+  uint64_t off[kMaxDirect];
+};
+
 struct PassIO {
   uint64_t nnz;
   const uint64_t* keys_in;
@@ -35,6 +45,7 @@ struct PassIO {
   int world;
   uint32_t idx_base;
   uint64_t* counts64;
+  const DirectOut* direct;  // partition: scatter into the receivers' buffers
 };
 
 // Pointers into a pass control block (pass_ctrl_bytes()).
@@ -78,6 +89,10 @@ ScatterIO pass_buffers(const PassIO& io, int j, bool last, const uint32_t* toff)
 cudaError_t run_pass(int rb, const PassParams& a, const PassIO& io, int j, bool first, bool last,
                      const Launch& L, bool count_only = false);
 cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
+// partition (io.splitters set): one pass; count_only stops after the digit totals
+// (io.counts64 written)
+cudaError_t run_partition(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L,
+                          bool count_only);
 uint32_t leaf_cap();      // largest leaf one CTA sorts in shared memory
 uint32_t leaf_target();   // expected leaf size the MSD digits aim for (warp leaves)
 uint32_t cta_leaf_cap();  // largest leaf k_leafc sorts

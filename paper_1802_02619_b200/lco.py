@@ -92,6 +92,10 @@ _SIGS = {
     "lco_partition": (ctypes.c_int, [_P, _U64, _P, _P, ctypes.c_uint32, ctypes.c_int, _P, _P, _P,
                                      _P, _P, _P, ctypes.c_size_t, _P]),
     "lco_key_histogram": (ctypes.c_int, [_P, _U64, _P, ctypes.c_int, _P, _P]),
+    "lco_partition_counts": (ctypes.c_int, [_P, _U64, _P, ctypes.c_int, _P, _P, _P,
+                                            ctypes.c_size_t, _P]),
+    "lco_partition_direct": (ctypes.c_int, [_P, _U64, _P, _P, ctypes.c_uint32, ctypes.c_int, _P,
+                                            _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _P]),
     "lco_add_workspace_size": (ctypes.c_int, [_P, _U64, _U64, ctypes.POINTER(ctypes.c_size_t)]),
     "lco_compress_workspace_size": (ctypes.c_int, [_U64, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
     "lco_compress": (ctypes.c_int, [_U64, _P, _U64, _U64, ctypes.c_int, _P, _P, _P, _P, _P,
@@ -382,6 +386,53 @@ class Plan:
                                        _ptr(sp), _ptr(sk), _ptr(sv), _ptr(si), _ptr(cnt), wptr,
                                        wlen, _stream_ptr(stream, dev)))
         return sk, sv, si, cnt
+
+    def partition_counts(self, keys, splitters, stream=None, workspace=None):
+        """Records per destination rank of the multisplit (device int64[world])."""
+        dev = keys.device
+        n = keys.numel()
+        world = 1 if splitters is None else splitters.numel() + 1
+        cnt = torch.zeros(world, dtype=torch.int64, device=dev)
+        if workspace is None:
+            ws, off = _workspace(self.workspace_size(n), dev)
+        else:
+            ws, off = workspace, (-workspace.data_ptr()) % 256
+        wptr = None if ws is None else ctypes.c_void_p(ws.data_ptr() + off)
+        wlen = 0 if ws is None else ws.numel() - off
+        sp = None if splitters is None else splitters.contiguous()
+        with torch.cuda.device(dev):
+            _check(lib().lco_partition_counts(self._h, n, _ptr(keys), world, _ptr(sp), _ptr(cnt),
+                                              wptr, wlen, _stream_ptr(stream, dev)))
+        return cnt
+
+    def partition_direct(self, keys, vals, idx_base, splitters, recv_keys, recv_vals, recv_idx,
+                         recv_offsets, stream=None, workspace=None):
+        """The partition with the exchange fused in: records go straight into the
+        receivers' buffers (lists of device tensors, peer-mapped on a multi-GPU box) at
+        recv_offsets[d] + index.  Returns the device send counts."""
+        dev = keys.device
+        n = keys.numel()
+        world = 1 if splitters is None else splitters.numel() + 1
+        cnt = torch.zeros(world, dtype=torch.int64, device=dev)
+        if workspace is None:
+            ws, off = _workspace(self.workspace_size(n), dev)
+        else:
+            ws, off = workspace, (-workspace.data_ptr()) % 256
+        wptr = None if ws is None else ctypes.c_void_p(ws.data_ptr() + off)
+        wlen = 0 if ws is None else ws.numel() - off
+        sp = None if splitters is None else splitters.contiguous()
+        arr = ctypes.c_void_p * world
+        rk = arr(*[t.data_ptr() for t in recv_keys])
+        rv = None if vals is None else arr(*[t.data_ptr() for t in recv_vals])
+        ri = arr(*[t.data_ptr() for t in recv_idx])
+        ro = (ctypes.c_uint64 * world)(*[int(x) for x in recv_offsets])
+        with torch.cuda.device(dev):
+            _check(lib().lco_partition_direct(
+                self._h, n, _ptr(keys), _ptr(vals), int(idx_base), world, _ptr(sp),
+                ctypes.cast(rk, _P), None if rv is None else ctypes.cast(rv, _P),
+                ctypes.cast(ri, _P), ctypes.cast(ro, _P), _ptr(cnt), wptr, wlen,
+                _stream_ptr(stream, dev)))
+        return cnt
 
     def key_histogram(self, keys, bits, counts=None, stream=None):
         dev = keys.device

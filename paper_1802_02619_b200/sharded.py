@@ -46,6 +46,12 @@ class CudaOps:
     def permute(self, keys, vals, idx):
         return self.plan.permute(keys, vals, idx)
 
+    def partition_counts(self, keys, splitters):
+        return self.plan.partition_counts(keys, splitters)
+
+    def partition_direct(self, keys, vals, idx_base, splitters, rk, rv, ri, offsets):
+        return self.plan.partition_direct(keys, vals, idx_base, splitters, rk, rv, ri, offsets)
+
 
 def key_bits(dims) -> int:
     total = 1
@@ -75,12 +81,16 @@ def choose_splitters(global_hist: torch.Tensor, world: int, kbits: int, bits: in
     return spl
 
 
-def permute_sharded(keys, vals, dims, perm, group=None, ops=None, bits=14, timings=None):
+def permute_sharded(keys, vals, dims, perm, group=None, ops=None, bits=14, timings=None,
+                    exchange="nccl"):
     """Permute the globally sorted LCO tensor whose slice this rank holds.
 
     Returns (keys_out, vals_out, perm_out) of this rank's part of the output; perm_out
     holds GLOBAL source indices.  ``timings`` (dict) receives per-phase seconds measured
-    with CUDA events when running on CUDA."""
+    with CUDA events when running on CUDA.  ``exchange``: "nccl" (partition into send
+    buffers, then all_to_all_single) or "direct" (the partition scatter stores every
+    record into its receiver's symmetric-memory buffer over NVLink: lco_partition_direct;
+    CUDA only)."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     ops = ops or CudaOps(dims, perm)
@@ -109,6 +119,9 @@ def permute_sharded(keys, vals, dims, perm, group=None, ops=None, bits=14, timin
     spl = choose_splitters(hist, world, kbits, bits)
     splitters = torch.tensor(spl, dtype=torch.int64, device=dev) if world > 1 else None
     mark("splitters")
+    if exchange == "direct":
+        return _direct_exchange(keys, vals, ops, splitters, idx_base, world, rank, group, mark,
+                                ev, timings, cuda)
     sk, sv, si, send_counts = ops.partition(keys, vals, idx_base, splitters)
     mark("partition")
     recv_counts = torch.empty_like(send_counts)
@@ -134,6 +147,51 @@ def permute_sharded(keys, vals, dims, perm, group=None, ops=None, bits=14, timin
             torch.cuda.synchronize(dev)
             for (n0, e0), (n1, e1) in zip(ev[:-1], ev[1:]):
                 timings[n1] = e0.elapsed_time(e1) / 1e3
+    return out
+
+
+def _direct_exchange(keys, vals, ops, splitters, idx_base, world, rank, group, mark, ev, timings,
+                     cuda):
+    """Partition and exchange in one kernel: counts -> all_gather -> each source's offset
+    in every receiver (source-rank order = global input order) -> lco_partition_direct
+    into the peers' symmetric-memory buffers -> barrier -> local permute."""
+    if not cuda:
+        raise ValueError("exchange='direct' needs CUDA tensors (peer-mapped device memory)")
+    import torch.distributed._symmetric_memory as symm_mem
+    dev = keys.device
+    counts = ops.partition_counts(keys, splitters)  # [world] to each destination
+    allc = torch.empty(world * world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allc, counts, group=group)
+    allc = allc.view(world, world).cpu()  # [src][dst]
+    offs = [int(allc[:rank, d].sum()) for d in range(world)]
+    nrecv = int(allc[:, rank].sum())
+    cap = max(1, int(allc.sum(0).max()))  # symmetric buffers: the same size on every rank
+    group_name = (group or dist.group.WORLD).group_name
+    bufs = []
+    for dt in (torch.int64, torch.float64 if vals is not None else None, torch.int32):
+        if dt is None:
+            bufs.append(None)
+            continue
+        t = symm_mem.empty(cap, dtype=dt, device=dev)
+        h = symm_mem.rendezvous(t, group_name)
+        bufs.append((t, h))
+    peers = [None if b is None else [b[1].get_buffer(d, (cap,), b[0].dtype) for d in range(world)]
+             for b in bufs]
+    ops.partition_direct(keys, vals, idx_base, splitters, peers[0], peers[1], peers[2], offs)
+    bufs[0][1].barrier(channel=0)  # every rank's stores have landed
+    mark("exchange")
+    rk = bufs[0][0][:nrecv]
+    rv = None if bufs[1] is None else bufs[1][0][:nrecv]
+    ri = bufs[2][0][:nrecv]
+    out = ops.permute(rk, rv, ri)
+    mark("local_permute")
+    if timings is not None:
+        timings["sent_bytes"] = int(sum(int(allc[rank, d]) for d in range(world) if d != rank)) * (
+            8 + (8 if vals is not None else 0) + 4)
+        timings["recv_nnz"] = nrecv
+        torch.cuda.synchronize(dev)
+        for (n0, e0), (n1, e1) in zip(ev[:-1], ev[1:]):
+            timings[n1] = e0.elapsed_time(e1) / 1e3
     return out
 
 
@@ -172,7 +230,7 @@ def bench_main(args):
     torch.cuda.empty_cache()
     ops = CudaOps(dims, perm)
     for _ in range(args.warmup):
-        permute_sharded(keys, vals, dims, perm, ops=ops)
+        permute_sharded(keys, vals, dims, perm, ops=ops, exchange=getattr(args, 'exchange', 'nccl'))
     torch.cuda.synchronize()
     clocks = _bench.ClockSampler(local) if rank == 0 else None
     if clocks:
@@ -184,7 +242,8 @@ def bench_main(args):
         t = {}
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        permute_sharded(keys, vals, dims, perm, ops=ops, timings=t)
+        permute_sharded(keys, vals, dims, perm, ops=ops, timings=t,
+                        exchange=getattr(args, 'exchange', 'nccl'))
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
@@ -215,7 +274,8 @@ def bench_main(args):
             a.record()
             dk.copy_(hk, non_blocking=True)
             dv.copy_(hv, non_blocking=True)
-            ko, vo, po = permute_sharded(dk, dv, dims, perm, ops=ops)
+            ko, vo, po = permute_sharded(dk, dv, dims, perm, ops=ops,
+                                         exchange=getattr(args, 'exchange', 'nccl'))
             if outs is None:
                 outs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (ko, vo, po)]
             for h, d in zip(outs, (ko, vo, po)):
@@ -250,7 +310,10 @@ def bench_main(args):
             "dtype": "u64 keys / f64 values (moved, bit-exact)", "data": "synthetic",
             "config": {"workload": f"{cfg}: {recipe}; perm {tuple(perm)}; sharded by key range "
                                    f"over {world} GPUs", "nnz": n,
-                       "parallelism": f"key-range sharding x{world} (NCCL all_to_all)",
+                       "parallelism": f"key-range sharding x{world} ("
+                                      + ("partition stores into peer symmetric memory"
+                                         if getattr(args, "exchange", "nccl") == "direct"
+                                         else "NCCL all_to_all") + ")",
                        "l2": "inputs >> L2"},
             "exchange": {"seconds": t_ex, "sent_bytes_per_gpu": sent,
                          "nvlink_frac_of_900GBps": nvlink},

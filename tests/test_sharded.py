@@ -141,6 +141,63 @@ def test_virtual_ranks_cuda(world, cuda_device):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("world,vals", [(2, True), (4, True), (8, False), (16, True)])
+def test_virtual_ranks_direct_exchange(world, vals, cuda_device):
+    """The exchange fused into the partition (lco_partition_direct): each (emulated) rank
+    counts its records per destination (lco_partition_counts), the counts give every
+    source chunk its offset in each receiver (source-rank order), and the partition
+    scatter stores the records straight into the receivers' buffers -- which on a
+    multi-GPU box are peer-mapped NVLink memory.  The receivers' buffers must equal the
+    send chunks of lco_partition concatenated in source order, and the local permutes
+    the single-GPU oracle."""
+    import paper_1802_02619_b200 as lco
+    import workloads
+    w = workloads.config("C5", scale=300_000, device=cuda_device)
+    dims, perm = w.dims, w.perms[0]
+    p = lco.plan(dims, perm)
+    n = w.keys.numel()
+    cuts = [n * r // world for r in range(world + 1)]
+    kb = sharded.key_bits(dims)
+    hist = sum(p.key_histogram(w.keys[cuts[r]:cuts[r + 1]], 12) for r in range(world))
+    spl = torch.tensor(sharded.choose_splitters(hist, world, kb, 12), dtype=torch.int64,
+                       device=cuda_device)
+    sl = [(w.keys[cuts[r]:cuts[r + 1]], w.vals[cuts[r]:cuts[r + 1]] if vals else None)
+          for r in range(world)]
+    counts = torch.stack([p.partition_counts(k, spl) for k, _ in sl]).cpu()  # [src][dst]
+    total = counts.sum(0)
+    rk = [torch.full((int(total[d]),), -1, dtype=torch.int64, device=cuda_device) for d in range(world)]
+    rv = [torch.full((int(total[d]),), float("nan"), dtype=torch.float64, device=cuda_device)
+          for d in range(world)] if vals else None
+    ri = [torch.full((int(total[d]),), -1, dtype=torch.int32, device=cuda_device) for d in range(world)]
+    for r, (k, v) in enumerate(sl):
+        offs = [int(counts[:r, d].sum()) for d in range(world)]
+        cnt = p.partition_direct(k, v, cuts[r], spl, rk, rv, ri, offs)
+        assert torch.equal(cnt.cpu(), counts[r])
+    torch.cuda.synchronize()
+    outs = []
+    for d in range(world):
+        exp_k, exp_v, exp_i = [], [], []
+        for r, (k, v) in enumerate(sl):
+            sk, sv, si, cnt = p.partition(k, v if vals else None, cuts[r], spl)
+            o, c = int(cnt[:d].sum()), int(cnt[d])
+            exp_k.append(sk[o:o + c]); exp_i.append(si[o:o + c])
+            if vals:
+                exp_v.append(sv[o:o + c])
+        assert torch.equal(rk[d], torch.cat(exp_k)) and torch.equal(ri[d], torch.cat(exp_i))
+        if vals:
+            assert torch.equal(rv[d].view(torch.int64), torch.cat(exp_v).view(torch.int64))
+        outs.append(p.permute(rk[d], rv[d] if vals else None, ri[d]))
+    torch.cuda.synchronize()
+    ko = torch.cat([o[0] for o in outs]).cpu().numpy().view(np.uint64)
+    po = torch.cat([o[2] for o in outs]).cpu().numpy().view(np.uint32)
+    ek, ev, ep = oracle.permute(dims, perm, w.keys.cpu().numpy().view(np.uint64), w.vals.cpu().numpy())
+    assert np.array_equal(ko, ek) and np.array_equal(po, ep)
+    if vals:
+        vo = torch.cat([o[1] for o in outs]).cpu().numpy()
+        assert np.array_equal(vo.view(np.uint64), ev.view(np.uint64))
+
+
+@pytest.mark.gpu
 def test_permute_sharded_world1_nccl(cuda_device, tmp_path):
     """permute_sharded end to end through NCCL with a single rank."""
     import workloads
@@ -156,3 +213,23 @@ def test_permute_sharded_world1_nccl(cuda_device, tmp_path):
                                 w.vals.cpu().numpy())
     assert np.array_equal(ko.cpu().numpy().view(np.uint64), ek)
     assert np.array_equal(po.cpu().numpy().view(np.uint32), ep)
+
+
+@pytest.mark.gpu
+def test_permute_sharded_world1_direct(cuda_device, tmp_path):
+    """permute_sharded with the fused exchange (symmetric memory + lco_partition_direct)
+    end to end with a single rank."""
+    import workloads
+    w = workloads.config("C5", scale=100_000, device=cuda_device)
+    store = dist.FileStore(str(tmp_path / "store"), 1)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=cuda_device)
+    try:
+        ko, vo, po = sharded.permute_sharded(w.keys, w.vals, w.dims, w.perms[0], exchange="direct")
+        torch.cuda.synchronize()
+    finally:
+        dist.destroy_process_group()
+    ek, ev, ep = oracle.permute(w.dims, w.perms[0], w.keys.cpu().numpy().view(np.uint64),
+                                w.vals.cpu().numpy())
+    assert np.array_equal(ko.cpu().numpy().view(np.uint64), ek)
+    assert np.array_equal(po.cpu().numpy().view(np.uint32), ep)
+    assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64))
