@@ -75,9 +75,14 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   // pow2 first pass: the digit is a few bit fields of the OLD key, no full shuffle
   const bool direct = FIRST && !a.splitters && a.kp.ndmv[a.pass] >= 0;
   __syncthreads();
-  constexpr int H = kItems / 2;  // two rounds of 8 keys keep the registers low
+#ifndef LCO_CNT_HF
+#define LCO_CNT_HF 2
+#endif
+  // keys loaded per round: first passes (a few bit moves per key) run more CTAs per SM
+  // with 2 (C5 count 0.97 -> 0.76 ms); later passes keep 8 (4: 0.71 -> 0.75 ms)
+  constexpr int H = FIRST ? LCO_CNT_HF : kItems / 2;
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
+  for (int half = 0; half < kItems / H; ++half) {
     uint64_t k[H];
 #pragma unroll
     for (int it = 0; it < H; ++it) {
