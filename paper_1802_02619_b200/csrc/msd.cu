@@ -1357,7 +1357,7 @@ __global__ void __launch_bounds__(kXThreads, kXLg == 4 ? 2 : 1)
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem[];
-  // [chunk] sent records (key, position | (destination | local rank << 3) << 16)
+  // [chunk] sent records (key, position | (destination | local rank << kXLg) << 16)
   uint2* S = reinterpret_cast<uint2*>(smem);
   uint2* Rv = S + kXChunk;                                     // [recv] (key, pos)
   uint32_t* Bk = reinterpret_cast<uint32_t*>(Rv + kXRecv);    // [2^kXBBits] key buckets
@@ -1366,7 +1366,7 @@ __global__ void __launch_bounds__(kXThreads, kXLg == 4 ? 2 : 1)
   __shared__ uint32_t s_hist[kXCS], s_all[kXCS * kXCS], s_tot[kXCS], s_off[kXCS], s_warp[32],
       s_flag;
   __shared__ unsigned long long s_min, s_max;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const uint32_t r = cl.block_rank(), slot = blockIdx.x / kXCS;
   LeafDesc d;
   if (!leaf_at(L, 1, slot, &d)) return;  // uniform: empty bucket
