@@ -108,14 +108,13 @@ __device__ __forceinline__ void reencode_moves(const KeyPlan& p, uint64_t (&k)[N
   for (int j = 0; j < p.nmv; ++j) {
     const BitMove m = p.mv[j];
     const uint32_t mul = 1u << m.b;
+    // one 64-bit funnel shift per key (a = 0..63), mask, multiply-add into its word
     if (m.hi) {
 #pragma unroll
-      for (int i = 0; i < N; ++i)
-        ohi[i] += (bm_window((uint32_t)k[i], (uint32_t)(k[i] >> 32), m.a) & m.mask) * mul;
+      for (int i = 0; i < N; ++i) ohi[i] += ((uint32_t)(k[i] >> m.a) & m.mask) * mul;
     } else {
 #pragma unroll
-      for (int i = 0; i < N; ++i)
-        olo[i] += (bm_window((uint32_t)k[i], (uint32_t)(k[i] >> 32), m.a) & m.mask) * mul;
+      for (int i = 0; i < N; ++i) olo[i] += ((uint32_t)(k[i] >> m.a) & m.mask) * mul;
     }
   }
 #pragma unroll
