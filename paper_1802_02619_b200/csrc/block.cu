@@ -133,18 +133,13 @@ __global__ void __launch_bounds__(256) k_scan_tiles(uint64_t n, uint32_t* __rest
 // ---------------------------------------------------------------------------------
 constexpr int kBtThreads = 256;
 constexpr int kBtLgWarps = 3;
-#ifndef LCO_BT_CAP
-#define LCO_BT_CAP 2048
-#define LCO_BT_MINB 4
-#define LCO_BT_TARGET 1700
-#endif
-constexpr int kBtCap = LCO_BT_CAP;  // staged nonzeros per tile: 17 B each
-#ifndef LCO_BT_U
-#define LCO_BT_U 2
-#endif
-constexpr int kBtU = LCO_BT_U;  // nonzeros per thread per round (register path)
+// measured on C4: 2,048-nonzero stages at 4 CTAs/SM beat 3,072-4,096 at
+// 2-3 CTAs/SM and 1,024-1,800 at 5-6; 2 nonzeros per thread per round beat 4 and 8
+constexpr int kBtCap = 2048;    // staged nonzeros per tile: 17 B each
+constexpr int kBtMinBlocks = 4;
+constexpr int kBtU = 2;         // nonzeros per thread per round (register path)
 constexpr int kBtWU = 4;        // nonzeros per thread per round (stage -> output)
-constexpr int kBtTarget = LCO_BT_TARGET;  // expected nonzeros per tile the host sizes tiles for
+constexpr int kBtTarget = 1700;  // expected nonzeros per tile the host sizes tiles for
 
 struct BlockTiling {
   uint64_t dA, dB;
@@ -209,7 +204,7 @@ __global__ void __launch_bounds__(256) k_block_counts(const __grid_constant__ Bl
 }
 
 template <bool VALS>
-__global__ void __launch_bounds__(kBtThreads, LCO_BT_MINB) k_block_tiles(
+__global__ void __launch_bounds__(kBtThreads, kBtMinBlocks) k_block_tiles(
     const __grid_constant__ BlockTiling g, const __grid_constant__ KeyPlan kp,
     const __grid_constant__ KeyPlan kb, FastDiv fF, const uint64_t* __restrict__ keys_in,
     const double* __restrict__ vals_in, const uint32_t* __restrict__ idx_in,

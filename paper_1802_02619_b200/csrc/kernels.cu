@@ -75,12 +75,9 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   // pow2 first pass: the digit is a few bit fields of the OLD key, no full shuffle
   const bool direct = FIRST && !a.splitters && a.kp.ndmv[a.pass] >= 0;
   __syncthreads();
-#ifndef LCO_CNT_HF
-#define LCO_CNT_HF 2
-#endif
   // keys loaded per round: first passes (a few bit moves per key) run more CTAs per SM
   // with 2 (C5 count 0.97 -> 0.76 ms); later passes keep 8 (4: 0.71 -> 0.75 ms)
-  constexpr int H = FIRST ? LCO_CNT_HF : kItems / 2;
+  constexpr int H = FIRST ? 2 : kItems / 2;
 #pragma unroll
   for (int half = 0; half < kItems / H; ++half) {
     uint64_t k[H];

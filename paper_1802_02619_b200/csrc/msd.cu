@@ -1339,10 +1339,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
 // CTAs per SM) and 189 us (the final gathers of K', V and position from L2 are 8-byte
 // random reads that waste 3/4 of every sector) -- DESIGN.md §12.
 // ---------------------------------------------------------------------------------
-#ifndef LCO_XLG
-#define LCO_XLG 4
-#endif
-constexpr int kXLg = LCO_XLG;                    // log2 CTAs per cluster
+constexpr int kXLg = 4;                          // log2 CTAs per cluster (8: same speed)
 constexpr int kXCS = 1 << kXLg;                  // 16: non-portable size, two CTAs per SM
 constexpr int kXThreads = 512;
 constexpr int kXChunk = 65536 >> kXLg;           // records sent per CTA (bucket <= 64K)
