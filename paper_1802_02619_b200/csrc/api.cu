@@ -1000,7 +1000,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
     if (cp.path == kPathCopy || cp.path == kPathLocal) launches = 1;
     else if (cp.path == kPathTile) launches = 3;  // bounds, tile sorts, deferred tiles
     else if (cp.path == kPathSeg) launches = 6;   // count, scan, tiles, count, offsets, scatter
-    else if (cp.path == kPathBlock) launches = 7; // bounds, counts, 3 scan, delta, scatter
+    else if (cp.path == kPathBlock) launches = 5; // bounds, counts, 2 scan, tiles
     else if (cp.path == kPathOnesweep) launches = 4 * cp.passes;
     else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 2;  // passes, leaves, deferred
   }
