@@ -130,6 +130,10 @@ struct PassParams {
   const TileEntry* ttab;      // segmented mode: tile table (else tiles are t * kTile)
   const uint32_t* ntiles;     // segmented mode: number of valid table entries
   uint32_t pf_dist;           // L2 prefetch distance in tiles (resident CTAs), 0 = off
+  // LSD passes: k_count adds every tile's number of distinct digits here; k_scatter ranks
+  // with match.any instead of one ballot per digit bit when tiles hold few distinct digits
+  uint32_t* distinct;
+  int adapt;  // host side: run_pass points `distinct` into its control block
 };
 
 // PER consecutive uint16 tile-histogram entries in, PER uint32 offsets out (vector

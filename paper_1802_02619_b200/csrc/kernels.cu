@@ -58,7 +58,7 @@ __global__ void k_copy(uint64_t nnz, const uint64_t* __restrict__ keys_in,
 // its chunk's sums csum[t / ctiles][BINS] (segmented mode: into its segment's
 // totals csum[seg][BINS]); csum is zeroed by the launcher.
 // ---------------------------------------------------------------------------------
-template <int RB, bool FIRST>
+template <int RB, bool FIRST, bool ADAPT = false>
 __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ PassParams a,
                                                     const uint64_t* __restrict__ keys,
                                                     uint16_t* __restrict__ thist,
@@ -110,6 +110,12 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
     const uint32_t v = h[d];
     row[d] = (uint16_t)v;
     if (v) atomicAdd(cs + d, v);
+  }
+  if (ADAPT && (t & 31u) == 0) {  // distinct digits of every 32nd tile
+    uint32_t nz = 0;
+    for (int d = tid; d < BINS; d += kThreads) nz += h[d] != 0u;
+    nz = __reduce_add_sync(0xffffffffu, nz);
+    if (lane == 0 && nz) atomicAdd(a.distinct, nz);
   }
 }
 
@@ -227,7 +233,7 @@ constexpr size_t scatter_smem_bytes() {
 // NT threads (IT = kTile / NT nonzeros each): 512 for digits of <= 10 bits (more warps
 // in flight per SM, half the serial work per thread), 256 for 11-bit digits (whose
 // per-warp counters would not fit in sV with 16 warps).
-template <int RB, bool FIRST, bool LAST, bool VALS, int NT>
+template <int RB, bool FIRST, bool LAST, bool VALS, int NT, bool ADAPT = false>
 __global__ void __launch_bounds__(NT, 2)
     k_scatter(const __grid_constant__ PassParams a, const __grid_constant__ ScatterIO io) {
   constexpr int BINS = 1 << RB;
@@ -317,6 +323,9 @@ __global__ void __launch_bounds__(NT, 2)
   // ---- warp-level stable ranking into per-warp digit counters ----
   uint16_t* wh = whist + warp * BINS;
   const uint32_t ltm = lanemask_lt();
+  // few distinct digits per tile (structured keys): match.any, whose cost grows with the
+  // distinct values per warp, beats one ballot per digit bit
+  const bool few = ADAPT && *a.distinct < (uint64_t)((a.tiles + 31) / 32) * (BINS / 8);
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const uint32_t d = meta[it];
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(NT, 2)
     // ranking loop, ncu: +25 % on C5); for 11-bit digits match.any (12 ballots cost
     // more: -6 % on C4)
     uint32_t peers;
-    if (RB >= 11) {
+    if (RB >= 11 || (ADAPT && few)) {
       peers = __match_any_sync(0xffffffffu, d) & (ok ? 0xffffffffu : 0u);
     } else {
       peers = __ballot_sync(0xffffffffu, ok);
@@ -471,6 +480,9 @@ static cudaError_t set_smem_attrs() {
 #define LCO_ATTR(F, L, V)                                                       \
   e = cudaFuncSetAttribute(k_scatter<RB, F, L, V, scatter_nt(RB)>,              \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
+  if (e != cudaSuccess) return e;                                               \
+  e = cudaFuncSetAttribute(k_scatter<RB, F, L, V, scatter_nt(RB), true>,        \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
   if (e != cudaSuccess) return e;
   LCO_ATTR(true, true, false)
   LCO_ATTR(true, true, true)
@@ -533,8 +545,14 @@ PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl) {
 template <int RB>
 static cudaError_t launch_count_rb(bool first, const PassParams& a, const uint64_t* keys,
                                    uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s) {
-  if (first) k_count<RB, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
-  else k_count<RB, false><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  if (a.distinct) {
+    if (first) k_count<RB, true, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+    else k_count<RB, false, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  } else if (first) {
+    k_count<RB, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  } else {
+    k_count<RB, false><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  }
   return cudaGetLastError();
 }
 
@@ -556,8 +574,14 @@ static cudaError_t launch_scatter_rb(bool first, bool last, bool vals, const Pas
   const size_t smem = scatter_smem_bytes<RB>();
   constexpr int NT = scatter_nt(RB);
 #define LCO_LAUNCH(F, LST)                                                     \
-  if (vals) k_scatter<RB, F, LST, true, NT><<<grid, NT, smem, s>>>(a, io);    \
-  else k_scatter<RB, F, LST, false, NT><<<grid, NT, smem, s>>>(a, io);
+  if (a.distinct) {                                                            \
+    if (vals) k_scatter<RB, F, LST, true, NT, true><<<grid, NT, smem, s>>>(a, io); \
+    else k_scatter<RB, F, LST, false, NT, true><<<grid, NT, smem, s>>>(a, io);     \
+  } else if (vals) {                                                           \
+    k_scatter<RB, F, LST, true, NT><<<grid, NT, smem, s>>>(a, io);             \
+  } else {                                                                     \
+    k_scatter<RB, F, LST, false, NT><<<grid, NT, smem, s>>>(a, io);            \
+  }
   if (first && last) {
     LCO_LAUNCH(true, true)
   } else if (first) {
@@ -614,9 +638,10 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
   a.ctiles = chunk_tiles(c.tiles);
   cudaError_t e;
   const bool part = io.splitters != nullptr;
-  if ((e = cudaMemsetAsync(c.csum, 0, ((size_t)c.nchunks * BINS + 2 * BINS) * 4 + 4, L.stream)) !=
+  if ((e = cudaMemsetAsync(c.csum, 0, ((size_t)c.nchunks * BINS + 2 * BINS) * 4 + 8, L.stream)) !=
       cudaSuccess)
-    return e;  // chunk sums, totals, bucket starts and k_scan's completion counter
+    return e;  // chunk sums, totals, bucket starts, k_scan's completion counter, distinct
+  if (a0.adapt) a.distinct = c.done + 1;  // LSD passes (run_passes) only
   const uint64_t* in_keys = first ? io.keys_in : ((j % 2 == 1) ? io.kA : io.kB);
   if (L.mark) L.mark(L.ctx, first ? "k_count_first" : "k_count");
   if ((e = launch_count(rb, first, a, in_keys, c.thist, c.csum, c.tiles, L.stream)) != cudaSuccess)
@@ -681,6 +706,8 @@ cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch
   a.nnz = io.nnz;
   a.splitters = io.splitters;
   a.world = io.world;
+  // LSD passes choose their ranking from the distinct digits per tile (k_count samples)
+  a.adapt = !part && !getenv("LCO_NO_MATCH");
   for (int j = 0; j < P; ++j) {
     cudaError_t e = run_pass(rb, a, io, j, j == 0, j == P - 1, L);
     if (e != cudaSuccess) return e;
