@@ -325,32 +325,39 @@ __global__ void __launch_bounds__(NT, 2)
   const uint32_t ltm = lanemask_lt();
   // few distinct digits per tile (structured keys): match.any, whose cost grows with the
   // distinct values per warp, beats one ballot per digit bit
-  const bool few = ADAPT && *a.distinct < (uint64_t)((a.tiles + 31) / 32) * (BINS / 8);
-#pragma unroll
-  for (int it = 0; it < IT; ++it) {
+  const bool few = ADAPT && *a.distinct < (uint64_t)((a.tiles + 31) / 32) *
+                                              ((1u << a.kp.dbits[a.pass]) / 8);  // < 1/8 used
+  // lanes holding the same digit: for <= 10-bit digits one ballot per digit bit (ALU
+  // pipe; match.any goes through the MIO queue and its latency dominated the 8-bit
+  // ranking loop on random keys, ncu: +25 % on C5); for 11-bit digits, or tiles with few
+  // distinct digits, match.any (12 ballots cost more: -6 % on C4).  One loop per method,
+  // chosen once per tile, so each keeps its own register allocation.
+  auto rank_item = [&](int it, uint32_t peers) {
     const uint32_t d = meta[it];
     const bool ok = d != kInvalid;
-    // lanes holding the same digit: for <= 10-bit digits one ballot per digit bit (ALU
-    // pipe; match.any goes through the MIO queue and its latency dominated the 8-bit
-    // ranking loop, ncu: +25 % on C5); for 11-bit digits match.any (12 ballots cost
-    // more: -6 % on C4)
-    uint32_t peers;
-    if (RB >= 11 || (ADAPT && few)) {
-      peers = __match_any_sync(0xffffffffu, d) & (ok ? 0xffffffffu : 0u);
-    } else {
-      peers = __ballot_sync(0xffffffffu, ok);
-#pragma unroll
-      for (int b = 0; b < RB; ++b) {
-        const uint32_t bit = (d >> b) & 1u;
-        peers &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
-      }
-    }
+    peers &= ok ? 0xffffffffu : 0u;
     const uint32_t below = __popc(peers & ltm);
     const uint32_t before = ok ? (uint32_t)wh[d] : 0u;  // every peer reads the same counter
     __syncwarp();
     if (ok && below == 0) wh[d] = (uint16_t)(before + __popc(peers));
     meta[it] = d | ((before + below) << 16);
     __syncwarp();
+  };
+  if (RB >= 11 || (ADAPT && few)) {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) rank_item(it, __match_any_sync(0xffffffffu, meta[it]));
+  } else {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const uint32_t d = meta[it];
+      uint32_t peers = __ballot_sync(0xffffffffu, d != kInvalid);
+#pragma unroll
+      for (int b = 0; b < RB; ++b) {
+        const uint32_t bit = (d >> b) & 1u;
+        peers &= __ballot_sync(0xffffffffu, bit) ^ (bit - 1u);
+      }
+      rank_item(it, peers);
+    }
   }
   __syncthreads();
   // ---- per digit: exclusive prefix across warps, tile count ----
