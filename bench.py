@@ -33,32 +33,23 @@ import torch  # noqa: E402
 METRIC = "nonzeros permuted/sec and achieved HBM GB/s fraction at 1/2/4/8 B200"
 UNIT = "nonzeros/s"
 
-# Algorithmic bytes per nonzero of each kernel: the bytes the
-# kernel must move at minimum for the work it does (reads + writes, perm included).
-KERNEL_BYTES = {
-    "k_count_first": 8,       # read K (LIV shuffle + digit histogram)
-    "k_count": 8,             # read K'
-    "k_count_seg": 8,         # read K'
-    "k_scatter_first": 36,    # read K, V; write K', V, position
-    "k_scatter_single": 36,   # read K, V; write K', V, perm
-    "k_scatter_mid": 40,      # read K', V, position; write them
-    "k_scatter_seg": 40,
-    "k_scatter_last": 40,
-    "k_leafw": 40,            # read K', V, position; write K', V, perm (final)
-    "k_leafw_l1": 40,
-    "k_leafr": 40,            # CTA leaves, 32-bit sort keys (read K', V, pos; write)
-    "k_leafs": 40,            # CTA leaves, fully staged
-    "k_leafc": 40,            # CTA leaves, 64-bit sort keys
-    "k_leaf_l1": 40,
-    "k_leafc_tiles": 36,      # segment-local tiles: read K, V; write K', V, perm
-    "k_leaf": 36,
-    "k_leaf_deferred": 40,
-    "k_copy": 36,             # read K, V; write K, V, perm
-    "k_block_bounds": 8,      # read K (run bounds of the blocks)
-    "k_block_tiles": 36,      # read K, V; write K', V, perm (tiled transpose of runs)
+# Algorithmic bytes: read key + value, write key + value = 32 B per
+# nonzero, 36 B with the uint32 permutation vector.  Every roofline fraction below is
+# (these bytes x the nonzeros one launch / one step processes) / time / measured peak --
+# the same figure for the dominant kernel and for the step, so that a kernel's own extra
+# traffic (carried positions, re-reads) lowers its fraction instead of inflating it.
+ALG_BYTES = 32
+ALG_BYTES_PERM = 36
+# The bytes each kernel itself must move at minimum, reported beside the
+# fraction for context only.
+KERNEL_MODEL_BYTES = {
+    "k_count_first": 8, "k_count": 8, "k_count_seg": 8,
+    "k_scatter_first": 36, "k_scatter_single": 36, "k_scatter_mid": 40, "k_scatter_seg": 40,
+    "k_scatter_last": 40, "k_leafw": 40, "k_leafw_l1": 40, "k_leafr": 40, "k_leafs": 40,
+    "k_leafc": 40, "k_leafs_l1": 40, "k_leafr_l1": 40, "k_leafc_l1": 40, "k_leafc_tiles": 36,
+    "k_leaf_deferred": 40, "k_copy": 36, "k_block_bounds": 8, "k_block_tiles": 36,
     "k_partition": 36,
 }
-STEP_BYTES = 36  # read K+V, write K'+V (32) + the uint32 perm (4)
 
 CONFIGS = {
     # name: (workloads config, perm index)
@@ -126,6 +117,20 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def traffic_of(config, marker):
+    """DRAM bytes (read + write) per launch of the kernel behind `marker`, from one ncu
+    capture (profiles/traffic.json, written by scripts/save_profiles.py, which matches
+    every bench marker to the launch of the same kernel name in ncu's launch list)."""
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        e = json.load(open(tpath)).get(config, {}).get(marker)
+    except Exception:  # noqa: BLE001
+        return None
+    if isinstance(e, dict):
+        return e.get("bytes")
+    return None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -133,8 +138,21 @@ def dist_env():
     return world, rank, local
 
 
-def oracle_baseline(w, perm, target_s=15.0, max_nnz=40_000_000):
-    """Time the CPU oracle (1 core, as it stands) on a strided sample of the workload."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_baseline(w, perm, max_nnz=40_000_000):
+    """Time the CPU oracle as it stands on a strided sample of the workload (itself a
+    sorted LCO tensor): the single-core definition and the same
+    definition on every core of the process affinity mask (§8(d)(ii): OpenMP decode /
+    gather, __gnu_parallel::stable_sort)."""
     import oracle
     n = w.keys.numel()
     stride = max(1, -(-n // max_nnz))
@@ -144,10 +162,24 @@ def oracle_baseline(w, perm, target_s=15.0, max_nnz=40_000_000):
     t0 = time.perf_counter()
     oracle.permute(w.dims, perm, ks, vs)
     dt = time.perf_counter() - t0
-    return {"value": len(ks) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"every {stride}th nonzero of the sorted {w.name} input "
-                      f"({len(ks)} nnz, itself a sorted LCO tensor), one oracle.permute call "
-                      f"(decode / re-encode / std::stable_sort / gather), {dt:.2f} s"}
+    sample = (f"every {stride}th nonzero of the sorted {w.name} input ({len(ks)} nnz, itself a "
+              f"sorted LCO tensor), one oracle permute call (decode / re-encode / stable sort / "
+              f"gather)")
+    out = {"value": len(ks) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"{sample}, {dt:.2f} s", "cpu_model": cpu_model()}
+    try:
+        threads = oracle.par_threads()
+        oracle.permute_par(w.dims, perm, ks[:100_000], vs[:100_000])  # load / warm
+        t0 = time.perf_counter()
+        oracle.permute_par(w.dims, perm, ks, vs)
+        dp = time.perf_counter() - t0
+        out["all_cores"] = {"value": len(ks) / dp, "unit": UNIT, "cores": threads,
+                            "affinity_cpus": len(os.sched_getaffinity(0)),
+                            "kind": "oracle (OpenMP + __gnu_parallel::stable_sort)",
+                            "sample": f"{sample}, {dp:.2f} s"}
+    except Exception as ex:  # noqa: BLE001
+        out["all_cores"] = {"error": repr(ex)[:200]}
+    return out
 
 
 def run_reference(args):
@@ -216,24 +248,32 @@ def run_single(args):
     for _ in range(args.warmup):
         p.permute(w.keys, w.vals, out=out, workspace=ws)
     torch.cuda.synchronize()
-    p.profile_enable(args.steps)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    clocks = ClockSampler(0)
-    clocks.start()
-    time.sleep(0.3)
-    torch.cuda.synchronize()
-    wall0 = time.perf_counter()
-    for s in range(args.steps):
-        if flush:
-            fbuf.fill_(float(s))
-        ev[s][0].record(stream)
-        p.permute(w.keys, w.vals, out=out, workspace=ws)
-        ev[s][1].record(stream)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    clk = clocks.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
+
+    def timed(steps, outs, do_flush, profile=False, sample_clocks=False):
+        """CUDA events on the launching stream around each step; L2 flushed before each
+        step when do_flush (inputs smaller than 4x L2)."""
+        if profile:
+            p.profile_enable(steps)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        clocks = ClockSampler(0) if sample_clocks else None
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for st in range(steps):
+            if do_flush:
+                fbuf.fill_(float(st))
+            ev[st][0].record(stream)
+            p.permute(w.keys, w.vals, out=outs, workspace=ws)
+            ev[st][1].record(stream)
+        torch.cuda.synchronize()
+        wall_s = time.perf_counter() - w0
+        clk_ = clocks.stop() if clocks else None
+        return [x.elapsed_time(y) for x, y in ev], wall_s, clk_
+
+    step_ms, wall, clk = timed(args.steps, out, flush, profile=True, sample_clocks=True)
     ms = float(np.mean(step_ms))
     names, rows = p.profile_read()
     p.profile_enable(0)
@@ -252,17 +292,25 @@ def run_single(args):
     dom = max(kernels_only, key=kernels_only.get)
     dom_launch_ms = tot[dom] / counts[dom]
     peak, peak_src = peaks()
-    alg = KERNEL_BYTES.get(dom, STEP_BYTES) * n
-    achieved = alg / (dom_launch_ms / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.config, {}).get(dom)
-        except Exception:
-            traffic = None
-    step_achieved = STEP_BYTES * n / (ms / 1e3) / 1e9
+    # 32 B x the nonzeros one launch processes (every launch of the
+    # dominant kernel here processes all n), over that kernel's CUDA-event launch time
+    achieved = ALG_BYTES * n / (dom_launch_ms / 1e3) / 1e9
+    traffic = traffic_of(args.config, dom)
+    step_achieved = ALG_BYTES * n / (ms / 1e3) / 1e9
     value = n / (ms / 1e3)
+    # secondary figures: without the permutation vector (40 B/nnz schedule
+    # row), and for sub-L2 inputs the L2-warm time beside the flushed (cold) one
+    extra = {}
+    np_ms, _, _ = timed(max(3, args.steps // 2), (ko, vo, None), flush)
+    extra["no_perm"] = {"ms_per_step": float(np.mean(np_ms)),
+                        "value": n / (float(np.mean(np_ms)) / 1e3),
+                        "step_frac_32B": ALG_BYTES * n / (float(np.mean(np_ms)) / 1e3) / 1e9 / peak}
+    if flush:
+        wm, _, _ = timed(args.steps, out, False)
+        extra["l2_warm"] = {"ms_per_step": float(np.mean(wm)), "value": n / (float(np.mean(wm)) / 1e3),
+                            "note": "inputs left in L2 between steps (no flush)"}
+        extra["l2_cold"] = {"ms_per_step": ms, "value": value,
+                            "note": "L2 flushed before every step (the headline)"}
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -348,11 +396,17 @@ def run_single(args):
         "hbm_frac": step_achieved / peak,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "alg_bytes_per_nnz": KERNEL_BYTES.get(dom), "launch_ms": dom_launch_ms,
+                     "alg_bytes_per_nnz": ALG_BYTES, "alg_bytes_per_launch": ALG_BYTES * n,
+                     "frac_36B": ALG_BYTES_PERM * n / (dom_launch_ms / 1e3) / 1e9 / peak,
+                     "launch_ms": dom_launch_ms, "launch_share_of_step": tot[dom] / ms,
+                     "kernel_model_bytes_per_nnz": KERNEL_MODEL_BYTES.get(dom),
                      "peak_source": peak_src},
-        "step_roofline": {"alg_bytes_per_nnz": STEP_BYTES, "achieved": step_achieved,
-                          "peak": peak, "unit": "GB/s", "frac": step_achieved / peak},
+        "step_roofline": {"alg_bytes_per_nnz": ALG_BYTES, "achieved": step_achieved,
+                          "peak": peak, "unit": "GB/s", "frac": step_achieved / peak,
+                          "frac_36B": ALG_BYTES_PERM * n / (ms / 1e3) / 1e9 / peak},
+        **extra,
         "kernels_ms": {k: round(v, 4) for k, v in tot.items()},
+        "markers": names,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": info["launches"] * args.steps,
@@ -375,9 +429,11 @@ def main():
     ap.add_argument("--e2e-sequential", action="store_true",
                     help="e2e: one stream only (no overlap of consecutive steps)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "direct"],
-                    help="N > 1: NCCL all_to_all after the partition, or the partition storing "
-                         "straight into the peers' symmetric memory (lco_partition_direct)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "segments", "nccl", "direct"],
+                    help="N > 1: auto (segments when identity-prefix segments stay in place, "
+                         "else nccl), the exchange-free segment path, partition + one grouped "
+                         "NCCL exchange, or the partition storing straight into the peers' "
+                         "symmetric memory (lco_partition_direct)")
     ap.add_argument("--cpu-nnz", type=int, default=40_000_000)
     ap.add_argument("--ref-nnz", type=int, default=20_000_000)
     ap.add_argument("--scale", type=int, default=None,

@@ -18,18 +18,27 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
+_SRC_PAR = os.path.join(_HERE, "oracle_par.cpp")
+_LIB_PAR = os.path.join(_HERE, "liboracle_par.so")
 
 _ERR = {1: "bad argument", 2: "coordinate/key out of range", 3: "product of dims > 2^63-1",
         4: "RP claim violated (region not ordered by a resting index)"}
 
 
+def _compile(src, lib, extra, force):
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+        tmp = lib + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", *extra, "-o", tmp,
+                               src])
+        os.replace(tmp, lib)
+    return lib
+
+
 def build(force: bool = False) -> str:
-    """Compile oracle.cpp with g++ (-O2, single thread).  Returns the .so path."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", tmp, _SRC])
-        os.replace(tmp, _LIB)
-    return _LIB
+    """Compile oracle.cpp with g++ (-O2, single thread) and the all-cores variant
+    oracle_par.cpp (-fopenmp).  Returns the single-thread .so path."""
+    _compile(_SRC_PAR, _LIB_PAR, ["-fopenmp"], force)
+    return _compile(_SRC, _LIB, [], force)
 
 
 _lib = None
@@ -70,6 +79,28 @@ def _get():
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     return _lib
+
+
+_lib_par = None
+
+
+def _get_par():
+    global _lib_par
+    if _lib_par is None:
+        build()
+        _lib_par = ctypes.CDLL(_LIB_PAR)
+        f = _lib_par.oracle_permute_par
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p,
+                      ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        _lib_par.oracle_par_threads.restype = ctypes.c_int
+    return _lib_par
+
+
+def par_threads() -> int:
+    """Threads the all-cores oracle uses (OpenMP: the process affinity mask by default)."""
+    return int(_get_par().oracle_par_threads())
 
 
 def _dims(dims):
@@ -144,6 +175,12 @@ def _run(fn, dims, perm, keys, vals, idx):
 def permute(dims, perm, keys, vals=None, idx=None):
     """LIV shuffle + std::stable_sort (the definition).  Returns (keys, vals, perm)."""
     return _run(_get().oracle_permute, dims, perm, keys, vals, idx)
+
+
+def permute_par(dims, perm, keys, vals=None, idx=None):
+    """The same definition on all cores (OpenMP decode / gather, __gnu_parallel::stable_sort);
+    bit-identical to permute()."""
+    return _run(_get_par().oracle_permute_par, dims, perm, keys, vals, idx)
 
 
 def sort(dims, perm, keys, vals=None, idx=None):

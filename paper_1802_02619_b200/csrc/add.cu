@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(1024) k_merge_scan(const uint32_t* __restrict_
 
 cudaError_t run_count_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, uint64_t* total,
                            const Launch& L) {
-  if (L.mark) L.mark(L.ctx, "k_count_scan");
+  if (L.mark) L.mark(L.ctx, "k_merge_scan_counts");
   k_merge_scan<<<1, 1024, 0, L.stream>>>(counts, n, offsets, total);
   return cudaGetLastError();
 }
@@ -263,15 +263,11 @@ cudaError_t run_merge(uint64_t na, const uint64_t* ka, const double* va, uint64_
   k_merge_split<<<(unsigned)((nt + 1 + 255) / 256), 256, 0, L.stream>>>(ka, na, kb, nb, nt, split);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  static bool attr = false;
-  if (!attr) {
-    if ((e = cudaFuncSetAttribute(k_merge<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)merge_smem(false))) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(k_merge<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)merge_smem(true))) != cudaSuccess)
-      return e;
-    attr = true;
-  }
+  if ((e = kernel_setup(reinterpret_cast<const void*>(k_merge<false>), merge_smem(false),
+                        kMThreads)) != cudaSuccess ||
+      (e = kernel_setup(reinterpret_cast<const void*>(k_merge<true>), merge_smem(true),
+                        kMThreads)) != cudaSuccess)
+    return e;
   if (L.mark) L.mark(L.ctx, "k_merge_count");
   k_merge<false><<<(unsigned)nt, kMThreads, merge_smem(false), L.stream>>>(
       ka, va, na, kb, vb, nb, sign, split, tcount, nullptr, nullptr, nullptr);

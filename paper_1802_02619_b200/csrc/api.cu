@@ -48,7 +48,35 @@ struct CallPlan {
   KeyPlan kb;
 };
 
-CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
+// Environment overrides of the schedule (tests and A/B measurements only), read once by
+// lco_create; clamped so that no value can break a kernel's limits.
+Tuning read_tuning() {
+  Tuning t;
+  memset(&t, 0, sizeof t);
+  auto flag = [](const char* n) { return getenv(n) != nullptr ? 1 : 0; };
+  auto num = [](const char* n, int lo, int hi, int dflt) {
+    const char* v = getenv(n);
+    if (!v) return dflt;
+    int x = atoi(v);
+    return x < lo ? lo : (x > hi ? hi : x);
+  };
+  t.no_tile = flag("LCO_NO_TILE");
+  t.no_block = flag("LCO_NO_BLOCK");
+  t.no_seg = flag("LCO_NO_SEG");
+  t.msd_force = flag("LCO_MSD");
+  t.msd_b1 = num("LCO_MSD_B1", 4, 11, 0);
+  t.msd_b2 = num("LCO_MSD_B2", 4, 11, 0);
+  t.msd_cta = num("LCO_MSD_CTA", 0, 1, -1);
+  t.leafs_force = flag("LCO_LEAFS");
+  t.no_leafs = flag("LCO_NO_LEAFS");
+  t.no_leafr = flag("LCO_NO_LEAFR");
+  t.no_match = flag("LCO_NO_MATCH");
+  t.lsd_maxbits = num("LCO_LSD_MAXBITS", 1, 11, 0);
+  t.stable_msd = flag("LCO_STABLE_MSD");
+  return t;
+}
+
+CallPlan choose_plan(const OpPlan& op, uint64_t nnz, const Tuning& tu) {
   CallPlan c;
   memset(&c, 0, sizeof c);
   c.kp = op.kp;
@@ -67,7 +95,7 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   }
   // Identity prefix with small segments: every segment stays in place, so one on-chip
   // sort per tile of whole segments finishes the permutation (one read, one write).
-  if (op.segments > 1 && nnz / op.segments <= 3072 && !getenv("LCO_NO_TILE")) {
+  if (op.segments > 1 && nnz / op.segments <= 3072 && !tu.no_tile) {
     c.path = kPathTile;
     c.segdiv = op.segdiv;
     c.segments = op.segments;
@@ -85,7 +113,7 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
   // All rearranged modes in a small old-order prefix: a transpose of runs, no sorting
   // (block.cu): one read of the keys for the run bounds, O(blocks) tables, one tiled
   // copy that reads and writes long runs.
-  if (op.nblocks && op.nblocks * 4 <= nnz && op.nblocks < (1ull << 31) && !getenv("LCO_NO_BLOCK")) {
+  if (op.nblocks && op.nblocks * 4 <= nnz && op.nblocks < (1ull << 31) && !tu.no_block) {
     const double bcost = 8 + 36 + 24.0 * (double)op.nblocks / (double)nnz;
     if (bcost < c.cost) {
       c.path = kPathBlock;
@@ -105,7 +133,7 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     const int gb = ceil_log2(op.segments), mb = ceil_log2(op.middle);
     const bool pow2_mid = (op.middle & (op.middle - 1)) == 0;
     if (op.segments > 1 && gb <= 10 && mb >= 1 && mb <= 11 && pow2_mid && op.passes >= 2 &&
-        !getenv("LCO_NO_SEG")) {
+        !tu.no_seg) {
       c.path = kPathSeg;
       c.passes = 1;
       c.msd.b1 = gb;
@@ -141,17 +169,6 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     m.cta = (nnz >> m.b1) > wt;
     m.staged = m.cta && (nnz >> m.b1) <= st;
     mcost = 8 + 36 + 40;
-  } else if ((nnz >> 8) <= cluster_leaf_cap() * 15 / 16 && B - 8 <= 35 && B - 8 >= 4 &&
-             getenv("LCO_CLUSTER")) {
-    // one 8-bit MSD pass, then every bucket (up to ~60K nonzeros) sorted inside a
-    // cluster of CTAs (k_leafx): the second digit moves over DSMEM, not through HBM
-    // (opt-in: measured slower than two LSD passes on C3a, msd.cu)
-    m.levels = 1;
-    m.b1 = 8;
-    m.b2 = 0;
-    m.cta = 1;
-    m.cluster = 1;
-    mcost = 8 + 36 + 40;
   } else {
     m.levels = 2;
     m.b1 = 8;
@@ -162,18 +179,20 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz) {
     m.staged = m.cta && (nnz >> (m.b1 + m.b2)) <= st;
     mcost = 8 + 36 + 8 + 40 + 40;
   }
-  if (getenv("LCO_LEAFS")) m.staged = 1;
-  // schedule overrides for tests and A/B measurements (the defaults above otherwise)
-  if (getenv("LCO_MSD_B1")) m.b1 = atoi(getenv("LCO_MSD_B1"));
-  if (getenv("LCO_MSD_B2") && m.levels == 2) m.b2 = atoi(getenv("LCO_MSD_B2"));
-  if (getenv("LCO_MSD_CTA")) m.cta = atoi(getenv("LCO_MSD_CTA"));
+  if (tu.leafs_force) m.staged = 1;
+  // schedule overrides for tests and A/B measurements (the defaults above otherwise),
+  // kept inside the key: b1 + b2 < B
+  if (tu.msd_b1) m.b1 = tu.msd_b1 < B - 1 ? tu.msd_b1 : B - 1;
+  if (tu.msd_b2 && m.levels == 2) m.b2 = tu.msd_b2 < B - m.b1 ? tu.msd_b2 : B - m.b1 - 1;
+  if (m.levels == 2 && m.b2 < 1) m.levels = 1, m.b2 = 0;
+  if (tu.msd_cta >= 0) m.cta = tu.msd_cta;
   m.rb = B - m.b1 - m.b2;
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
   // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
   // and with a clear modelled win.
   // (one level: below 0.9 of the LSD model, C2a 0.105 vs 0.127 ms; two levels: below
   // 0.75 -- structured tensors (Table 2's Laplacian) fill two-level buckets unevenly)
-  if ((op.segments == 1 && mcost < (m.levels == 1 ? 0.9 : 0.75) * c.cost) || getenv("LCO_MSD")) {
+  if ((op.segments == 1 && mcost < (m.levels == 1 ? 0.9 : 0.75) * c.cost) || tu.msd_force) {
     c.path = kPathMsd;
     c.msd = m;
     c.cost = mcost;
@@ -293,10 +312,11 @@ lco_status check_handle(lco_handle h) {
 
 // Run one flat plan on device buffers with the workspace `ws` (layout_for of its call
 // plan); launches only, no checks.
-cudaError_t execute(lco_plan_s* h, const OpPlan& op, uint64_t nnz, const uint64_t* keys_in,
-                    const double* vals_in, const uint32_t* idx_in, uint64_t* keys_out,
-                    double* vals_out, uint32_t* perm_out, char* ws, const Launch& L) {
-  const CallPlan cp = choose_plan(op, nnz);
+cudaError_t execute(lco_plan_s* h, const OpPlan& op, bool unique, uint64_t nnz,
+                    const uint64_t* keys_in, const double* vals_in, const uint32_t* idx_in,
+                    uint64_t* keys_out, double* vals_out, uint32_t* perm_out, char* ws,
+                    const Launch& L) {
+  const CallPlan cp = choose_plan(op, nnz, h->tune);
   const WsLayout w = layout_for(cp, nnz);
   if (cp.path == kPathCopy)
     return run_copy(nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, L);
@@ -309,6 +329,8 @@ cudaError_t execute(lco_plan_s* h, const OpPlan& op, uint64_t nnz, const uint64_
   io.keys_out = keys_out;
   io.vals_out = vals_out;
   io.perm_out = perm_out;
+  io.tune = &h->tune;
+  io.unique = unique && !h->tune.stable_msd;
   io.ctrl = reinterpret_cast<uint32_t*>(ws + w.ctrl);
   const bool mv = vals_out != nullptr, mp = perm_out != nullptr;
   const bool hasA = cp.path == kPathMsd || cp.path == kPathTile || cp.passes >= 2;
@@ -340,11 +362,11 @@ struct Hier {
 Hier hier_for(const lco_plan_s* h, bool sort, uint64_t nnz) {
   Hier r;
   memset(&r, 0, sizeof r);
-  r.flat_cost = choose_plan(sort ? h->op_sort : h->op_permute, nnz).cost;
+  r.flat_cost = choose_plan(sort ? h->op_sort : h->op_permute, nnz, h->tune).cost;
   if (sort || h->nstages < 2 || nnz == 0) return r;
   size_t inner = 0;
   for (int j = 0; j < h->nstages; ++j) {
-    const CallPlan cp = choose_plan(h->stages[j].op, nnz);
+    const CallPlan cp = choose_plan(h->stages[j].op, nnz, h->tune);
     r.cost += cp.cost;
     const size_t t = layout_for(cp, nnz).total;
     inner = t > inner ? t : inner;
@@ -396,7 +418,7 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
       }
   }
   const Hier hp = hier_for(h, sort, nnz);
-  const size_t need = hp.use ? hp.total : layout_for(choose_plan(op, nnz), nnz).total;
+  const size_t need = hp.use ? hp.total : layout_for(choose_plan(op, nnz, h->tune), nnz).total;
   if (!workspace || ws_bytes < need || (reinterpret_cast<uintptr_t>(workspace) % kAlign)) {
     set_error("workspace needs %zu bytes, 256-byte aligned (got %zu at %p)", need, ws_bytes,
               workspace);
@@ -432,7 +454,7 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
   const bool prof = prof_begin(h, s, &pc, &L);
   cudaError_t e = cudaSuccess;
   if (!hp.use) {
-    e = execute(h, op, nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, ws, L);
+    e = execute(h, op, !sort, nnz, keys_in, vals_in, idx_in, keys_out, vals_out, perm_out, ws, L);
   } else {
     // stage j reads stage j-1's (K', V, position) from one of two intermediate buffer
     // sets and the last stage writes the outputs; positions compose through idx_in.
@@ -449,7 +471,7 @@ lco_status run_op(lco_handle h, const OpPlan& op, bool sort, uint64_t nnz, const
                            : (vals_in ? reinterpret_cast<double*>(buf + align_up(nnz * 8)) : nullptr);
       uint32_t* p_out = last ? perm_out
                              : (mp ? reinterpret_cast<uint32_t*>(buf + 2 * align_up(nnz * 8)) : nullptr);
-      e = execute(h, h->stages[j].op, nnz, k_in, v_in, i_in, k_out, v_out, p_out, inner, L);
+      e = execute(h, h->stages[j].op, true, nnz, k_in, v_in, i_in, k_out, v_out, p_out, inner, L);
       k_in = k_out;
       v_in = v_out;
       i_in = p_out;
@@ -489,6 +511,7 @@ lco_status lco_create(lco_handle* out, int order, const uint64_t* dims, const in
     return LCO_ERR_ARG;
   }
   memset(h, 0, sizeof *h);
+  h->tune = read_tuning();
   lco_status st = build_plan(h, order, dims, perm);
   if (st != LCO_OK) {
     delete h;
@@ -520,10 +543,10 @@ lco_status lco_workspace_size(lco_handle h, uint64_t nnz, size_t* bytes) {
   }
   const OpPlan& a = h->op_permute;
   const OpPlan& b = h->op_sort;
-  size_t x = layout_for(choose_plan(a, nnz), nnz).total;
+  size_t x = layout_for(choose_plan(a, nnz, h->tune), nnz).total;
   const Hier hp = hier_for(h, false, nnz);
   if (hp.use && hp.total > x) x = hp.total;
-  size_t y = layout_for(choose_plan(b, nnz), nnz).total;
+  size_t y = layout_for(choose_plan(b, nnz, h->tune), nnz).total;
   // partition (up to 2048 ranks) uses at most a single 11-bit pass
   CallPlan part;
   memset(&part, 0, sizeof part);
@@ -665,6 +688,7 @@ lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
   io.world = world;
   io.idx_base = idx_base;
   io.counts64 = send_counts;
+  io.tune = &h->tune;
   Launch L{s, nullptr, nullptr};
   ProfCtx pc;
   const bool prof = prof_begin(h, s, &pc, &L);
@@ -713,6 +737,7 @@ static lco_status partition_setup(lco_handle h, uint64_t nnz, const uint64_t* ke
   io->splitters = world > 1 ? splitters : reinterpret_cast<const uint64_t*>(send_counts);
   io->world = world;
   io->counts64 = send_counts;
+  io->tune = &h->tune;
   return LCO_OK;
 }
 
@@ -722,7 +747,7 @@ lco_status lco_partition_counts(lco_handle h, uint64_t nnz, const uint64_t* keys
   PassIO io;
   int rb = 8;
   lco_status st = partition_setup(h, nnz, keys_in, nullptr, world, splitters, send_counts,
-                                  workspace, workspace_bytes, 4096, &io, &rb);
+                                  workspace, workspace_bytes, 2048, &io, &rb);
   if (st) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = nnz == 0 ? cudaMemsetAsync(send_counts, 0, (size_t)world * 8, s)
@@ -945,7 +970,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   info->middle_size = op.middle;
   info->num_segments = op.segments;
   info->sort_bits = op.sort_bits;
-  const CallPlan cp = choose_plan(op, nnz);
+  const CallPlan cp = choose_plan(op, nnz, h->tune);
   info->passes = cp.passes;
   for (int j = 0; j < cp.passes && j < 8; ++j) info->digit_bits[j] = cp.kp.dbits[j];
   if (cp.path == kPathSeg) info->digit_bits[0] = cp.msd.b2;  // the middle digit
@@ -958,7 +983,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   info->msd_levels = cp.msd.levels;
   info->leaf_bits = cp.path == kPathMsd || cp.path == kPathLocal ? cp.msd.rb : 0;
   info->leaf_kind = (cp.path == kPathLocal || cp.path == kPathTile) ? 2
-                                                                     : (cp.path == kPathMsd ? (cp.msd.cluster ? 3 : (cp.msd.cta ? 2 : 1)) : 0);
+                                                                     : (cp.path == kPathMsd ? (cp.msd.cta ? 2 : 1) : 0);
   if (cp.path == kPathTile) info->leaf_bits = cp.msd.rb;
   info->model_bytes = cp.cost;
   info->flat_model_bytes = cp.cost;
@@ -972,7 +997,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   const Hier hp = hier_for(h, sort != 0, nnz);
   info->stages = sort ? 1 : (h->nstages >= 2 ? h->nstages : 1);
   for (int j = 0; j < h->nstages && j < 8 && !sort; ++j) {
-    const CallPlan sc = choose_plan(h->stages[j].op, nnz);
+    const CallPlan sc = choose_plan(h->stages[j].op, nnz, h->tune);
     info->stage_path[j] = sc.path;
     info->stage_sort_bits[j] = h->stages[j].op.sort_bits;
   }
@@ -983,7 +1008,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
     for (int j = 0; j < h->nstages; ++j) {
       lco_plan_info si;
       (void)si;
-      const CallPlan sc = choose_plan(h->stages[j].op, nnz);
+      const CallPlan sc = choose_plan(h->stages[j].op, nnz, h->tune);
       launches_h += sc.path == kPathCopy || sc.path == kPathLocal ? 1
                     : sc.path == kPathTile ? 3
                     : sc.path == kPathBlock ? 7

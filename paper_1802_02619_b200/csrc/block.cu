@@ -437,9 +437,8 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   if (L.mark) L.mark(L.ctx, "k_block_counts");
   k_block_counts<<<(unsigned)nct, 256, 0, L.stream>>>(gc, kb, bstart, bend, cnew, sums);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (L.mark) L.mark(L.ctx, "k_block_scan");
-  if ((e = run_count_scan(sums, nt, toff, total, Launch{L.stream, nullptr, nullptr})) != cudaSuccess)
-    return e;
+  if ((e = run_count_scan(sums, nt, toff, total, L)) != cudaSuccess) return e;
+  if (L.mark) L.mark(L.ctx, "k_scan_tiles");
   k_scan_tiles<<<(unsigned)nt, 256, 0, L.stream>>>(nblocks, cnew, toff);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // tile shape: about kBtTarget expected nonzeros, at most 32 x 32 blocks and 256 in all,
@@ -464,29 +463,11 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   g.mid = (uint32_t)bg.mid;
   const size_t smem = (size_t)kBtCap * 17;
   if (L.mark) L.mark(L.ctx, "k_block_tiles");
-  if (io.vals_out) {
-    static bool attr = false;
-    if (!attr) {
-      if ((e = cudaFuncSetAttribute(k_block_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)) != cudaSuccess)
-        return e;
-      attr = true;
-    }
-    k_block_tiles<true><<<(unsigned)ntiles, kBtThreads, smem, L.stream>>>(
-        g, kp, kb, fF, io.keys_in, io.vals_in, io.idx_in, bstart, bend, cnew, io.keys_out,
-        io.vals_out, io.perm_out);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      if ((e = cudaFuncSetAttribute(k_block_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)) != cudaSuccess)
-        return e;
-      attr = true;
-    }
-    k_block_tiles<false><<<(unsigned)ntiles, kBtThreads, smem, L.stream>>>(
-        g, kp, kb, fF, io.keys_in, io.vals_in, io.idx_in, bstart, bend, cnew, io.keys_out,
-        io.vals_out, io.perm_out);
-  }
+  auto fn = io.vals_out ? k_block_tiles<true> : k_block_tiles<false>;
+  if ((e = kernel_setup(reinterpret_cast<const void*>(fn), smem, kBtThreads)) != cudaSuccess) return e;
+  fn<<<(unsigned)ntiles, kBtThreads, smem, L.stream>>>(g, kp, kb, fF, io.keys_in, io.vals_in,
+                                                       io.idx_in, bstart, bend, cnew, io.keys_out,
+                                                       io.vals_out, io.perm_out);
   return cudaGetLastError();
 }
 

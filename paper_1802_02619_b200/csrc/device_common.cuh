@@ -134,6 +134,9 @@ struct PassParams {
   // with match.any instead of one ballot per digit bit when tiles hold few distinct digits
   uint32_t* distinct;
   int adapt;  // host side: run_pass points `distinct` into its control block
+  // MSD passes of lco_permute: slots inside a tile's digit run in any order (k_scatter
+  // UNST); the leaves order records by (remaining q bits, K'), unique for unique keys
+  int unstable;
 };
 
 // PER consecutive uint16 tile-histogram entries in, PER uint32 offsets out (vector

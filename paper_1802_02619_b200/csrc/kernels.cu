@@ -233,7 +233,10 @@ constexpr size_t scatter_smem_bytes() {
 // NT threads (IT = kTile / NT nonzeros each): 512 for digits of <= 10 bits (more warps
 // in flight per SM, half the serial work per thread), 256 for 11-bit digits (whose
 // per-warp counters would not fit in sV with 16 warps).
-template <int RB, bool FIRST, bool LAST, bool VALS, int NT, bool ADAPT = false>
+// UNST (MSD passes of lco_permute, unique keys): the order inside a tile's digit run is
+// free, because every leaf sorts its records on (remaining bits of q, K') and K' is unique
+// -- so a record takes its slot with one shared atomic (no per-warp counters, no ballots).
+template <int RB, bool FIRST, bool LAST, bool VALS, int NT, bool ADAPT = false, bool UNST = false>
 __global__ void __launch_bounds__(NT, 2)
     k_scatter(const __grid_constant__ PassParams a, const __grid_constant__ ScatterIO io) {
   constexpr int BINS = 1 << RB;
@@ -277,7 +280,11 @@ __global__ void __launch_bounds__(NT, 2)
       prefetch_l2(io.toff + (size_t)t2 * BINS, (size_t)BINS * 4);
     }
   }
-  for (int i = tid; i < W * BINS / 2; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
+  if (UNST) {
+    for (int i = tid; i < BINS; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
+  } else {
+    for (int i = tid; i < W * BINS / 2; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
+  }
   // ---- load keys; warp w owns a contiguous slice, lanes consecutive ----
   uint64_t key[IT];
   uint32_t meta[IT];
@@ -320,6 +327,43 @@ __global__ void __launch_bounds__(NT, 2)
     }
   }
   __syncthreads();
+  if (UNST) {
+    // ---- unordered slots: one shared atomic per record on the tile's digit counter;
+    // tiles with few distinct digits aggregate a warp's equal digits first (match.any)
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(whist);
+    const bool few = ADAPT && *a.distinct < (uint64_t)((a.tiles + 31) / 32) *
+                                                ((1u << a.kp.dbits[a.pass]) / 8);
+    if (few) {
+      const uint32_t ltm = lanemask_lt();
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const uint32_t d = meta[it];
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t base = 0;
+        if (d != kInvalid && (peers & ltm) == 0) base = atomicAdd(&cnt[d], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, __ffs(peers) - 1);
+        if (d != kInvalid) meta[it] = d | ((base + __popc(peers & ltm)) << 16);
+      }
+    } else {
+#pragma unroll
+      for (int it = 0; it < IT; ++it) {
+        const uint32_t d = meta[it];
+        if (d != kInvalid) meta[it] = d | (atomicAdd(&cnt[d], 1u) << 16);
+      }
+    }
+    __syncthreads();
+    block_scan_bins<NT, BINS>(cnt, loff, s_warp);
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const uint32_t d = meta[it] & 0xFFFFu;
+      if (d != kInvalid) {
+        const uint32_t lp = loff[d] + (meta[it] >> 16);
+        sK[lp] = key[it];
+        sdig[lp] = (uint16_t)d;
+        meta[it] = d | (lp << 16);
+      }
+    }
+  } else {
   // ---- warp-level stable ranking into per-warp digit counters ----
   uint16_t* wh = whist + warp * BINS;
   const uint32_t ltm = lanemask_lt();
@@ -388,6 +432,7 @@ __global__ void __launch_bounds__(NT, 2)
       meta[it] = d | (lp << 16);
     }
   }
+  }  // stable ranking
   __syncthreads();  // the warp counters (in sV) are dead from here on
   // ---- gather values / positions into their slots (cp.async, global -> shared) ----
   const bool want_p = io.pout != nullptr || io.direct;
@@ -478,44 +523,14 @@ __global__ void __launch_bounds__(512) k_keyhist(const __grid_constant__ KeyPlan
 // ---------------------------------------------------------------------------------
 // Launchers (called from api.cu)
 // ---------------------------------------------------------------------------------
-template <int RB>
-static cudaError_t set_smem_attrs() {
-  static bool done = false;
-  if (done) return cudaSuccess;
-  const int bytes = (int)scatter_smem_bytes<RB>();
-  cudaError_t e = cudaSuccess;
-#define LCO_ATTR(F, L, V)                                                       \
-  e = cudaFuncSetAttribute(k_scatter<RB, F, L, V, scatter_nt(RB)>,              \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-  if (e != cudaSuccess) return e;                                               \
-  e = cudaFuncSetAttribute(k_scatter<RB, F, L, V, scatter_nt(RB), true>,        \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); \
-  if (e != cudaSuccess) return e;
-  LCO_ATTR(true, true, false)
-  LCO_ATTR(true, true, true)
-  LCO_ATTR(true, false, false)
-  LCO_ATTR(true, false, true)
-  LCO_ATTR(false, false, false)
-  LCO_ATTR(false, false, true)
-  LCO_ATTR(false, true, false)
-  LCO_ATTR(false, true, true)
-#undef LCO_ATTR
-  done = true;
-  return cudaSuccess;
-}
-
 uint64_t pass_tiles(uint64_t nnz) { return (nnz + kTile - 1) / kTile; }
 
 // L2 prefetch distance of the pass kernels: one wave of resident CTAs (2 per SM), so a
 // CTA brings the tile its successor on the same SM will load into L2 (measured: -3 to
 // -6 % on the C4 / C5 / C3a passes).
 uint32_t prefetch_distance() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
-  }
+  int sms = 148;
+  if (device_sms(&sms) != cudaSuccess) sms = 148;
   return (uint32_t)sms;
 }
 int pass_tile() { return kTile; }
@@ -573,33 +588,33 @@ cudaError_t launch_count(int rb, bool first, const PassParams& a, const uint64_t
   return cudaErrorInvalidValue;
 }
 
+template <int RB, bool F, bool LST>
+static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const ScatterIO& io,
+                                   uint32_t grid, cudaStream_t s) {
+  constexpr int NT = scatter_nt(RB);
+  const size_t smem = scatter_smem_bytes<RB>();
+  void (*fn)(const PassParams, const ScatterIO);
+  if (a.unstable && !LST) {  // MSD passes of lco_permute (the last pass is never one)
+    if (a.distinct) fn = vals ? k_scatter<RB, F, false, true, NT, true, true> : k_scatter<RB, F, false, false, NT, true, true>;
+    else fn = vals ? k_scatter<RB, F, false, true, NT, false, true> : k_scatter<RB, F, false, false, NT, false, true>;
+  } else if (a.distinct) {
+    fn = vals ? k_scatter<RB, F, LST, true, NT, true> : k_scatter<RB, F, LST, false, NT, true>;
+  } else {
+    fn = vals ? k_scatter<RB, F, LST, true, NT> : k_scatter<RB, F, LST, false, NT>;
+  }
+  cudaError_t e = kernel_setup(reinterpret_cast<const void*>(fn), smem, NT);
+  if (e != cudaSuccess) return e;
+  fn<<<grid, NT, smem, s>>>(a, io);
+  return cudaGetLastError();
+}
+
 template <int RB>
 static cudaError_t launch_scatter_rb(bool first, bool last, bool vals, const PassParams& a,
                                      const ScatterIO& io, uint32_t grid, cudaStream_t s) {
-  cudaError_t e = set_smem_attrs<RB>();
-  if (e != cudaSuccess) return e;
-  const size_t smem = scatter_smem_bytes<RB>();
-  constexpr int NT = scatter_nt(RB);
-#define LCO_LAUNCH(F, LST)                                                     \
-  if (a.distinct) {                                                            \
-    if (vals) k_scatter<RB, F, LST, true, NT, true><<<grid, NT, smem, s>>>(a, io); \
-    else k_scatter<RB, F, LST, false, NT, true><<<grid, NT, smem, s>>>(a, io);     \
-  } else if (vals) {                                                           \
-    k_scatter<RB, F, LST, true, NT><<<grid, NT, smem, s>>>(a, io);             \
-  } else {                                                                     \
-    k_scatter<RB, F, LST, false, NT><<<grid, NT, smem, s>>>(a, io);            \
-  }
-  if (first && last) {
-    LCO_LAUNCH(true, true)
-  } else if (first) {
-    LCO_LAUNCH(true, false)
-  } else if (!last) {
-    LCO_LAUNCH(false, false)
-  } else {
-    LCO_LAUNCH(false, true)
-  }
-#undef LCO_LAUNCH
-  return cudaGetLastError();
+  if (first && last) return launch_scatter_t<RB, true, true>(vals, a, io, grid, s);
+  if (first) return launch_scatter_t<RB, true, false>(vals, a, io, grid, s);
+  if (!last) return launch_scatter_t<RB, false, false>(vals, a, io, grid, s);
+  return launch_scatter_t<RB, false, true>(vals, a, io, grid, s);
 }
 
 cudaError_t launch_scatter(int rb, bool first, bool last, bool vals, const PassParams& a,
@@ -714,7 +729,7 @@ cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch
   a.splitters = io.splitters;
   a.world = io.world;
   // LSD passes choose their ranking from the distinct digits per tile (k_count samples)
-  a.adapt = !part && !getenv("LCO_NO_MATCH");
+  a.adapt = !part && !(io.tune && io.tune->no_match);
   for (int j = 0; j < P; ++j) {
     cudaError_t e = run_pass(rb, a, io, j, j == 0, j == P - 1, L);
     if (e != cudaSuccess) return e;
@@ -757,13 +772,8 @@ cudaError_t run_validate(uint64_t nnz, const uint64_t* keys, uint64_t total, int
 
 cudaError_t run_keyhist(const KeyPlan& kp, uint64_t nnz, const uint64_t* keys, int shift,
                         int bins, uint64_t* counts, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_keyhist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         16384 * 4);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = kernel_setup(reinterpret_cast<const void*>(k_keyhist), 16384 * 4, 0);
+  if (e != cudaSuccess) return e;
   const int grid = (int)umin64((nnz + 511) / 512, 148 * 2);
   k_keyhist<<<grid > 0 ? grid : 1, 512, (size_t)bins * 4, s>>>(
       kp, keys, nnz, shift, bins, reinterpret_cast<unsigned long long*>(counts));

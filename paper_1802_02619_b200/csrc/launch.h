@@ -7,6 +7,13 @@
 
 namespace lco {
 
+// Per-device, thread-safe one-time setup of a kernel (runtime.cu): raises its dynamic
+// shared-memory limit on the current device when smem > 48 KB and returns the resident
+// CTAs per SM (per_sm) and the device's SM count (sms), either pointer may be null.
+cudaError_t kernel_setup(const void* fn, size_t smem, int threads, int* per_sm = nullptr,
+                         int* sms = nullptr);
+cudaError_t device_sms(int* sms);  // SM count of the current device (cached per device)
+
 struct Launch {
   cudaStream_t stream;
   void (*mark)(void* ctx, const char* name);  // profiling hook (before each launch)
@@ -46,6 +53,9 @@ struct PassIO {
   uint32_t idx_base;
   uint64_t* counts64;
   const DirectOut* direct;  // partition: scatter into the receivers' buffers
+  const Tuning* tune;       // the handle's schedule overrides (never null on a call)
+  int unique;               // keys are unique (lco_permute's precondition): MSD passes may
+                            // place records unordered inside a digit run (k_scatter UNST)
 };
 
 // Pointers into a pass control block (pass_ctrl_bytes()).
@@ -68,7 +78,6 @@ struct MsdPlan {
   int rb;
   int cta;     // leaves sorted by one CTA per leaf instead of k_leafw (one warp)
   int staged;  // CTA leaves of <= ~2K nonzeros: the fully staged k_leafs
-  int cluster; // one-level plans: buckets sorted by a CTA cluster in DSMEM (k_leafx)
 };
 
 struct PassParams;
@@ -76,7 +85,6 @@ struct ScatterIO;
 
 uint64_t pass_tiles(uint64_t nnz);
 uint32_t prefetch_distance();  // L2 prefetch distance of the pass kernels (tiles)
-uint32_t cluster_leaf_cap();   // largest level-1 bucket a k_leafx cluster sorts
 int pass_tile();
 int pass_rb(int bits);
 size_t pass_ctrl_bytes(int rb, uint64_t nnz);

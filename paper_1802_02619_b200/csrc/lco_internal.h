@@ -227,6 +227,25 @@ struct StagePlan {
   OpPlan op;
 };
 
+// Schedule overrides for tests and A/B measurements.  lco_create reads them ONCE from the
+// environment into the handle (read_tuning, api.cu); no call ever reads the environment.
+// All zero = the default schedule (DESIGN.md §2 lists the variables).
+struct Tuning {
+  int no_tile;      // LCO_NO_TILE: no segment-local tile schedule
+  int no_block;     // LCO_NO_BLOCK: no block transpose
+  int no_seg;       // LCO_NO_SEG: no segmented single pass
+  int msd_force;    // LCO_MSD: MSD schedule whenever it applies
+  int msd_b1;       // LCO_MSD_B1 (0: default), clamped to 4..11
+  int msd_b2;       // LCO_MSD_B2 (0: default), clamped to 4..11
+  int msd_cta;      // LCO_MSD_CTA: -1 default, 0 warp leaves, 1 CTA leaves
+  int leafs_force;  // LCO_LEAFS: fully staged CTA leaves whenever they fit
+  int no_leafs;     // LCO_NO_LEAFS
+  int no_leafr;     // LCO_NO_LEAFR
+  int no_match;     // LCO_NO_MATCH: LSD passes never rank with match.any
+  int lsd_maxbits;  // LCO_LSD_MAXBITS (0: default), clamped to 1..11
+  int stable_msd;   // LCO_STABLE_MSD: MSD passes of lco_permute ranked stably
+};
+
 }  // namespace lco
 
 struct lco_plan_s {
@@ -242,6 +261,7 @@ struct lco_plan_s {
   int prefix_len, suffix_start;
   uint64_t max_nnz;
   uint32_t flags;
+  lco::Tuning tune;        // read once at lco_create
   lco::OpPlan op_permute;  // nnz-independent parts; path refined per call
   lco::OpPlan op_sort;
   lco::KeyPlan kp_full;    // re-encode only (partition, histogram)
@@ -260,7 +280,7 @@ namespace lco {
 constexpr int kProfStages = 48;
 // Host planning (plan.cpp)
 lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int32_t* perm);
-void choose_passes(OpPlan* op, int sort_bits);
+void choose_passes(OpPlan* op, int sort_bits, int max_digit);  // max_digit 0: default
 void build_digit_moves(KeyPlan* kp);  // after dshift / dbits are final (pow2 plans)
 int ceil_log2(uint64_t x);  // smallest b with 2^b >= x
 void set_error(const char* fmt, ...);

@@ -61,7 +61,7 @@ FastDiv make_fastdiv(uint64_t d) {
 
 // Digit schedule: P = ceil(bits / 11) passes of <= 11 bits, as even as possible
 // (results do not depend on the digit size).
-void choose_passes(OpPlan* op, int bits) {
+void choose_passes(OpPlan* op, int bits, int max_digit) {
   op->sort_bits = bits;
   if (bits <= 0) {
     op->passes = 0;
@@ -71,8 +71,9 @@ void choose_passes(OpPlan* op, int bits) {
   // digits of <= 10 bits unless one 11-bit pass does it all: an 11-bit digit writes runs
   // of ~2 nonzeros per bucket per 4,096-nonzero tile and ran at half the speed of a 7-bit
   // one (C3a: 11 + 10 bits 0.66 ms, 7 + 7 + 7 bits 0.60 ms; 10-bit digits as fast as 8)
-  const int kMaxDigit =
-      getenv("LCO_LSD_MAXBITS") ? atoi(getenv("LCO_LSD_MAXBITS")) : (bits <= 11 ? 11 : 10);
+  int kMaxDigit = max_digit > 0 ? (max_digit > 11 ? 11 : max_digit) : (bits <= 11 ? 11 : 10);
+  // at most kMaxPasses passes (64-bit keys need digits of >= 8 bits)
+  if ((bits + kMaxDigit - 1) / kMaxDigit > kMaxPasses) kMaxDigit = (bits + kMaxPasses - 1) / kMaxPasses;
   int P = (bits + kMaxDigit - 1) / kMaxDigit;
   int b = (bits + P - 1) / P;
   op->passes = P;
@@ -227,7 +228,7 @@ static void normalize(int order, const uint64_t* dims, const int32_t* perm, Flat
 }
 
 // The flat plan: sort on q = K' div T (prefix + middle digits), T = prod of suffix dims.
-static void flat_permute(const FlatInfo& fi, OpPlan* op) {
+static void flat_permute(const FlatInfo& fi, OpPlan* op, int max_digit) {
   const int n = fi.n, a = fi.a, b = fi.b;
   const uint64_t* nd = fi.nd;
   const int32_t* np = fi.np;
@@ -244,10 +245,10 @@ static void flat_permute(const FlatInfo& fi, OpPlan* op) {
   op->segdiv = D;
   if (n <= 1) {
     op->path = kPathCopy;
-    choose_passes(op, 0);
+    choose_passes(op, 0, max_digit);
   } else {
     op->path = kPathOnesweep;
-    choose_passes(op, ceil_log2(G * S));
+    choose_passes(op, ceil_log2(G * S), max_digit);
   }
   // block-transpose schedule (block.cu): blocks = old modes 0..k
   op->nblocks = 0;
@@ -317,7 +318,7 @@ static void build_stages(lco_plan_s* h, const FlatInfo& fi) {
         if (O[j] == On[i]) S.perm[i] = j;
     FlatInfo sfi;
     normalize(n, S.dims, S.perm, &sfi);
-    flat_permute(sfi, &S.op);
+    flat_permute(sfi, &S.op, h->tune.lsd_maxbits);
     for (int i = 0; i < n; ++i) O[i] = On[i];
     t = u;
   }
@@ -373,7 +374,7 @@ lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int3
   }
   h->prefix_len = fi.a;
   h->suffix_start = fi.b;
-  flat_permute(fi, &h->op_permute);
+  flat_permute(fi, &h->op_permute, h->tune.lsd_maxbits);
   build_stages(h, fi);
   // sort: q = K' (all key digits)
   OpPlan& os = h->op_sort;
@@ -385,10 +386,10 @@ lco_status build_plan(lco_plan_s* h, int order, const uint64_t* dims, const int3
   os.segdiv = total;
   if (total <= 1) {
     os.path = kPathCopy;
-    choose_passes(&os, 0);
+    choose_passes(&os, 0, h->tune.lsd_maxbits);
   } else {
     os.path = kPathOnesweep;
-    choose_passes(&os, h->key_bits);
+    choose_passes(&os, h->key_bits, h->tune.lsd_maxbits);
   }
   h->kp_full = make_keyplan(n, nd, fi.np, 1);
   return LCO_OK;

@@ -130,6 +130,14 @@ def lib():
                     raise ImportError(
                         f"{LIB_PATH} is missing; build it with "
                         "`python -c 'import __graft_entry__ as g; g.build()'`")
+                from . import _build
+                if not _build.up_to_date():
+                    # the .so does not match the sources (content hash): never run a stale
+                    # binary; rebuild in place (nvcc is part of the image)
+                    import sys
+                    print(f"[lco] {LIB_PATH} is stale for the current sources; rebuilding",
+                          file=sys.stderr, flush=True)
+                    _build.build(force=True)
                 L = ctypes.CDLL(LIB_PATH)
                 for name, (res, args) in _SIGS.items():
                     f = getattr(L, name)
@@ -166,6 +174,35 @@ def _workspace(nbytes, device):
     buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
     off = (-buf.data_ptr()) % 256
     return buf, off
+
+
+def _on(stream, device):
+    """Allocate on and launch into `stream` (default: the current stream): workspace and
+    outputs this module allocates then belong to that stream in the caching allocator,
+    so their memory is never reused while the call's kernels run, and zero-fills are
+    ordered before them."""
+    return _Ctx(stream, device)
+
+
+class _Ctx:
+    def __init__(self, stream, device):
+        cuda = torch.device(device).type == "cuda"  # else the call itself raises
+        self.d = torch.cuda.device(device) if cuda else None
+        self.s = torch.cuda.stream(stream) if (stream is not None and cuda) else None
+
+    def __enter__(self):
+        if self.d is not None:
+            self.d.__enter__()
+        if self.s is not None:
+            self.s.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self.s is not None:
+            self.s.__exit__(*exc)
+        if self.d is not None:
+            self.d.__exit__(*exc)
+        return False
 
 
 class Plan:
@@ -246,7 +283,7 @@ class Plan:
             "tile": pi.tile,
             "msd_levels": pi.msd_levels,
             "leaf_bits": pi.leaf_bits,
-            "leaf_kind": {0: None, 1: "warp", 2: "cta", 3: "cluster"}.get(pi.leaf_kind, pi.leaf_kind),
+            "leaf_kind": {0: None, 1: "warp", 2: "cta"}.get(pi.leaf_kind, pi.leaf_kind),
             "model_bytes": pi.model_bytes,
             "stages": pi.stages,
             "stage_paths": [PATHS.get(x, x) for x in pi.stage_path[:pi.stages]] if pi.stages > 1 else [],
@@ -299,6 +336,12 @@ class Plan:
         """Index-matched addition (lco_add): A + sign * permute(B, match) where this plan
         holds B's dims and the match.  Returns (keys_c, vals_c, nnz_c); with trim=True the
         outputs are cut to nnz_c (one device->host read of the count)."""
+        with _on(stream, keys_a.device):
+            return self._add_impl(keys_a=keys_a, vals_a=vals_a, keys_b=keys_b, vals_b=vals_b,
+                                  sign=sign, stream=stream, out=out, workspace=workspace, trim=trim)
+
+    def _add_impl(self, keys_a, vals_a, keys_b, vals_b, sign=1.0, stream=None, out=None,
+            workspace=None, trim=True):
         for t in (keys_a, vals_a, keys_b, vals_b):
             if not t.is_cuda:
                 raise ValueError("operands must be CUDA tensors (no CPU fallback)")
@@ -333,15 +376,25 @@ class Plan:
 
     def permute(self, keys, vals=None, idx=None, return_perm=True, stream=None, out=None,
                 workspace=None):
-        return self._run(lib().lco_permute, keys, vals, idx, return_perm, stream, out, workspace)
+        with _on(stream, keys.device):
+            return self._run(lib().lco_permute, keys, vals, idx, return_perm, stream, out,
+                             workspace)
 
     def sort(self, keys, vals=None, idx=None, return_perm=True, stream=None, out=None,
              workspace=None):
-        return self._run(lib().lco_sort, keys, vals, idx, return_perm, stream, out, workspace)
+        with _on(stream, keys.device):
+            return self._run(lib().lco_sort, keys, vals, idx, return_perm, stream, out, workspace)
 
     def permute_host(self, keys, vals=None, return_perm=True, device=None, stream=None,
                      out=None, workspace=None):
         """Host (ideally pinned) tensors in and out; copies run inside the call."""
+        with _on(stream, torch.device(device or 'cuda')):
+            return self._permute_host_impl(keys=keys, vals=vals, return_perm=return_perm,
+                                           device=device, stream=stream, out=out,
+                                           workspace=workspace)
+
+    def _permute_host_impl(self, keys, vals=None, return_perm=True, device=None, stream=None,
+                     out=None, workspace=None):
         if keys.is_cuda:
             raise ValueError("permute_host takes host tensors")
         dev = torch.device(device or "cuda")
@@ -367,6 +420,11 @@ class Plan:
     def partition(self, keys, vals, idx_base, splitters, stream=None, workspace=None):
         """Stable multisplit by new-key range: returns (send_keys, send_vals, send_idx,
         send_counts) on the device; send_keys are OLD keys."""
+        with _on(stream, keys.device):
+            return self._partition_impl(keys=keys, vals=vals, idx_base=idx_base,
+                                        splitters=splitters, stream=stream, workspace=workspace)
+
+    def _partition_impl(self, keys, vals, idx_base, splitters, stream=None, workspace=None):
         dev = keys.device
         n = keys.numel()
         world = 1 if splitters is None else splitters.numel() + 1
@@ -389,6 +447,11 @@ class Plan:
 
     def partition_counts(self, keys, splitters, stream=None, workspace=None):
         """Records per destination rank of the multisplit (device int64[world])."""
+        with _on(stream, keys.device):
+            return self._partition_counts_impl(keys=keys, splitters=splitters, stream=stream,
+                                               workspace=workspace)
+
+    def _partition_counts_impl(self, keys, splitters, stream=None, workspace=None):
         dev = keys.device
         n = keys.numel()
         world = 1 if splitters is None else splitters.numel() + 1
@@ -410,6 +473,15 @@ class Plan:
         """The partition with the exchange fused in: records go straight into the
         receivers' buffers (lists of device tensors, peer-mapped on a multi-GPU box) at
         recv_offsets[d] + index.  Returns the device send counts."""
+        with _on(stream, keys.device):
+            return self._partition_direct_impl(keys=keys, vals=vals, idx_base=idx_base,
+                                               splitters=splitters, recv_keys=recv_keys,
+                                               recv_vals=recv_vals, recv_idx=recv_idx,
+                                               recv_offsets=recv_offsets, stream=stream,
+                                               workspace=workspace)
+
+    def _partition_direct_impl(self, keys, vals, idx_base, splitters, recv_keys, recv_vals, recv_idx,
+                         recv_offsets, stream=None, workspace=None):
         dev = keys.device
         n = keys.numel()
         world = 1 if splitters is None else splitters.numel() + 1
@@ -436,9 +508,9 @@ class Plan:
 
     def key_histogram(self, keys, bits, counts=None, stream=None):
         dev = keys.device
-        if counts is None:
-            counts = torch.zeros(1 << bits, dtype=torch.int64, device=dev)
-        with torch.cuda.device(dev):
+        with _on(stream, dev):
+            if counts is None:
+                counts = torch.zeros(1 << bits, dtype=torch.int64, device=dev)
             _check(lib().lco_key_histogram(self._h, keys.numel(), _ptr(keys), int(bits),
                                            _ptr(counts), _stream_ptr(stream, dev)))
         return counts
@@ -462,8 +534,11 @@ _plan_cache: dict = {}
 
 
 def plan(dims, perm=None, max_nnz=(1 << 32) - 1, validate=False, hierarchical=False) -> Plan:
+    # the library reads its LCO_* schedule overrides once per handle (lco_create): a
+    # cached handle is only reused under the same overrides
+    env = tuple(sorted((k, v) for k, v in os.environ.items() if k.startswith("LCO_")))
     key = (tuple(int(d) for d in dims), None if perm is None else tuple(int(p) for p in perm),
-           int(max_nnz), bool(validate), bool(hierarchical))
+           int(max_nnz), bool(validate), bool(hierarchical), env)
     p = _plan_cache.get(key)
     if p is None:
         p = _plan_cache[key] = Plan(dims, perm, max_nnz, validate, hierarchical)

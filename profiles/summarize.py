@@ -63,9 +63,13 @@ def launches(path, out, traffic_key=None):
 
 
 def marker_traffic(path, markers):
-    """DRAM bytes (read + write) per launch of each bench marker: the launch list's kernels
-    of this library, in launch order, zipped cyclically with the marker names of one call
-    (bench.py kernels_ms keys; one launch per marker), averaged over the calls."""
+    """DRAM bytes (read + write) per launch of the kernel behind each bench marker.
+
+    `markers` is one call's launch sequence (bench.py "markers"); the launch list's kernels
+    of this library, in launch order, must repeat it exactly: each launch's kernel name
+    (before the template arguments) must equal its marker or prefix it up to a "_"
+    (k_scatter<10, ...> for k_scatter_seg).  Any mismatch raises instead of keying bytes
+    to the wrong kernel.  Returns {marker: {"kernel": ncu name, "bytes": mean per launch}}."""
     rows = list(csv.reader(l for l in open(path) if not l.startswith("==")))
     hdr = rows[0]
     ki, mi, vi = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value"))
@@ -75,15 +79,22 @@ def marker_traffic(path, markers):
         if len(r) != len(hdr):
             continue
         k = short(r[ki])
-        if not any(k.startswith(o) for o in OURS) and not k.startswith("k_"):
+        if not k.startswith("k_"):
             continue
         per.setdefault(r[idi], {"name": k})[r[mi]] = float(r[vi].replace(",", ""))
     launches = list(per.values())
+    if not markers or len(launches) % len(markers):
+        raise ValueError(f"{len(launches)} launches do not repeat the {len(markers)} markers")
     out = collections.defaultdict(list)
+    names = {}
     for j, l in enumerate(launches):
-        out[markers[j % len(markers)]].append(l.get("dram__bytes_read.sum", 0.0)
-                                              + l.get("dram__bytes_write.sum", 0.0))
-    return {m: sum(v) / len(v) for m, v in out.items()}
+        m = markers[j % len(markers)]
+        base = l["name"].split("<")[0]
+        if not (m == base or m.startswith(base + "_")):
+            raise ValueError(f"launch {j}: kernel {l['name']} does not match marker {m}")
+        names[m] = l["name"]
+        out[m].append(l.get("dram__bytes_read.sum", 0.0) + l.get("dram__bytes_write.sum", 0.0))
+    return {m: {"kernel": names[m], "bytes": sum(v) / len(v)} for m, v in out.items()}
 
 
 WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",

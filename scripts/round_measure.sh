@@ -1,30 +1,29 @@
 #!/bin/bash
 # End-of-milestone measurement on one B200 (gpurun): gpu tests, one bench line per
-# BASELINE config (with e2e and the CPU-oracle baseline), the C5 launch list and full
-# ncu captures of the dominant kernels of C5 and C4.  Outputs under gpurun_out/.
+# BASELINE config (with e2e and the CPU-oracle baselines), every config's ncu launch list
+# (kernel times + DRAM bytes: the per-marker traffic bench.py reports) and full ncu
+# captures of the dominant kernels of C5 and C4.  Outputs under gpurun_out/.
+# usage: bash scripts/round_measure.sh [notests]
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/m_tests.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/m_tests.log
+if [ "$1" != "notests" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/m_tests.log 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/m_tests.log
+fi
 for c in C5 C4 C3a C3b C2a C2b C1; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/m_bench_$c.json 2> gpurun_out/m_bench_$c.err
   echo "bench $c rc=$?"
 done
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/m_ref_C5.json 2> gpurun_out/m_ref_C5.err; echo "ref rc=$?"
-python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    --csv --log-file gpurun_out/m_c5_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_launch.log 2>&1
-echo "launches rc=$?"
+for c in C5 C4 C3a C3b C2a C2b C1; do
+  lc=$(echo $c | tr A-Z a-z)
+  python bench.py --config $c --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain_$c.log 2>&1 && \
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      --csv --log-file gpurun_out/m_${lc}_launches.csv python bench.py --config $c --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_launch_$c.log 2>&1
+  echo "launches $c rc=$?"
+done
 ncu --set full --clock-control none --import-source on -k regex:"k_leaf|k_scatter" -s 4 -c 3 \
     -o gpurun_out/m_c5_full -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_c5.log 2>&1
 echo "c5 full rc=$?"
-python bench.py --config C4 --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain4.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    --csv --log-file gpurun_out/m_c4_launches.csv python bench.py --config C4 --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_launch4.log 2>&1
-echo "c4 launches rc=$?"
-python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain4b.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_block_tiles|k_block_bounds" -s 2 -c 2 \
     -o gpurun_out/m_c4_full -f python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_c4.log 2>&1
 echo "c4 full rc=$?"
 python benchmarks/table2.py --reps 5 --out gpurun_out/m_table2.md > gpurun_out/m_table2.log 2>&1; echo "table2 rc=$?"
-python benchmarks/addition.py --out gpurun_out/m_addition.json > gpurun_out/m_addition.log 2>&1; echo "addition rc=$?"
-python benchmarks/addition.py --hierarchical --n 2896 --out gpurun_out/m_addition_hier.json > gpurun_out/m_addition_hier.log 2>&1; echo "addition hier rc=$?"
-python benchmarks/mdt.py --out gpurun_out/m_mdt.json > gpurun_out/m_mdt.log 2>&1; echo "mdt rc=$?"

@@ -26,16 +26,16 @@ import summarize  # noqa: E402
 
 traffic = {}
 # per bench marker (what bench.py's roofline.traffic looks up), from the launch lists
-for c in ("C5", "C4"):
+for c in ("C5", "C4", "C3a", "C3b", "C2a", "C2b", "C1"):
     lpath = os.path.join(G, f"m_{c.lower()}_launches.csv")
     bpath = os.path.join(G, f"m_bench_{c}.json")
     if os.path.exists(lpath) and os.path.exists(bpath):
-        markers = [m for m in json.load(open(bpath))["kernels_ms"]]
-        traffic.setdefault(c, {}).update(summarize.marker_traffic(lpath, markers))
-        if c == "C4":
-            shutil.copy(lpath, os.path.join(P, f"{tag}_c4_launches.csv"))
+        markers = json.load(open(bpath))["markers"]  # one call's launch sequence
+        traffic[c] = summarize.marker_traffic(lpath, markers)
+        if c != "C5":
+            shutil.copy(lpath, os.path.join(P, f"{tag}_{c.lower()}_launches.csv"))
             subprocess.check_call([sys.executable, summ, "launches", lpath,
-                                   os.path.join(P, f"{tag}_c4_launches.md")])
+                                   os.path.join(P, f"{tag}_{c.lower()}_launches.md")])
 for c, rep in (("C5", "m_c5_full.ncu-rep"), ("C4", "m_c4_full.ncu-rep")):
     path = os.path.join(G, rep)
     if not os.path.exists(path):
@@ -55,7 +55,8 @@ for c, rep in (("C5", "m_c5_full.ncu-rep"), ("C4", "m_c4_full.ncu-rep")):
         name = row[ki].split("(")[0].replace("void ", "").replace("lco::", "")
         b = float(row[r]) * scale.get(units[r], 1) + float(row[w]) * scale.get(units[w], 1)
         per.setdefault(name, []).append(b)
-    traffic.setdefault(c, {}).update({k: sum(v) / len(v) for k, v in per.items()})
+    # full-capture bytes by exact ncu kernel name (beside the per-marker launch-list bytes)
+    traffic.setdefault(c, {})["by_kernel"] = {k: sum(v) / len(v) for k, v in per.items()}
 tp = os.path.join(P, "traffic.json")
 old = json.load(open(tp)) if os.path.exists(tp) else {}
 old.update(traffic)

@@ -424,30 +424,6 @@ def test_msd_leaf_variants(env, cuda_device, monkeypatch):
         check(dims, (1, 4, 0, 3, 2), keys, None)
 
 
-@pytest.mark.parametrize("dims,perm,nnz", [((4096, 4096, 16), (1, 0, 2), 3_000_000),
-                                           ((256,) * 4, (3, 2, 1, 0), 4_000_000),
-                                           ((3000, 3000, 50), (1, 0, 2), 5_000_000),
-                                           ((1 << 16, 4096), (1, 0), 3_000_000)])
-def test_cluster_leaves(dims, perm, nnz, cuda_device, monkeypatch):
-    """One 8-bit MSD pass, then every bucket sorted by a cluster of 16 CTAs in DSMEM
-    (k_leafx, opt-in): 4..16 remaining bits, a non-power-of-two middle, and (2^16 x 4096)
-    buckets whose ~700 nonzeros per key crowd one key bucket -> whole buckets deferred
-    to the block-level kernel; and C3a at full size."""
-    monkeypatch.setenv("LCO_CLUSTER", "1")
-    rng = np.random.default_rng(nnz + len(dims))
-    keys, vals = _rand_sorted(rng, dims, nnz)
-    info = lco.plan(dims, perm).info(len(keys))
-    assert info["path"] == "msd" and info["leaf_kind"] == "cluster", info
-    check(dims, perm, keys, vals)
-    check(dims, perm, keys, None, return_perm=False)
-    idx = rng.permutation(len(keys)).astype(np.uint32)
-    check(dims, perm, keys, vals, idx=idx)
-    if nnz == 3_000_000 and len(dims) == 3:
-        w = workloads.config("C3")
-        assert lco.plan(w.dims, w.perms[0]).info(w.keys.numel())["leaf_kind"] == "cluster"
-        check(w.dims, w.perms[0], _np_u64(w.keys), w.vals.numpy())
-
-
 # ------------------------------------------------------------------ segmented single pass
 @pytest.mark.parametrize("dims,perm,nnz", [((256, 16, 64, 32), (0, 2, 1, 3), 1_000_000),
                                            ((128, 16, 2048, 4), (0, 2, 1, 3), 1_000_000),
@@ -650,3 +626,50 @@ def test_block_path(dims, perm, cuda_device):
     w = workloads.config("C4", scale=300)
     assert lco.plan(w.dims, w.perms[0]).info(w.keys.numel())["path"] == "block"
     check(w.dims, w.perms[0], _np_u64(w.keys), w.vals.numpy())
+
+
+# ------------------------------------------------------------------ concurrency (lco.h threading)
+def test_one_handle_two_threads_two_streams(cuda_device):
+    """include/lco.h: a handle may be used concurrently from several host threads on
+    different streams with different workspaces.  Two threads drive one handle on two
+    streams (C5-shaped MSD schedule and a C3b-shaped LSD schedule alternate), every
+    result bit-exact with the oracle."""
+    import threading
+    rng = np.random.default_rng(99)
+    dims, perm = (4096,) * 5, (4, 3, 2, 1, 0)
+    keys = np.unique(rng.integers(0, 2 ** 60, 2_100_000, dtype=np.int64))[:2_000_000].astype(np.uint64)
+    vals = rng.standard_normal(len(keys))
+    ek, ev, ep = oracle.permute(dims, perm, keys, vals)
+    p = lco.Plan(dims, perm)
+    k = torch.as_tensor(keys.view(np.int64)).to(cuda_device)
+    v = torch.as_tensor(vals).to(cuda_device)
+    errors, results = [], {}
+
+    def work(tid):
+        try:
+            st = torch.cuda.Stream(device=cuda_device)
+            ws = torch.empty(p.workspace_size(len(keys)) + 256, dtype=torch.uint8, device=cuda_device)
+            outs = []
+            for _ in range(4):
+                with torch.cuda.stream(st):
+                    ko = torch.empty_like(k)
+                    vo = torch.empty_like(v)
+                    po = torch.empty(len(keys), dtype=torch.int32, device=cuda_device)
+                p.permute(k, v, out=(ko, vo, po), workspace=ws, stream=st)
+                outs.append((ko, vo, po))
+            st.synchronize()
+            results[tid] = outs
+        except Exception as ex:  # noqa: BLE001
+            errors.append(ex)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for outs in results.values():
+        for ko, vo, po in outs:
+            assert np.array_equal(_np_u64(ko), ek)
+            assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64))
+            assert np.array_equal(po.cpu().numpy().view(np.uint32), ep)

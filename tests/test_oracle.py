@@ -229,6 +229,41 @@ def test_errors():
     assert len(ko) == 0
 
 
+# ------------------------------------------------------------------ all-cores oracle
+def test_parallel_oracle_dense_bruteforce():
+    """oracle.permute_par (the same definition on all cores) vs numpy
+    dense transposes over every permutation of order 4."""
+    rng = np.random.default_rng(404)
+    dims = (3, 5, 4, 6)
+    total = int(np.prod(dims))
+    keys = np.sort(rng.choice(total, 200, replace=False)).astype(np.uint64)
+    vals = rng.standard_normal(200)
+    for perm in itertools.permutations(range(4)):
+        ek, ev, ep = brute.dense_permute(dims, perm, keys, vals)
+        ko, vo, po = oracle.permute_par(dims, perm, keys, vals)
+        assert np.array_equal(ko, ek) and np.array_equal(po, ep), perm
+        assert np.array_equal(vo.view(np.uint64), ev.view(np.uint64))
+
+
+def test_parallel_oracle_stable_on_duplicates_large():
+    """Large enough that libstdc++'s parallel mergesort engages: ties keep input order
+    (PAPER.md:245), i.e. numpy's stable argsort of the re-encoded keys."""
+    rng = np.random.default_rng(405)
+    dims, perm = (64, 64, 64), (2, 0, 1)
+    n = 400_000
+    keys = rng.integers(0, 64 ** 3, n).astype(np.uint64)
+    vals = rng.standard_normal(n)
+    idx = rng.permutation(n).astype(np.uint32)
+    new = brute.reencode_np(dims, perm)(keys)
+    order = np.argsort(new, kind="stable")
+    ko, vo, po = oracle.permute_par(dims, perm, keys, vals, idx)
+    assert np.array_equal(ko, new[order]) and np.array_equal(po, idx[order])
+    assert np.array_equal(vo, vals[order])
+    assert oracle.par_threads() >= 1
+    with pytest.raises(ValueError):
+        oracle.permute_par((4, 4), (1, 0), [16])
+
+
 # ------------------------------------------------------------------ index-matched addition
 def test_add_self_negation_keeps_explicit_zeros():
     """t + (-1) t over the identity match: t's support with +0.0 everywhere (SPEC add:

@@ -280,3 +280,32 @@ def test_block_grid_decomposition():
         assert da * db * mid * hi == nb
     # too few nonzeros per block (< 4 on average): sorted instead
     assert lco.Plan((2048,) * 4, (1, 0, 2, 3)).info(4_000_000)["path"] != "block"
+
+
+def test_partition_world_bound_and_tuning_read_once(monkeypatch):
+    """lco_partition_counts / lco_partition take 1..2048 ranks (the widest
+    partition digit is 11 bits) and reject 2049 on the host; schedule overrides are read
+    once at lco_create, clamped, and never on a call."""
+    import ctypes
+    lib = lco.lib()
+    h = lco.Plan((64, 64, 64), (2, 1, 0))
+    dummy = ctypes.c_void_p(256)
+    for fn in (lib.lco_partition_counts,):
+        assert fn(h._h, 0, None, 2049, dummy, dummy, None, 0, None) == 12  # LCO_ERR_ARG
+    assert lib.lco_partition(h._h, 0, None, None, 0, 2049, dummy, None, None, None, dummy, None,
+                             0, None) == 12
+    # LCO_LSD_MAXBITS=1 on 60 key bits would need 60 passes: clamped to <= 8 passes
+    monkeypatch.setenv("LCO_LSD_MAXBITS", "1")
+    for dims, perm in (((4096,) * 5, (4, 3, 2, 1, 0)), ((64, 64, 64), (2, 1, 0))):
+        info = lco.Plan(dims, perm).info(100_000, sort=True)
+        assert 1 <= info["passes"] <= 8
+        assert all(1 <= b <= 11 for b in info["digit_bits"])
+    monkeypatch.setenv("LCO_LSD_MAXBITS", "0")  # clamped to 1, no division by zero
+    assert lco.Plan((64, 64, 64), (2, 1, 0)).info(100_000)["passes"] >= 1
+    monkeypatch.delenv("LCO_LSD_MAXBITS")
+    # an override set after lco_create does not change the handle's schedule
+    q = lco.Plan((512,) * 4, (2, 3, 0, 1), max_nnz=(1 << 32) - 2)
+    before = q.info(1_308_672)
+    monkeypatch.setenv("LCO_MSD", "1")
+    monkeypatch.setenv("LCO_NO_BLOCK", "1")
+    assert q.info(1_308_672) == before

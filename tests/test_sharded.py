@@ -36,6 +36,14 @@ class OracleOps:
         return (torch.from_numpy(sk.view(np.int64)), torch.from_numpy(sv),
                 torch.from_numpy(si.view(np.int32)), torch.from_numpy(cnt.astype(np.int64)))
 
+    def segment_divisor(self):
+        """Identity prefix a (perm[t] = t for t < a) -> segments of constant (c_0..c_{a-1}):
+        D = prod(dims[a:]) (0: no prefix), computed here from the definition."""
+        a = 0
+        while a < len(self.perm) and self.perm[a] == a:
+            a += 1
+        return int(np.prod(self.dims[a:])) if 0 < a < len(self.perm) else 0
+
     def permute(self, keys, vals, idx):
         ko, vo, po = oracle.permute(self.dims, self.perm, keys.numpy().view(np.uint64),
                                     vals.numpy(), idx.numpy().view(np.uint32))
@@ -51,24 +59,31 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, dims, perm, keys, vals, cuts, outdir):
+def _worker(rank, world, port, dims, perm, keys, vals, cuts, outdir, exchange="auto"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lo, hi = cuts[rank], cuts[rank + 1]
     k = torch.from_numpy(keys[lo:hi].view(np.int64).copy())
     v = torch.from_numpy(vals[lo:hi].copy())
-    ko, vo, po = sharded.permute_sharded(k, v, dims, perm, ops=OracleOps(dims, perm), bits=6)
+    ko, vo, po = sharded.permute_sharded(k, v, dims, perm, ops=OracleOps(dims, perm), bits=6,
+                                         exchange=exchange)
     np.savez(os.path.join(outdir, f"r{rank}.npz"), k=ko.numpy(), v=vo.numpy(), p=po.numpy())
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,dims,perm,nnz,uneven", [
-    (2, (64, 48, 32), (2, 0, 1), 5000, False),
-    (2, (16, 16, 16, 16), (3, 1, 2, 0), 20000, True),
-    (3, (40, 30, 20), (1, 2, 0), 7000, True),
+@pytest.mark.parametrize("world,dims,perm,nnz,uneven,exchange", [
+    (2, (64, 48, 32), (2, 0, 1), 5000, False, "auto"),
+    (2, (16, 16, 16, 16), (3, 1, 2, 0), 20000, True, "auto"),
+    (3, (40, 30, 20), (1, 2, 0), 7000, True, "auto"),
+    # identity-prefix segments (C2b / C3b shapes): exchange-free; segments of ~40 nonzeros
+    # straddle the cuts, one rank's slice lies inside a single segment
+    (3, (64, 8, 8, 16), (0, 2, 1, 3), 6000, True, "auto"),
+    (2, (32, 16, 16), (0, 2, 1), 4000, False, "segments"),
+    # the same shape through the partition + exchange path
+    (3, (64, 8, 8, 16), (0, 2, 1, 3), 6000, True, "nccl"),
 ])
-def test_sharded_matches_single_device(world, dims, perm, nnz, uneven, tmp_path):
+def test_sharded_matches_single_device(world, dims, perm, nnz, uneven, exchange, tmp_path):
     rng = np.random.default_rng(nnz)
     total = int(np.prod(dims))
     keys = np.sort(rng.choice(total, nnz, replace=False)).astype(np.uint64)
@@ -79,8 +94,8 @@ def test_sharded_matches_single_device(world, dims, perm, nnz, uneven, tmp_path)
         cuts = sorted(cuts)
     else:
         cuts = [nnz * r // world for r in range(world + 1)]
-    mp.spawn(_worker, args=(world, _free_port(), dims, perm, keys, vals, cuts, str(tmp_path)),
-             nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), dims, perm, keys, vals, cuts, str(tmp_path),
+                            exchange), nprocs=world, join=True)
     parts = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
     ko = np.concatenate([p["k"] for p in parts]).view(np.uint64)
     vo = np.concatenate([p["v"] for p in parts])
@@ -96,9 +111,20 @@ def test_sharded_matches_single_device(world, dims, perm, nnz, uneven, tmp_path)
 def test_choose_splitters_quantiles():
     h = torch.tensor([10, 0, 30, 0, 0, 60, 0, 0], dtype=torch.int64)
     spl = sharded.choose_splitters(h, 2, kbits=6, bits=3)
-    below = int(h[: spl[0] >> 3].sum())
+    below = int(h[: int(spl[0]) >> 3].sum())
     assert below == 40  # 40 / 60 is the split closest to the median
-    assert sharded.choose_splitters(h, 1, 6, 3) == []
+    assert sharded.choose_splitters(h, 1, 6, 3).numel() == 0
+    # device-side: ascending, one per rank boundary, every cut at a quantile-closest bin
+    rng = np.random.default_rng(3)
+    h = torch.from_numpy(rng.integers(0, 50, 256).astype(np.int64))
+    for world in (2, 3, 8):
+        spl = sharded.choose_splitters(h, world, kbits=16, bits=8)
+        assert spl.numel() == world - 1 and bool((spl[1:] >= spl[:-1]).all())
+        cum = np.concatenate([[0], np.cumsum(h.numpy())])
+        for r, s in enumerate(spl.tolist(), start=1):
+            target = (int(cum[-1]) * r + world - 1) // world
+            best = min(abs(int(c) - target) for c in cum)
+            assert abs(int(cum[s >> 8]) - target) == best
 
 
 @pytest.mark.gpu
@@ -116,8 +142,7 @@ def test_virtual_ranks_cuda(world, cuda_device):
     cuts = [n * r // world for r in range(world + 1)]
     kb = sharded.key_bits(dims)
     hist = sum(p.key_histogram(w.keys[cuts[r]:cuts[r + 1]], 12) for r in range(world))
-    spl = torch.tensor(sharded.choose_splitters(hist, world, kb, 12), dtype=torch.int64,
-                       device=cuda_device)
+    spl = sharded.choose_splitters(hist, world, kb, 12)
     sends = [p.partition(w.keys[cuts[r]:cuts[r + 1]], w.vals[cuts[r]:cuts[r + 1]], cuts[r], spl)
              for r in range(world)]
     outs = []
@@ -159,8 +184,7 @@ def test_virtual_ranks_direct_exchange(world, vals, cuda_device):
     cuts = [n * r // world for r in range(world + 1)]
     kb = sharded.key_bits(dims)
     hist = sum(p.key_histogram(w.keys[cuts[r]:cuts[r + 1]], 12) for r in range(world))
-    spl = torch.tensor(sharded.choose_splitters(hist, world, kb, 12), dtype=torch.int64,
-                       device=cuda_device)
+    spl = sharded.choose_splitters(hist, world, kb, 12)
     sl = [(w.keys[cuts[r]:cuts[r + 1]], w.vals[cuts[r]:cuts[r + 1]] if vals else None)
           for r in range(world)]
     counts = torch.stack([p.partition_counts(k, spl) for k, _ in sl]).cpu()  # [src][dst]
@@ -233,3 +257,46 @@ def test_permute_sharded_world1_direct(cuda_device, tmp_path):
     assert np.array_equal(ko.cpu().numpy().view(np.uint64), ek)
     assert np.array_equal(po.cpu().numpy().view(np.uint32), ep)
     assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_virtual_ranks_segments_cuda(world, cuda_device):
+    """The exchange-free path on the CUDA kernels, ranks emulated one after another on one
+    GPU: C3b (identity-prefix segments of ~114K nonzeros at full scale, here scaled) cut
+    into equal slices that straddle segments; each rank hands its head to the segment's
+    owner (segment_handover), permutes whole segments with global indices, and the
+    concatenation equals the single-GPU oracle bit for bit."""
+    import paper_1802_02619_b200 as lco
+    import workloads
+    w = workloads.config("C3", scale=48, device=cuda_device)
+    dims, perm = w.dims, w.perms[1]
+    p = lco.plan(dims, perm)
+    ops = sharded.CudaOps(dims, perm)
+    D = ops.segment_divisor()
+    assert D > 0
+    n = w.keys.numel()
+    cuts = [n * r // world for r in range(world + 1)]
+    sl = [(w.keys[cuts[r]:cuts[r + 1]], w.vals[cuts[r]:cuts[r + 1]]) for r in range(world)]
+    tab = [sharded.segment_row(k, D).tolist() for k, _ in sl]
+    give = sharded.segment_handover(tab)
+    assert any(c for _, c in give)  # some slice starts inside a segment
+    outs = []
+    for r in range(world):
+        k, v = sl[r]
+        c = give[r][1]
+        ks, vs = [k[c:]], [v[c:]]
+        for s2 in range(r + 1, world):
+            if give[s2][0] == r:
+                ks.append(sl[s2][0][:give[s2][1]])
+                vs.append(sl[s2][1][:give[s2][1]])
+        lk, lv = torch.cat(ks), torch.cat(vs)
+        idx = torch.arange(cuts[r] + c, cuts[r] + c + lk.numel(), device=cuda_device).to(torch.int32)
+        outs.append(p.permute(lk, lv, idx))
+    torch.cuda.synchronize()
+    ko = torch.cat([o[0] for o in outs]).cpu().numpy().view(np.uint64)
+    vo = torch.cat([o[1] for o in outs]).cpu().numpy()
+    po = torch.cat([o[2] for o in outs]).cpu().numpy().view(np.uint32)
+    ek, ev, ep = oracle.permute(dims, perm, w.keys.cpu().numpy().view(np.uint64), w.vals.cpu().numpy())
+    assert np.array_equal(ko, ek) and np.array_equal(po, ep)
+    assert np.array_equal(vo.view(np.uint64), ev.view(np.uint64))
