@@ -16,6 +16,9 @@ __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) {
 constexpr int kThreads = 256;  // k_scatter / k_count CTA size (8 warps)
 constexpr int kItems = 16;     // nonzeros per thread per tile
 constexpr int kTile = kThreads * kItems;
+// Large tiles of the unordered MSD passes (k_scatter UNST, one 1,024-thread CTA per SM):
+// twice the records per digit run of a 4,096-record tile.
+constexpr int kTileL = 8192;
 constexpr int kChunkTiles = 64;  // max tiles per scan chunk
 
 // Tiles per scan chunk: up to 64, fewer for small inputs so that k_offsets' running
@@ -137,6 +140,8 @@ struct PassParams {
   // MSD passes of lco_permute: slots inside a tile's digit run in any order (k_scatter
   // UNST); the leaves order records by (remaining q bits, K'), unique for unique keys
   int unstable;
+  uint32_t tile;  // records per tile of unsegmented passes (0: kTile)
+  int persist;    // persistent grid: each CTA loops over tiles (tile table length on device)
 };
 
 // PER consecutive uint16 tile-histogram entries in, PER uint32 offsets out (vector
@@ -244,8 +249,9 @@ __device__ __forceinline__ bool tile_range(const PassParams& a, uint32_t t, uint
     *seg = e.seg;
     return true;
   }
-  *base = (uint64_t)t * kTile;
-  *n = (uint32_t)umin64(kTile, a.nnz - *base);
+  const uint32_t tl = a.tile ? a.tile : (uint32_t)kTile;
+  *base = (uint64_t)t * tl;
+  *n = (uint32_t)umin64(tl, a.nnz - *base);
   *seg = t / a.ctiles;
   return true;
 }

@@ -58,7 +58,7 @@ __global__ void k_copy(uint64_t nnz, const uint64_t* __restrict__ keys_in,
 // its chunk's sums csum[t / ctiles][BINS] (segmented mode: into its segment's
 // totals csum[seg][BINS]); csum is zeroed by the launcher.
 // ---------------------------------------------------------------------------------
-template <int RB, bool FIRST, bool ADAPT = false>
+template <int RB, bool FIRST, bool ADAPT = false, int ITEMS = kItems, bool PERSIST = false>
 __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ PassParams a,
                                                     const uint64_t* __restrict__ keys,
                                                     uint16_t* __restrict__ thist,
@@ -66,7 +66,9 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   constexpr int BINS = 1 << RB;
   __shared__ uint32_t h[BINS];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t t = blockIdx.x;
+  // one tile per CTA, or (a.persist: tile tables whose length only the device knows)
+  // tiles blockIdx.x, + gridDim.x, ... of a persistent grid
+  for (uint32_t t = blockIdx.x; !PERSIST || t < a.tiles; t += gridDim.x) {
   uint64_t base;
   uint32_t n, seg;
   if (!tile_range(a, t, &base, &n, &seg)) return;
@@ -79,17 +81,17 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   // with 2 (C5 count 0.97 -> 0.76 ms); later passes keep 8 (4: 0.71 -> 0.75 ms)
   constexpr int H = FIRST ? 2 : kItems / 2;
 #pragma unroll
-  for (int half = 0; half < kItems / H; ++half) {
+  for (int half = 0; half < ITEMS / H; ++half) {
     uint64_t k[H];
 #pragma unroll
     for (int it = 0; it < H; ++it) {
-      const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
+      const uint32_t pos = warp * 32 * ITEMS + (half * H + it) * 32 + lane;
       k[it] = pos < n ? __ldcs(keys + base + pos) : 0ull;
     }
     if (direct) {
 #pragma unroll
       for (int it = 0; it < H; ++it) {
-        const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
+        const uint32_t pos = warp * 32 * ITEMS + (half * H + it) * 32 + lane;
         if (pos < n) atomicAdd(&h[digit_from_old(a.kp, a.pass, k[it])], 1u);
       }
       continue;
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
     if (FIRST) reencode_keys<H>(a.kp, k);  // LIV shuffle
 #pragma unroll
     for (int it = 0; it < H; ++it) {
-      const uint32_t pos = warp * 32 * kItems + (half * H + it) * 32 + lane;
+      const uint32_t pos = warp * 32 * ITEMS + (half * H + it) * 32 + lane;
       // plain shared atomics: a histogram needs no order (conflicting lanes of a warp
       // are serialized by the hardware, which only costs on long runs of equal digits)
       if (pos < n) atomicAdd(&h[dg(a, k[it])], 1u);
@@ -116,6 +118,9 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
     for (int d = tid; d < BINS; d += kThreads) nz += h[d] != 0u;
     nz = __reduce_add_sync(0xffffffffu, nz);
     if (lane == 0 && nz) atomicAdd(a.distinct, nz);
+  }
+  if (!PERSIST) return;
+  __syncthreads();  // h is zeroed for the next tile
   }
 }
 
@@ -223,11 +228,13 @@ __global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ Pa
 // Shared memory: sK [tile] u64 | sV [tile] f64 (holds the per-warp counters while
 // ranking) | sP [tile] u32 | sdig [tile] u16 | gbase [bins] u32 | loff [bins] u32.
 // ---------------------------------------------------------------------------------
-constexpr int scatter_nt(int rb) { return rb <= 10 ? 512 : 256; }
+constexpr int scatter_nt(int rb, int tile = kTile) {
+  return tile > kTile ? 1024 : (rb <= 10 ? 512 : 256);
+}
 
-template <int RB>
+template <int RB, int TILE = kTile>
 constexpr size_t scatter_smem_bytes() {
-  return (size_t)kTile * (8 + 8 + 4 + 2) + (size_t)(1 << RB) * 8;
+  return (size_t)TILE * (8 + 8 + 4 + 2) + (size_t)(1 << RB) * 8;
 }
 
 // NT threads (IT = kTile / NT nonzeros each): 512 for digits of <= 10 bits (more warps
@@ -236,26 +243,28 @@ constexpr size_t scatter_smem_bytes() {
 // UNST (MSD passes of lco_permute, unique keys): the order inside a tile's digit run is
 // free, because every leaf sorts its records on (remaining bits of q, K') and K' is unique
 // -- so a record takes its slot with one shared atomic (no per-warp counters, no ballots).
-template <int RB, bool FIRST, bool LAST, bool VALS, int NT, bool ADAPT = false, bool UNST = false>
-__global__ void __launch_bounds__(NT, 2)
+template <int RB, bool FIRST, bool LAST, bool VALS, int NT, bool ADAPT = false, bool UNST = false,
+          int TILE = kTile>
+__global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
     k_scatter(const __grid_constant__ PassParams a, const __grid_constant__ ScatterIO io) {
   constexpr int BINS = 1 << RB;
   constexpr int W = NT / 32;
-  constexpr int IT = kTile / NT;
+  constexpr int IT = TILE / NT;
   constexpr int NB = BINS >= NT ? BINS / NT : 1;
-  static_assert(W * BINS * 2 <= kTile * 8, "warp counters must fit in sV");
+  static_assert(UNST || W * BINS * 2 <= TILE * 8, "warp counters must fit in sV");
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* sK = reinterpret_cast<uint64_t*>(smem);              // [kTile]
-  double* sV = reinterpret_cast<double*>(sK + kTile);             // [kTile]
+  uint64_t* sK = reinterpret_cast<uint64_t*>(smem);              // [TILE]
+  double* sV = reinterpret_cast<double*>(sK + TILE);              // [TILE]
   uint16_t* whist = reinterpret_cast<uint16_t*>(sV);              // [W][BINS] (ranking only)
-  uint32_t* sP = reinterpret_cast<uint32_t*>(sV + kTile);         // [kTile]
-  uint16_t* sdig = reinterpret_cast<uint16_t*>(sP + kTile);       // [kTile]
-  uint32_t* gbase = reinterpret_cast<uint32_t*>(sdig + kTile);    // [BINS]
+  uint32_t* sP = reinterpret_cast<uint32_t*>(sV + TILE);          // [TILE]
+  uint16_t* sdig = reinterpret_cast<uint16_t*>(sP + TILE);        // [TILE]
+  uint32_t* gbase = reinterpret_cast<uint32_t*>(sdig + TILE);     // [BINS]
   uint32_t* loff = gbase + BINS;                                  // [BINS]
   __shared__ uint32_t s_warp[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t t = blockIdx.x;
+  // one tile per CTA, or (a.persist) tiles blockIdx.x, + gridDim.x, ... of a persistent grid
+  for (uint32_t t = blockIdx.x; t < a.tiles; t += gridDim.x) {
   uint64_t base;
   uint32_t n, seg;
   if (!tile_range(a, t, &base, &n, &seg)) return;
@@ -266,8 +275,8 @@ __global__ void __launch_bounds__(NT, 2)
     uint64_t b2 = 0;
     uint32_t m = 0;
     if (!a.ttab) {
-      b2 = (uint64_t)t2 * kTile;
-      m = b2 < a.nnz ? (uint32_t)umin64(kTile, a.nnz - b2) : 0u;
+      b2 = (uint64_t)t2 * TILE;
+      m = b2 < a.nnz ? (uint32_t)umin64(TILE, a.nnz - b2) : 0u;
     } else if (t2 < *a.ntiles) {
       const TileEntry e2 = a.ttab[t2];
       b2 = e2.start;
@@ -472,16 +481,19 @@ __global__ void __launch_bounds__(NT, 2)
       if (VALS) io.dv[d][w] = sV[p];
       io.dp[d][w] = sP[p];
     }
-    return;
-  }
-  for (uint32_t p = tid; p < n; p += NT) {
-    const uint32_t g = gbase[sdig[p]] + p;
-    io.kout[g] = sK[p];
-    if (VALS) io.vout[g] = sV[p];
-    if (want_p) {
-      const uint32_t v = sP[p];
-      io.pout[g] = remap ? __ldg(io.idx_in + v) : v;
+  } else {
+    for (uint32_t p = tid; p < n; p += NT) {
+      const uint32_t g = gbase[sdig[p]] + p;
+      io.kout[g] = sK[p];
+      if (VALS) io.vout[g] = sV[p];
+      if (want_p) {
+        const uint32_t v = sP[p];
+        io.pout[g] = remap ? __ldg(io.idx_in + v) : v;
+      }
     }
+  }
+  if (!a.persist) return;
+  __syncthreads();  // the stage is reused by the next tile
   }
 }
 
@@ -523,7 +535,7 @@ __global__ void __launch_bounds__(512) k_keyhist(const __grid_constant__ KeyPlan
 // ---------------------------------------------------------------------------------
 // Launchers (called from api.cu)
 // ---------------------------------------------------------------------------------
-uint64_t pass_tiles(uint64_t nnz) { return (nnz + kTile - 1) / kTile; }
+uint64_t pass_tiles(uint64_t nnz, uint32_t tile) { return (nnz + tile - 1) / tile; }
 
 // L2 prefetch distance of the pass kernels: one wave of resident CTAs (2 per SM), so a
 // CTA brings the tile its successor on the same SM will load into L2 (measured: -3 to
@@ -538,16 +550,16 @@ int pass_rb(int bits) { return bits <= 8 ? 8 : (bits <= 10 ? 10 : 11); }
 
 // control block: thist (uint16 [tiles][bins]) | toff ([tiles][bins]) | csum ([chunks][bins])
 //                | totals | bucket | counter
-size_t pass_ctrl_bytes(int rb, uint64_t nnz) {
-  const uint64_t tiles = pass_tiles(nnz);
+size_t pass_ctrl_bytes(int rb, uint64_t nnz, uint32_t tile) {
+  const uint64_t tiles = pass_tiles(nnz, tile);
   const uint64_t chunks = (tiles + chunk_tiles((uint32_t)tiles) - 1) / chunk_tiles((uint32_t)tiles);
   const size_t bins = (size_t)1 << rb;
   return (tiles * bins * 2 + 255) / 256 * 256 + tiles * bins * 4 + (chunks + 2) * bins * 4 + 512;
 }
 
-PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl) {
+PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl, uint32_t tile) {
   PassCtrl c;
-  const uint32_t tiles = (uint32_t)pass_tiles(nnz);
+  const uint32_t tiles = (uint32_t)pass_tiles(nnz, tile);
   const uint32_t nchunks = (tiles + chunk_tiles(tiles) - 1) / chunk_tiles(tiles);
   const size_t bins = (size_t)1 << rb;
   char* cb = reinterpret_cast<char*>(ctrl);
@@ -564,18 +576,30 @@ PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl) {
   return c;
 }
 
+template <int RB, int ITEMS>
+static cudaError_t launch_count_t(bool first, const PassParams& a, const uint64_t* keys,
+                                  uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s) {
+  if (a.persist) {  // table-driven later passes only (MSD level 3)
+    k_count<RB, false, false, ITEMS, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+    return cudaGetLastError();
+  }
+  if (a.distinct) {
+    if (first) k_count<RB, true, true, ITEMS><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+    else k_count<RB, false, true, ITEMS><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  } else if (first) {
+    k_count<RB, true, false, ITEMS><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  } else {
+    k_count<RB, false, false, ITEMS><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  }
+  return cudaGetLastError();
+}
+
 template <int RB>
 static cudaError_t launch_count_rb(bool first, const PassParams& a, const uint64_t* keys,
                                    uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s) {
-  if (a.distinct) {
-    if (first) k_count<RB, true, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
-    else k_count<RB, false, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
-  } else if (first) {
-    k_count<RB, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
-  } else {
-    k_count<RB, false><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
-  }
-  return cudaGetLastError();
+  if (a.tile == (uint32_t)kTileL)
+    return launch_count_t<RB, kTileL / kThreads>(first, a, keys, thist, csum, grid, s);
+  return launch_count_t<RB, kItems>(first, a, keys, thist, csum, grid, s);
 }
 
 cudaError_t launch_count(int rb, bool first, const PassParams& a, const uint64_t* keys,
@@ -592,8 +616,18 @@ template <int RB, bool F, bool LST>
 static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const ScatterIO& io,
                                    uint32_t grid, cudaStream_t s) {
   constexpr int NT = scatter_nt(RB);
-  const size_t smem = scatter_smem_bytes<RB>();
+  size_t smem = scatter_smem_bytes<RB>();
   void (*fn)(const PassParams, const ScatterIO);
+  if (a.unstable && !LST && a.tile == (uint32_t)kTileL) {  // large tiles, one CTA per SM
+    constexpr int NL = scatter_nt(RB, kTileL);
+    smem = scatter_smem_bytes<RB, kTileL>();
+    fn = vals ? k_scatter<RB, F, false, true, NL, false, true, kTileL>
+              : k_scatter<RB, F, false, false, NL, false, true, kTileL>;
+    cudaError_t e = kernel_setup(reinterpret_cast<const void*>(fn), smem, NL);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, NL, smem, s>>>(a, io);
+    return cudaGetLastError();
+  }
   if (a.unstable && !LST) {  // MSD passes of lco_permute (the last pass is never one)
     if (a.distinct) fn = vals ? k_scatter<RB, F, false, true, NT, true, true> : k_scatter<RB, F, false, false, NT, true, true>;
     else fn = vals ? k_scatter<RB, F, false, true, NT, false, true> : k_scatter<RB, F, false, false, NT, false, true>;
@@ -652,8 +686,10 @@ ScatterIO pass_buffers(const PassIO& io, int j, bool last, const uint32_t* toff)
 cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool first,
                      bool last, const Launch& L, bool count_only) {
   const int BINS = 1 << rb;
-  const PassCtrl c = pass_ctrl_layout(rb, io.nnz, io.ctrl);
+  const uint32_t tile = a0.tile ? a0.tile : (uint32_t)kTile;
+  const PassCtrl c = pass_ctrl_layout(rb, io.nnz, io.ctrl, tile);
   PassParams a = a0;
+  a.tile = tile;
   a.pass = j;
   a.tiles = c.tiles;
   a.nchunks = c.nchunks;

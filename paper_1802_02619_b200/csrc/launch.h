@@ -83,12 +83,12 @@ struct MsdPlan {
 struct PassParams;
 struct ScatterIO;
 
-uint64_t pass_tiles(uint64_t nnz);
+uint64_t pass_tiles(uint64_t nnz, uint32_t tile = 4096);
 uint32_t prefetch_distance();  // L2 prefetch distance of the pass kernels (tiles)
 int pass_tile();
 int pass_rb(int bits);
-size_t pass_ctrl_bytes(int rb, uint64_t nnz);
-PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl);
+size_t pass_ctrl_bytes(int rb, uint64_t nnz, uint32_t tile = 4096);
+PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl, uint32_t tile = 4096);
 cudaError_t launch_count(int rb, bool first, const PassParams& a, const uint64_t* keys,
                          uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s);
 cudaError_t launch_scatter(int rb, bool first, bool last, bool vals, const PassParams& a,
@@ -105,7 +105,7 @@ uint32_t leaf_cap();      // largest leaf one CTA sorts in shared memory
 uint32_t leaf_target();   // expected leaf size the MSD digits aim for (warp leaves)
 uint32_t cta_leaf_cap();  // largest leaf k_leafc sorts
 uint32_t staged_leaf_target();  // expected leaf size for k_leafs
-size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz);
+size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz, uint32_t tile = 4096);
 cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, const Launch& L);
 uint32_t tile_nominal(uint64_t nnz, uint64_t segments);  // segment-local path (msd.cu)
 cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const Launch& L);

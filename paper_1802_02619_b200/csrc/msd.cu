@@ -43,7 +43,7 @@ constexpr int kLeafWarps = kLeafThreads / 32;
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__ totals1,
                                                    const uint32_t* __restrict__ bucket1,
-                                                   int nb1, uint32_t cap,
+                                                   int nb1, uint32_t cap, uint32_t tile,
                                                    TileEntry* __restrict__ ttab,
                                                    uint32_t* __restrict__ tfirst,
                                                    uint32_t* __restrict__ tcnt,
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__
   __shared__ uint32_t s_warp[32];
   const int b = threadIdx.x;
   const uint32_t size = b < nb1 ? totals1[b] : 0u;
-  const uint32_t nt = size > cap ? (size + kTile - 1) / kTile : 0u;
+  const uint32_t nt = size > cap ? (size + tile - 1) / tile : 0u;
   cnt[b] = nt;
   __syncthreads();
   block_scan_bins<1024, 1024>(cnt, off, s_warp);
@@ -77,8 +77,8 @@ __global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__
       if (off[x + st] <= t) x += st;
     const uint32_t j = t - off[x];
     TileEntry e;
-    e.start = s_start[x] + j * kTile;
-    e.n = min((uint32_t)kTile, s_size[x] - j * kTile);
+    e.start = s_start[x] + j * tile;
+    e.n = min(tile, s_size[x] - j * tile);
     e.seg = x;
     e.pad = 0;
     ttab[t] = e;
@@ -96,12 +96,14 @@ __global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __rest
                                                           const uint32_t* __restrict__ btot,
                                                           const uint16_t* __restrict__ thist,
                                                           uint32_t* __restrict__ base2,
-                                                          uint32_t* __restrict__ toff) {
+                                                          uint32_t* __restrict__ toff,
+                                                          const uint32_t* __restrict__ nseg = nullptr) {
   constexpr int BINS = 1 << RB;
   __shared__ uint32_t tot[BINS];
   __shared__ uint32_t ex[BINS];
   __shared__ uint32_t s_warp[32];
   const int b = blockIdx.x;
+  if (nseg && (uint32_t)b >= *nseg) return;  // list-driven segments (level 3)
   const uint32_t nt = tcnt[b];
   if (nt == 0) return;
   for (int d = threadIdx.x; d < BINS; d += kThreads) tot[d] = btot[(size_t)b * BINS + d];
@@ -134,6 +136,71 @@ __global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __rest
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------------
+// k_list_tiles (MSD level 3): one CTA.  The level-2 leaves that did not fit a leaf kernel
+// (entries of `list`: level-2 slots, in any order) become the level-3 segments: start3 /
+// tcnt3 / tfirst3 per entry and the tile table over them (tiles never straddle a
+// segment).  Entries past `cap` go to the deferred list of the streaming leaf sort.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_list_tiles(const uint32_t* __restrict__ list,
+                                                    const uint32_t* __restrict__ nlist,
+                                                    const uint32_t* __restrict__ base2,
+                                                    const uint32_t* __restrict__ btot2,
+                                                    uint32_t cap, uint32_t tile,
+                                                    uint32_t* __restrict__ start3,
+                                                    uint32_t* __restrict__ size3,
+                                                    uint32_t* __restrict__ tfirst3,
+                                                    uint32_t* __restrict__ tcnt3,
+                                                    uint32_t* __restrict__ n3,
+                                                    TileEntry* __restrict__ ttab,
+                                                    uint32_t* __restrict__ ntiles,
+                                                    uint32_t* __restrict__ defer,
+                                                    uint32_t* __restrict__ ndefer) {
+  __shared__ uint32_t cnt[1024], off[1024], s_warp[32];
+  __shared__ uint32_t s_carry;
+  const int tid = threadIdx.x;
+  const uint32_t n = *nlist, m = min(n, cap);
+  if (tid == 0) {
+    s_carry = 0;
+    *n3 = m;
+  }
+  for (uint32_t e = m + tid; e < n; e += 1024)  // overflow: streaming sort (entry kept)
+    defer[atomicAdd(ndefer, 1u)] = list[e];
+  __syncthreads();
+  for (uint32_t c0 = 0; c0 < cap; c0 += 1024) {
+    const uint32_t e = c0 + tid;
+    uint32_t st = 0, sz = 0;
+    if (e < m) {
+      const uint32_t slot = list[e] & ((1u << 30) - 1u);  // entries: level << 30 | slot
+      st = base2[slot];
+      sz = btot2[slot];
+    }
+    const uint32_t nt = (sz + tile - 1) / tile;
+    cnt[tid] = nt;
+    __syncthreads();
+    block_scan_bins<1024, 1024>(cnt, off, s_warp);
+    const uint32_t carry = s_carry;
+    if (e < cap) {
+      start3[e] = st;
+      size3[e] = sz;
+      tfirst3[e] = carry + off[tid];
+      tcnt3[e] = nt;
+    }
+    for (uint32_t j = 0; j < nt; ++j) {
+      TileEntry te;
+      te.start = st + j * tile;
+      te.n = min(tile, sz - j * tile);
+      te.seg = e;
+      te.pad = 0;
+      ttab[carry + off[tid] + j] = te;
+    }
+    __syncthreads();
+    if (tid == 1023) s_carry = carry + off[1023] + nt;
+    __syncthreads();
+  }
+  if (tid == 0) *ntiles = s_carry;
 }
 
 // ---------------------------------------------------------------------------------
@@ -174,6 +241,15 @@ struct LeafArgs {
   // level 3: segment-aligned tiles of the raw input (k_tile_bounds), tstart[0..ntiles]
   const uint32_t* tstart;
   uint32_t ntiles;
+  // MSD level 3 (leaf level code 4, data in buffer A): level-2 leaves that did not fit a
+  // leaf were split again on the next b3 bits; entry e of the level-3 list owns slots
+  // e << b3 .. (e << b3) + 2^b3 - 1 of base3 / btot3
+  int b3;
+  int rb4;                 // deferred list: remaining bits of level-3 leaves
+  uint32_t cap3;           // level-3 list capacity (slots = cap3 << b3)
+  const uint32_t* n3;      // level-3 list length (device)
+  const uint32_t* btot3;
+  const uint32_t* base3;
   int keymode;             // 0: sort on q = K' div T (rb low bits); 1: on K' (rb bits)
   int staged;              // CTA leaves: fully staged k_leafs (<= kSCap nonzeros)
   int no_leafs, no_leafr;  // schedule overrides (Tuning)
@@ -201,12 +277,15 @@ constexpr size_t leaf_smem_bytes(int lb) {
 
 struct LeafDesc {
   uint32_t start, n;
-  int src;  // 0: raw input (re-encode), 1: buffer A, 2: buffer B  (== MSD level)
+  int src;    // 0: raw input (re-encode), 1: buffer A, 2: buffer B
+  int level;  // leaf level code (1, 2: MSD levels, 3: tile path, 4: MSD level 3)
 };
 
 __device__ __forceinline__ uint32_t leaf_slots(const LeafArgs& L, int level) {
   return level == 0 ? 1u
-                    : (level == 1 ? (1u << L.b1) : (level == 2 ? (1u << (L.b1 + L.b2)) : L.ntiles));
+                    : (level == 1 ? (1u << L.b1)
+                                  : (level == 2 ? (1u << (L.b1 + L.b2))
+                                                : (level == 4 ? (L.cap3 << L.b3) : L.ntiles)));
 }
 
 // Leaf `slot` of MSD level `level` (0: the raw input as one leaf); false if empty or
@@ -215,16 +294,19 @@ __device__ __forceinline__ bool leaf_at(const LeafArgs& L, int level, uint32_t s
                                         LeafDesc* d) {
   if (slot >= leaf_slots(L, level)) return false;
   if (level == 0) {
-    *d = LeafDesc{0u, (uint32_t)L.a.nnz, 0};
+    *d = LeafDesc{0u, (uint32_t)L.a.nnz, 0, 0};
   } else if (level == 1) {
     if (L.levels == 2 && L.tcnt[slot] > 0) return false;  // split again at level 2
-    *d = LeafDesc{L.bucket1[slot], L.totals1[slot], 1};
+    *d = LeafDesc{L.bucket1[slot], L.totals1[slot], 1, 1};
   } else if (level == 2) {
     if (L.tcnt[slot >> L.b2] == 0) return false;
-    *d = LeafDesc{L.base2[slot], L.btot[slot], 2};
+    *d = LeafDesc{L.base2[slot], L.btot[slot], 2, 2};
+  } else if (level == 4) {  // MSD level 3: buffer A
+    if ((slot >> L.b3) >= *L.n3) return false;
+    *d = LeafDesc{L.base3[slot], L.btot3[slot], 1, 4};
   } else {  // segment-aligned tile of the raw input
     const uint32_t s0 = L.tstart[slot];
-    *d = LeafDesc{s0, L.tstart[slot + 1] - s0, 0};
+    *d = LeafDesc{s0, L.tstart[slot + 1] - s0, 0, 3};
   }
   return d->n > 0;
 }
@@ -241,7 +323,7 @@ __device__ __forceinline__ bool next_leaf(const LeafArgs& L, uint32_t& k, LeafDe
     }
     return false;
   }
-  const uint32_t nslots = leaf_slots(L, L.only_level);
+  const uint32_t nslots = L.only_level == 4 ? (*L.n3 << L.b3) : leaf_slots(L, L.only_level);
   for (; k < nslots; k += gridDim.x)
     if (leaf_at(L, L.only_level, k, d)) return true;
   return false;
@@ -408,7 +490,7 @@ __global__ void __launch_bounds__(kLeafThreads) k_leaf(const __grid_constant__ L
     uint32_t* Ps = Pst[st];
     const uint32_t n = cur.n, start = cur.start;
     // level-1 leaves of a two-level plan sort more bits than level-2 leaves
-    const int rb = (L.dlist && cur.src == 1) ? L.rb1 : L.rb;
+    const int rb = !L.dlist ? L.rb : (cur.level == 1 ? L.rb1 : (cur.level == 4 ? L.rb4 : L.rb));
     const uint64_t mask = rb >= 64 ? ~0ull : ((1ull << rb) - 1ull);
     const int npass = (rb + LB - 1) / LB;
     if (n <= L.cap) {
@@ -1471,10 +1553,10 @@ static bool use_leafr(const LeafArgs& L, bool single) {
 
 // (markers start with the launched kernel's name: profiles/summarize.py checks them
 // against ncu's launch list)
-static const char* leafc_kernel(const LeafArgs& L, bool single, bool l1 = false) {
-  if (use_leafs(L, single)) return l1 ? "k_leafs_l1" : "k_leafs";
-  if (use_leafr(L, single)) return l1 ? "k_leafr_l1" : "k_leafr";
-  return l1 ? "k_leafc_l1" : "k_leafc";
+static const char* leafc_kernel(const LeafArgs& L, bool single, bool l1 = false, bool l3 = false) {
+  if (use_leafs(L, single)) return l1 ? "k_leafs_l1" : (l3 ? "k_leafs_l3" : "k_leafs");
+  if (use_leafr(L, single)) return l1 ? "k_leafr_l1" : (l3 ? "k_leafr_l3" : "k_leafr");
+  return l1 ? "k_leafc_l1" : (l3 ? "k_leafc_l3" : "k_leafc");
 }
 
 // Leaf levels (defer list present): 32-bit keys when the leaf bits allow, two CTAs per
@@ -1652,8 +1734,8 @@ cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const L
   cb += (tiles2 * rbins2 * 2 + 255) / 256 * 256;
   uint32_t* toff2 = reinterpret_cast<uint32_t*>(cb);
   if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
-  k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1, 0u, ttab, tfirst, tcnt,
-                                        ntiles);
+  k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1, 0u, (uint32_t)kTile, ttab,
+                                        tfirst, tcnt, ntiles);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess) return e;
   PassParams a2 = a;
@@ -1677,20 +1759,74 @@ cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const L
   return launch_scatter(rb2, true, true, vals, a2, sio, (uint32_t)tiles2, Lc.stream);
 }
 
+// MSD level 3 (the paper's recursion into regions, made data-adaptive as
+// LibNT's RP is): level-2 leaves too large or too crowded for a leaf kernel
+// are split again on the next 8 bits instead of going to the streaming sort.  At most
+// l3_cap entries (the rest stream); 8-bit digits.
+constexpr int kL3Bits = 8;   // bins of the level-3 pass (radix instantiation, slot stride)
+constexpr int kL3Digit = 8;  // bits of q the level-3 pass sorts on
+static uint32_t l3_cap(uint64_t nnz) {
+  const uint64_t c = nnz / 1024;
+  return (uint32_t)(c < 64 ? 64 : (c > 16384 ? 16384 : c));
+}
+struct L3Layout {
+  uint32_t* list;      // level-2 leaves deferred by the level-2 leaf launch
+  uint32_t* nlist;
+  uint32_t *start3, *size3, *tfirst3, *tcnt3, *n3, *ntiles3;
+  TileEntry* ttab3;
+  uint32_t* btot3;     // [cap3][256] sub-bucket sizes, then base3
+  uint32_t* base3;
+  uint16_t* thist3;
+  uint32_t* toff3;
+  uint64_t tiles3;
+  size_t bytes;
+};
+static L3Layout l3_layout(char* cb, size_t nb1, size_t rbins2, uint64_t nnz, uint32_t tile) {
+  L3Layout l;
+  const uint32_t cap = l3_cap(nnz);
+  const size_t bins = (size_t)1 << kL3Bits;
+  l.tiles3 = pass_tiles(nnz, tile) + cap;
+  size_t o = 0;
+  auto take = [&](size_t b) {
+    char* p = cb ? cb + o : nullptr;
+    o += (b + 255) / 256 * 256;
+    return p;
+  };
+  l.list = reinterpret_cast<uint32_t*>(take((nb1 * rbins2 + 1) * 4));
+  l.nlist = l.list ? l.list + nb1 * rbins2 : nullptr;
+  l.start3 = reinterpret_cast<uint32_t*>(take((size_t)cap * 16 + 8));
+  l.size3 = l.start3 ? l.start3 + cap : nullptr;
+  l.tfirst3 = l.start3 ? l.start3 + 2 * cap : nullptr;
+  l.tcnt3 = l.start3 ? l.start3 + 3 * cap : nullptr;
+  l.n3 = l.start3 ? l.start3 + 4 * cap : nullptr;
+  l.ntiles3 = l.n3 ? l.n3 + 1 : nullptr;
+  l.ttab3 = reinterpret_cast<TileEntry*>(take(l.tiles3 * sizeof(TileEntry)));
+  l.btot3 = reinterpret_cast<uint32_t*>(take((size_t)cap * bins * 8));
+  l.base3 = l.btot3 ? l.btot3 + (size_t)cap * bins : nullptr;
+  l.thist3 = reinterpret_cast<uint16_t*>(take(l.tiles3 * bins * 2));
+  l.toff3 = reinterpret_cast<uint32_t*>(take(l.tiles3 * bins * 4));
+  l.bytes = o;
+  return l;
+}
+static size_t l3_bytes(size_t nb1, size_t rbins2, uint64_t nnz, uint32_t tile) {
+  return l3_layout(nullptr, nb1, rbins2, nnz, tile).bytes;
+}
+
 // Workspace of the MSD schedule beyond the ping-pong buffers: the level-1 pass control
 // block, then the level-2 tables.
-size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz) {
+size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz, uint32_t tile) {
   const size_t nb1 = (size_t)1 << b1;
-  const uint64_t tiles2 = pass_tiles(nnz) + nb1;
-  size_t s = (pass_ctrl_bytes(pass_rb(b1), nnz) + 255) / 256 * 256;
+  const uint64_t tiles2 = pass_tiles(nnz, tile) + nb1;
+  size_t s = (pass_ctrl_bytes(pass_rb(b1), nnz, tile) + 255) / 256 * 256;
   if (b2 > 0) {
     const size_t rbins2 = (size_t)1 << pass_rb(b2);
     s += (tiles2 * sizeof(TileEntry) + 255) / 256 * 256;
     s += (nb1 * 12 + 4 + 255) / 256 * 256;          // tfirst, tcnt, ntiles
     s += (nb1 * rbins2 * 8 + 255) / 256 * 256;      // btot, base2
     s += (tiles2 * rbins2 * 2 + 255) / 256 * 256;   // thist2
-    s += tiles2 * rbins2 * 4;                       // toff2
-    s = (s + 255) / 256 * 256 + (nb1 * rbins2 + nb1 + 64) * 4;  // deferred leaf list
+    s += (tiles2 * rbins2 * 4 + 255) / 256 * 256;   // toff2
+    s += l3_bytes(nb1, rbins2, nnz, tile);          // level-3 re-split tables
+    s = (s + 255) / 256 * 256 + (nb1 * rbins2 + nb1 + (size_t)l3_cap(nnz) * 256 + 64) * 4;
   } else {
     s += (2 * nb1 + 64) * 4;
   }
@@ -1714,6 +1850,10 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   const bool unst = io.unique && mp.levels == 2 && mp.cta && log2T >= 0 &&
                     mp.rb + mp.b2 + log2T <= 64;
   a.unstable = unst ? 1 : 0;
+  // unordered passes after the first: 8,192-record tiles (twice as long a run per digit,
+  // one CTA per SM); the first pass keeps 4,096 (two CTAs per SM measured faster there)
+  const uint32_t tile = unst ? (uint32_t)kTileL : (uint32_t)kTile;
+  a.tile = kTile;
   LeafArgs L;
   memset(&L, 0, sizeof L);
   L.a = a;
@@ -1747,9 +1887,10 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   char* cb = reinterpret_cast<char*>(io.ctrl);
   PassIO io1 = io;
   io1.ctrl = reinterpret_cast<uint32_t*>(cb);
-  cb += (pass_ctrl_bytes(rb1, nnz) + 255) / 256 * 256;
+  cb += (pass_ctrl_bytes(rb1, nnz, kTile) + 255) / 256 * 256;
   if ((e = run_pass(rb1, a, io1, 0, true, false, Lc)) != cudaSuccess) return e;
-  const PassCtrl c1 = pass_ctrl_layout(rb1, nnz, io1.ctrl);
+  const PassCtrl c1 = pass_ctrl_layout(rb1, nnz, io1.ctrl, kTile);
+  a.tile = tile;  // later passes
   L.totals1 = c1.totals;
   L.bucket1 = c1.bucket;
   const uint32_t nb1 = 1u << mp.b1;
@@ -1757,7 +1898,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     // ---- level 2: stable segmented pass on the next b2 bits, A -> B ----
     const int rb2 = pass_rb(mp.b2);
     const size_t rbins2 = (size_t)1 << rb2;
-    const uint64_t tiles2 = pass_tiles(nnz) + nb1;
+    const uint64_t tiles2 = pass_tiles(nnz, tile) + nb1;
     TileEntry* ttab = reinterpret_cast<TileEntry*>(cb);
     cb += (tiles2 * sizeof(TileEntry) + 255) / 256 * 256;
     uint32_t* tfirst = reinterpret_cast<uint32_t*>(cb);
@@ -1773,7 +1914,8 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     cb += (tiles2 * rbins2 * 4 + 255) / 256 * 256;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
     k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1,
-                                          mp.cta ? kCCap : kLeafCap, ttab, tfirst, tcnt, ntiles);
+                                          mp.cta ? kCCap : kLeafCap, tile, ttab, tfirst, tcnt,
+                                          ntiles);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess)
       return e;
@@ -1803,16 +1945,34 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     L.base2 = base2;
     L.b2 = rb2;  // leaf slots are indexed with the bucket row stride
   }
-  // ---- leaves: warps sort the small ones, the block kernel drains the deferred list ----
+  L3Layout l3;
+  memset(&l3, 0, sizeof l3);
+  if (mp.levels == 2) {
+    l3 = l3_layout(cb, nb1, (size_t)1 << pass_rb(mp.b2), nnz, tile);
+    cb += l3.bytes;
+  }
+  // ---- leaves: CTAs / warps sort the small ones, the block kernel drains the deferred list ----
+  const size_t ndef_cap = ((size_t)nb1 << (mp.levels == 2 ? pass_rb(mp.b2) : 0)) + nb1 +
+                          (mp.levels == 2 ? (size_t)l3_cap(nnz) << kL3Bits : 0) + 64;
   uint32_t* defer = reinterpret_cast<uint32_t*>(cb);
-  uint32_t* ndefer = defer + ((size_t)1 << (mp.b1 + (mp.levels == 2 ? pass_rb(mp.b2) : 0))) + nb1;
+  uint32_t* ndefer = defer + ndef_cap - 1;
   if ((e = cudaMemsetAsync(ndefer, 0, 4, Lc.stream)) != cudaSuccess) return e;
   L.defer = defer;
   L.ndefer = ndefer;
+  // level 3 applies to CTA leaves with bits left to split
+  const bool lev3 = mp.levels == 2 && mp.cta && mp.rb >= 1;
+  // level-3 digit: 8 bits (4 bits measured: on Table 2's Laplacian the next bits of q hold
+  // a mode the stencil ties to an earlier one, so 16 sub-buckets stayed oversize)
+  const int b3 = lev3 ? (mp.rb < kL3Digit ? mp.rb : kL3Digit) : 0;
   if (mp.levels == 2) {
     LeafArgs L2 = L;
     L2.only_level = 2;
     L2.rb = mp.rb;
+    if (lev3) {  // level-2 leaves that do not fit are split again (level 3), not streamed
+      if ((e = cudaMemsetAsync(l3.nlist, 0, 4, Lc.stream)) != cudaSuccess) return e;
+      L2.defer = l3.list;
+      L2.ndefer = l3.nlist;
+    }
     if (mp.cta) {
       if (Lc.mark) Lc.mark(Lc.ctx, leafc_kernel(L2, false));
       e = launch_leafc(L2, vals, false, 1u << 30, Lc.stream);
@@ -1821,6 +1981,55 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
       e = vals ? launch_leafw<true>(L2, Lc.stream) : launch_leafw<false>(L2, Lc.stream);
     }
     if (e != cudaSuccess) return e;
+  }
+  if (lev3) {
+    // ---- level 3: segmented pass on the next b3 bits over the listed level-2 leaves,
+    // B -> A, then their leaves (level code 4) ----
+    const uint32_t cap3 = l3_cap(nnz);
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_list_tiles");
+    k_list_tiles<<<1, 1024, 0, Lc.stream>>>(l3.list, l3.nlist, L.base2, L.btot, cap3, tile,
+                                           l3.start3, l3.size3, l3.tfirst3, l3.tcnt3, l3.n3,
+                                           l3.ttab3, l3.ntiles3, defer, ndefer);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(l3.btot3, 0, (size_t)cap3 * (1u << kL3Bits) * 4, Lc.stream)) !=
+        cudaSuccess)
+      return e;
+    PassParams a3 = a;
+    a3.pass = 2;
+    a3.kp.passes = 3;
+    a3.kp.dshift[2] = mp.rb - b3;
+    a3.kp.dbits[2] = b3;
+    a3.ttab = l3.ttab3;
+    a3.ntiles = l3.ntiles3;
+    a3.tiles = (uint32_t)l3.tiles3;
+    a3.persist = 1;  // the table's length is known on the device only: persistent grids
+    int sms = 148;
+    if ((e = device_sms(&sms)) != cudaSuccess) return e;
+    const uint32_t g3 = (uint32_t)sms * (tile == (uint32_t)kTileL ? 1u : 2u);
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_count_l3");
+    if ((e = launch_count(kL3Bits, false, a3, io.kB, l3.thist3, l3.btot3, 4u * g3, Lc.stream)) !=
+        cudaSuccess)
+      return e;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg_l3");
+    k_offsets_seg<kL3Bits><<<cap3, kThreads, 0, Lc.stream>>>(l3.start3, l3.tfirst3, l3.tcnt3,
+                                                            l3.btot3, l3.thist3, l3.base3,
+                                                            l3.toff3, l3.n3);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const ScatterIO s3 = pass_buffers(io, 2, false, l3.toff3);
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_scatter_l3");
+    if ((e = launch_scatter(kL3Bits, false, false, vals, a3, s3, g3, Lc.stream)) != cudaSuccess)
+      return e;
+    L.b3 = kL3Bits;  // slot stride
+    L.rb4 = mp.rb - b3;
+    L.cap3 = cap3;
+    L.n3 = l3.n3;
+    L.btot3 = l3.btot3;
+    L.base3 = l3.base3;
+    LeafArgs L4 = L;
+    L4.only_level = 4;
+    L4.rb = mp.rb - b3;
+    if (Lc.mark) Lc.mark(Lc.ctx, leafc_kernel(L4, false, false, true));
+    if ((e = launch_leafc(L4, vals, false, 1u << 30, Lc.stream)) != cudaSuccess) return e;
   }
   // level-1 buckets that were not split again sort the bits left after level 1
   LeafArgs L1 = L;
@@ -1841,10 +2050,12 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   LD.dcount = ndefer;
   LD.rb = mp.rb;
   LD.rb1 = mp.rb + (mp.levels == 2 ? mp.b2 : 0);
+  LD.rb4 = mp.rb - b3;
   if (unst) {  // sort on K' bits: (remaining q bits, suffix), unique
     LD.keymode = 1;
     LD.rb += log2T;
     LD.rb1 += log2T;
+    LD.rb4 += log2T;
   }
   return run_leaf(LD, 1u << 20, vals, Lc.stream);
 }

@@ -673,3 +673,22 @@ def test_one_handle_two_threads_two_streams(cuda_device):
             assert np.array_equal(_np_u64(ko), ek)
             assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64))
             assert np.array_equal(po.cpu().numpy().view(np.uint32), ep)
+
+
+# ------------------------------------------------------------------ MSD level 3 (adaptive re-split)
+@pytest.mark.parametrize("perm,sort", [((3, 1, 2, 0), False), ((1, 3, 2, 0), False),
+                                       ((2, 0, 3, 1), False), ((0, 2, 1, 3), True),
+                                       ((3, 1, 0, 2), True)])
+def test_msd_level3_laplacian_skew(perm, sort, cuda_device, monkeypatch):
+    """Table 2's cliff: on the Eq (2.3) Laplacian, the level-2 digit of these permutations
+    lands on modes that the stencil ties together (l in {j-1, j, j+1}), so a few level-2
+    buckets hold thousands of nonzeros.  They are split again on the next 8 bits (level
+    3, buffer B -> A) instead of the streaming sort; bit-exact against the oracle."""
+    n = 724  # 2.6M nonzeros: two MSD levels (forced: the model picks LSD at this size)
+    monkeypatch.setenv("LCO_MSD", "1")
+    k, v = workloads.combinatorial_laplacian(n)
+    keys, vals = _np_u64(k), v.numpy()
+    info = lco.plan((n,) * 4, perm).info(len(keys), sort=sort)
+    assert info["path"] == "msd" and info["msd_levels"] == 2, info
+    check((n,) * 4, perm, keys, vals, sort=sort)
+    check((n,) * 4, perm, keys, None, sort=sort, return_perm=False)
