@@ -249,7 +249,15 @@ def run_single(args):
         p.permute(w.keys, w.vals, out=out, workspace=ws)
     torch.cuda.synchronize()
 
-    def timed(steps, outs, do_flush, profile=False, sample_clocks=False):
+    # The timed step replays one CUDA graph of the lco_permute call (every kernel of the
+    # call, same buffers: launch latency and host overhead removed); the
+    # per-kernel times come from the same call launched directly (graphs hide them).
+    graph = None
+    if not args.no_graph:
+        graph = p.graph(w.keys, w.vals, out=out, workspace=ws)
+        torch.cuda.synchronize()
+
+    def timed(steps, outs, do_flush, profile=False, sample_clocks=False, use_graph=False):
         """CUDA events on the launching stream around each step; L2 flushed before each
         step when do_flush (inputs smaller than 4x L2)."""
         if profile:
@@ -266,17 +274,22 @@ def run_single(args):
             if do_flush:
                 fbuf.fill_(float(st))
             ev[st][0].record(stream)
-            p.permute(w.keys, w.vals, out=outs, workspace=ws)
+            if use_graph:
+                graph.replay()
+            else:
+                p.permute(w.keys, w.vals, out=outs, workspace=ws)
             ev[st][1].record(stream)
         torch.cuda.synchronize()
         wall_s = time.perf_counter() - w0
         clk_ = clocks.stop() if clocks else None
         return [x.elapsed_time(y) for x, y in ev], wall_s, clk_
 
-    step_ms, wall, clk = timed(args.steps, out, flush, profile=True, sample_clocks=True)
-    ms = float(np.mean(step_ms))
+    direct_ms, _, _ = timed(args.steps, out, flush, profile=True)
     names, rows = p.profile_read()
     p.profile_enable(0)
+    step_ms, wall, clk = timed(args.steps, out, flush, sample_clocks=True,
+                               use_graph=graph is not None)
+    ms = float(np.mean(step_ms))
     counts = {}
     for nm in names:
         counts[nm] = counts.get(nm, 0) + 1
@@ -300,18 +313,22 @@ def run_single(args):
     value = n / (ms / 1e3)
     # secondary figures: without the permutation vector (40 B/nnz schedule
     # row), and for sub-L2 inputs the L2-warm time beside the flushed (cold) one
-    extra = {}
+    extra = {"direct_launch": {"ms_per_step": float(np.mean(direct_ms)),
+                               "value": n / (float(np.mean(direct_ms)) / 1e3),
+                               "note": "the same call launched kernel by kernel (no graph)"}}
     np_ms, _, _ = timed(max(3, args.steps // 2), (ko, vo, None), flush)
     extra["no_perm"] = {"ms_per_step": float(np.mean(np_ms)),
                         "value": n / (float(np.mean(np_ms)) / 1e3),
                         "step_frac_32B": ALG_BYTES * n / (float(np.mean(np_ms)) / 1e3) / 1e9 / peak}
     if flush:
-        wm, _, _ = timed(args.steps, out, False)
+        wm, _, _ = timed(args.steps, out, False, use_graph=graph is not None)
         extra["l2_warm"] = {"ms_per_step": float(np.mean(wm)), "value": n / (float(np.mean(wm)) / 1e3),
                             "note": "inputs left in L2 between steps (no flush)"}
         extra["l2_cold"] = {"ms_per_step": ms, "value": value,
                             "note": "L2 flushed before every step (the headline)"}
 
+    used_graph = graph is not None
+    graph = None  # releases the captured buffers' references
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -391,6 +408,8 @@ def run_single(args):
                    "dims": list(w.dims), "perm": list(perm), "parallelism": "single GPU",
                    "l2": ("L2 flushed between steps" if flush else
                           f"inputs {in_bytes / 1e9:.1f} GB >> L2 {l2_bytes / 1e6:.0f} MB"),
+                   "step": ("one CUDA-graph replay of the lco_permute call" if used_graph
+                            else "one lco_permute call"),
                    "plan": {k: info[k] for k in ("sort_bits", "passes", "digit_bits",
                                                   "radix_bits", "path", "tile")}},
         "hbm_frac": step_achieved / peak,
@@ -429,6 +448,8 @@ def main():
     ap.add_argument("--e2e-sequential", action="store_true",
                     help="e2e: one stream only (no overlap of consecutive steps)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the call launched kernel by kernel instead of a CUDA-graph replay")
     ap.add_argument("--exchange", default="auto", choices=["auto", "segments", "nccl", "direct"],
                     help="N > 1: auto (segments when identity-prefix segments stay in place, "
                          "else nccl), the exchange-free segment path, partition + one grouped "

@@ -73,6 +73,7 @@ Tuning read_tuning() {
   t.no_match = flag("LCO_NO_MATCH");
   t.lsd_maxbits = num("LCO_LSD_MAXBITS", 1, 11, 0);
   t.stable_msd = flag("LCO_STABLE_MSD");
+  t.no_single = flag("LCO_NO_SINGLE");
   return t;
 }
 
@@ -84,6 +85,18 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz, const Tuning& tu) {
   if (op.path == kPathCopy || B == 0) {
     c.path = kPathCopy;
     c.cost = 36;
+    return c;
+  }
+  // one tile, one digit: a single stable pass of one CTA (no count / scan kernels)
+  if (nnz <= 8192 && B <= 10 && !tu.no_single) {
+    c.path = kPathSingle;
+    c.rb = B <= 8 ? 8 : 10;
+    c.cost = 36;
+    c.passes = 1;
+    c.kp.passes = 1;  // the one digit: all B bits of q
+    c.kp.dshift[0] = 0;
+    c.kp.dbits[0] = B;
+    build_digit_moves(&c.kp);
     return c;
   }
   if (nnz <= leaf_cap()) {
@@ -341,6 +354,7 @@ cudaError_t execute(lco_plan_s* h, const OpPlan& op, bool unique, uint64_t nnz,
   io.kB = hasB ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
   io.vB = hasB && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
   io.pB = hasB && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
+  if (cp.path == kPathSingle) return run_single_tile(cp.rb, cp.kp, io, L);
   if (cp.path == kPathOnesweep) return run_passes(cp.rb, cp.kp, io, L);
   if (cp.path == kPathTile) return run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
   if (cp.path == kPathSeg) return run_seg(cp.msd.b1, cp.msd.b2, cp.kp, io, L);
@@ -974,10 +988,11 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   info->passes = cp.passes;
   for (int j = 0; j < cp.passes && j < 8; ++j) info->digit_bits[j] = cp.kp.dbits[j];
   if (cp.path == kPathSeg) info->digit_bits[0] = cp.msd.b2;  // the middle digit
-  info->radix_bits = cp.path == kPathOnesweep ? cp.rb
+  info->radix_bits = (cp.path == kPathOnesweep || cp.path == kPathSingle) ? cp.rb
                                                 : (cp.path == kPathMsd ? 8 : (cp.path == kPathSeg ? pass_rb(cp.msd.b2) : 0));
   info->path = cp.path;
-  info->tile = cp.path == kPathOnesweep || cp.path == kPathMsd
+  info->tile = cp.path == kPathSingle ? 8192
+              : cp.path == kPathOnesweep || cp.path == kPathMsd
                    ? pass_tile()
                    : (cp.path == kPathTile ? (int)tile_nominal(nnz, cp.segments) : 0);
   info->msd_levels = cp.msd.levels;
@@ -1022,7 +1037,7 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
   // kernels of this library per call (cudaMemsetAsync not counted)
   int launches = 0;
   if (nnz > 0) {
-    if (cp.path == kPathCopy || cp.path == kPathLocal) launches = 1;
+    if (cp.path == kPathCopy || cp.path == kPathLocal || cp.path == kPathSingle) launches = 1;
     else if (cp.path == kPathTile) launches = 3;  // bounds, tile sorts, deferred tiles
     else if (cp.path == kPathSeg) launches = 6;   // count, scan, tiles, count, offsets, scatter
     else if (cp.path == kPathBlock) launches = 5; // bounds, counts, 2 scan, tiles

@@ -142,6 +142,7 @@ struct PassParams {
   int unstable;
   uint32_t tile;  // records per tile of unsegmented passes (0: kTile)
   int persist;    // persistent grid: each CTA loops over tiles (tile table length on device)
+  int single;     // the whole input is one tile: its sorted order is the output order
 };
 
 // PER consecutive uint16 tile-histogram entries in, PER uint32 offsets out (vector

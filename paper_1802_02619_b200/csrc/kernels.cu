@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int d = tid + b * NT;
-    if (d < BINS) gbase[d] = __ldcs(io.toff + (size_t)t * BINS + d);
+    if (d < BINS) gbase[d] = a.single ? 0u : __ldcs(io.toff + (size_t)t * BINS + d);
   }
   {
     const DigitFn dg(a);
@@ -465,7 +465,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   for (int b = 0; b < NB; ++b) {
     const int d = tid + b * NT;
     if (d < BINS) {
-      gbase[d] -= loff[d];  // global position of local slot 0 of digit d
+      // global position of local slot 0 of digit d (single tile: the tile order is final)
+      gbase[d] = a.single ? 0u : gbase[d] - loff[d];
       if (io.direct) gbase[d] -= io.bucket[d];  // ... within its destination's chunk
     }
   }
@@ -649,6 +650,41 @@ static cudaError_t launch_scatter_rb(bool first, bool last, bool vals, const Pas
   if (first) return launch_scatter_t<RB, true, false>(vals, a, io, grid, s);
   if (!last) return launch_scatter_t<RB, false, false>(vals, a, io, grid, s);
   return launch_scatter_t<RB, false, true>(vals, a, io, grid, s);
+}
+
+// The whole input as one tile of up to kTileL records sorted on a digit of <= 10 bits:
+// one stable pass of one 1,024-thread CTA whose tile order is the final order (no
+// count / scan / offsets kernels: C1-sized tensors are launch-latency bound).
+template <int RB>
+static cudaError_t launch_single_t(bool vals, const PassParams& a, const ScatterIO& io,
+                                   cudaStream_t s) {
+  constexpr int NL = scatter_nt(RB, kTileL);
+  constexpr size_t smem = scatter_smem_bytes<RB, kTileL>();
+  auto fn = vals ? k_scatter<RB, true, true, true, NL, false, false, kTileL>
+                 : k_scatter<RB, true, true, false, NL, false, false, kTileL>;
+  cudaError_t e = kernel_setup(reinterpret_cast<const void*>(fn), smem, NL);
+  if (e != cudaSuccess) return e;
+  fn<<<1, NL, smem, s>>>(a, io);
+  return cudaGetLastError();
+}
+
+cudaError_t run_single_tile(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L) {
+  PassParams a;
+  memset(&a, 0, sizeof a);
+  a.kp = kp;
+  a.kp.passes = 1;
+  a.qshift = kp.divT.kind == 1 ? (int)kp.divT.s : (kp.divT.kind == 0 ? 0 : -1);
+  a.nnz = io.nnz;
+  a.tile = kTileL;
+  a.tiles = 1;
+  a.single = 1;
+  ScatterIO sio = pass_buffers(io, 0, true, nullptr);
+  if (L.mark) L.mark(L.ctx, "k_scatter_single_tile");
+  switch (rb) {
+    case 8: return launch_single_t<8>(io.vals_out != nullptr, a, sio, L.stream);
+    case 10: return launch_single_t<10>(io.vals_out != nullptr, a, sio, L.stream);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_scatter(int rb, bool first, bool last, bool vals, const PassParams& a,

@@ -97,6 +97,8 @@ ScatterIO pass_buffers(const PassIO& io, int j, bool last, const uint32_t* toff)
 cudaError_t run_pass(int rb, const PassParams& a, const PassIO& io, int j, bool first, bool last,
                      const Launch& L, bool count_only = false);
 cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
+// nnz <= 8,192 and one digit of <= 10 bits: one CTA, one stable pass (kernels.cu)
+cudaError_t run_single_tile(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
 // partition (io.splitters set): one pass; count_only stops after the digit totals
 // (io.counts64 written)
 cudaError_t run_partition(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L,

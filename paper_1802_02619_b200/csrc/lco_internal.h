@@ -197,7 +197,7 @@ LCO_HD uint32_t digit_of(const KeyPlan& p, uint64_t q, int pass) {
 }
 
 enum Path { kPathCopy = 0, kPathOnesweep = 1, kPathLocal = 2, kPathMsd = 3, kPathTile = 4,
-            kPathSeg = 5, kPathBlock = 7 };
+            kPathSeg = 5, kPathBlock = 7, kPathSingle = 8 };
 
 // Host plan for one operation (permute or sort) of a handle.
 struct OpPlan {
@@ -244,6 +244,7 @@ struct Tuning {
   int no_match;     // LCO_NO_MATCH: LSD passes never rank with match.any
   int lsd_maxbits;  // LCO_LSD_MAXBITS (0: default), clamped to 1..11
   int stable_msd;   // LCO_STABLE_MSD: MSD passes of lco_permute ranked stably
+  int no_single;    // LCO_NO_SINGLE: no single-tile pass for tiny inputs
 };
 
 }  // namespace lco

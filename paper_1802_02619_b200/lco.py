@@ -24,7 +24,8 @@ LIB_PATH = os.path.join(_HERE, "liblco.so")
 FLAG_VALIDATE = 1
 FLAG_HIERARCHICAL = 2
 MAX_ORDER = 16
-PATHS = {0: "copy", 1: "lsd", 2: "leaf", 3: "msd", 4: "tile", 5: "seg", 6: "hier", 7: "block"}
+PATHS = {0: "copy", 1: "lsd", 2: "leaf", 3: "msd", 4: "tile", 5: "seg", 6: "hier", 7: "block",
+         8: "single"}
 
 _STATUS = {
     0: "LCO_OK", 1: "LCO_ERR_NULL", 2: "LCO_ERR_ORDER", 3: "LCO_ERR_DIM", 4: "LCO_ERR_PERM",
@@ -514,6 +515,33 @@ class Plan:
             _check(lib().lco_key_histogram(self._h, keys.numel(), _ptr(keys), int(bits),
                                            _ptr(counts), _stream_ptr(stream, dev)))
         return counts
+
+    def graph(self, keys, vals=None, idx=None, out=None, workspace=None, sort=False):
+        """Capture one lco_permute (or lco_sort) call on fixed device buffers into a CUDA
+        graph and return it: ``g.replay()`` re-runs the whole call -- every kernel the
+        library launches for it, on the same inputs, outputs and workspace -- as one graph
+        launch, which removes the per-kernel launch latency and host overhead that bound
+        small tensors (SURVEY.md §7 "launch-latency-bound" configs).  The buffers must stay
+        alive and in place while the graph is used."""
+        fn = self.sort if sort else self.permute
+        n = keys.numel()
+        dev = keys.device
+        if out is None:
+            out = (torch.empty_like(keys), None if vals is None else torch.empty_like(vals),
+                   torch.empty(n, dtype=torch.int32, device=dev))
+        if workspace is None:
+            workspace = torch.empty(self.workspace_size(n) + 256, dtype=torch.uint8, device=dev)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up: kernel attributes set before capture
+            fn(keys, vals, idx, out=out, workspace=workspace)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn(keys, vals, idx, out=out, workspace=workspace)
+        g.out = out
+        g.workspace = workspace
+        return g
 
     # ---------------------------------------------------------------- measurement hook
     def profile_enable(self, calls: int):

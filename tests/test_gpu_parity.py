@@ -692,3 +692,30 @@ def test_msd_level3_laplacian_skew(perm, sort, cuda_device, monkeypatch):
     assert info["path"] == "msd" and info["msd_levels"] == 2, info
     check((n,) * 4, perm, keys, vals, sort=sort)
     check((n,) * 4, perm, keys, None, sort=sort, return_perm=False)
+
+
+@pytest.mark.parametrize("nnz", [1, 100, 4095, 4097, 5000, 8192])
+def test_single_tile_path(nnz, cuda_device):
+    """Inputs of <= 8,192 nonzeros whose disturbed digits fit 10 bits: one stable pass of
+    one CTA, the tile order is the output order (C1's schedule); every permutation of
+    an order-3 shape, with / without values, permutation vector and idx_in."""
+    rng = np.random.default_rng(nnz)
+    dims = (16, 12, 5)  # q of every permutation has <= 10 bits
+    total = int(np.prod(dims))
+    keys = np.sort(rng.choice(total, min(nnz, total), replace=False)).astype(np.uint64)
+    if nnz > total:  # larger tensors: (40, 30, 8) has q <= 10 bits for perms moving c2 first
+        dims = (40, 30, 8)
+        keys = np.sort(rng.choice(40 * 30 * 8, nnz, replace=False)).astype(np.uint64)
+    vals = rng.standard_normal(len(keys))
+    idx = (rng.permutation(len(keys)) + 17).astype(np.uint32)
+    for perm in itertools.permutations(range(3)):
+        info = lco.plan(dims, perm).info(len(keys))
+        if info["sort_bits"] == 0:
+            continue
+        if info["sort_bits"] <= 10:
+            assert info["path"] == "single", (perm, info["path"])
+        check(dims, perm, keys, vals)
+        check(dims, perm, keys, None, return_perm=False)
+        check(dims, perm, keys, vals, idx=idx)
+    w = workloads.config("C1")
+    assert lco.plan(w.dims, w.perms[0]).info(w.keys.numel())["path"] == "single"

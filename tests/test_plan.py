@@ -100,7 +100,7 @@ def test_baseline_config_plans():
     """Key bits the passes sort per BASELINE config (SURVEY.md §8(a) sizes table) and the
     schedule chosen at the config's nnz."""
     cases = {
-        ("C1", (64, 48, 32), (2, 0, 1), 5000): (5, "leaf"),
+        ("C1", (64, 48, 32), (2, 0, 1), 5000): (5, "single"),
         ("C2a", (512,) * 4, (2, 3, 0, 1), 1308672): (18, "msd"),
         ("C2b", (512,) * 4, (0, 2, 1, 3), 1308672): (18, "tile"),
         ("C3a", (128,) * 6, (3, 4, 5, 0, 1, 2), 14581760): (21, "lsd"),
@@ -135,6 +135,9 @@ def test_call_schedules():
     otherwise (modelled bytes decide; results are identical)."""
     p = lco.Plan((4096,) * 5, (4, 3, 2, 1, 0))
     assert p.info(1000)["path"] == "leaf"
+    # one tile of <= 8,192 nonzeros and a digit of <= 10 bits: one stable single-CTA pass
+    assert lco.Plan((64, 48, 32), (2, 0, 1)).info(5000)["path"] == "single"
+    assert lco.Plan((64, 48, 32), (2, 0, 1)).info(8193)["path"] != "single"
     i = p.info(500_000_000)
     assert i["path"] == "msd" and i["msd_levels"] == 2
     assert sum(i["digit_bits"]) + i["leaf_bits"] == 48
