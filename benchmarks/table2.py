@@ -4,8 +4,10 @@ SURVEY §8(f) NEXT 1): every one of the 23 non-identity permutations of a 4th-or
 tensor, permuted with RP (lco_permute: stable radix over only the disturbed digits of
 the shaved key) versus a full stable radix sort of the shuffled keys (lco_sort: all key
 digits), on (a) the combinatorial Laplacian of Eq (2.3) at N = 2^11.5 ~ 2896 (Table 2's
-size, ~42M nonzeros) and (b) a 2%-fill tensor.  Both produce identical outputs (checked
-here on every permutation).  Times are CUDA-event medians with inputs resident in HBM.
+size, ~42M nonzeros) and (b) a 2%-fill tensor.  Both produce identical outputs, and the
+RP output passes the output certificate (perm bijection, key = re-encode of its source,
+value bits, strictly increasing keys) -- both checked on every permutation.  Times are
+CUDA-event medians with inputs resident in HBM.
 
     python benchmarks/table2.py [--n 2896] [--fill-n 200] [--reps 5] [--out profiles/...]
 """
@@ -52,6 +54,33 @@ def timed(fn, reps):
     return float(np.median([a.elapsed_time(b) for a, b in ev]))
 
 
+def _reencode(keys, dims, perm):
+    """K' of every key by torch integer ops (decode from the last mode, Horner under the
+    new order): an independent check of the library's LIV shuffle."""
+    c = [None] * len(dims)
+    k = keys.clone()
+    for m in range(len(dims) - 1, -1, -1):
+        c[m] = k % dims[m]
+        k = k // dims[m]
+    out = torch.zeros_like(keys)
+    for p in perm:
+        out = out * dims[p] + c[p]
+    return out
+
+
+def certified(keys, vals, dims, perm, out):
+    """The output certificate (with unique input keys it implies equality with the
+    definition): perm a bijection, key = re-encode(source key), value bits of the source,
+    keys strictly increasing."""
+    ko, vo, po = out
+    n = keys.numel()
+    src = po.long()
+    return bool(torch.equal(torch.sort(src).values, torch.arange(n, device=keys.device))
+                and torch.equal(ko, _reencode(keys[src], dims, perm))
+                and torch.equal(vo.view(torch.int64), vals[src].view(torch.int64))
+                and bool((ko[1:] > ko[:-1]).all()))
+
+
 def run(name, keys, vals, dims, reps):
     n = keys.numel()
     rows = []
@@ -66,7 +95,8 @@ def run(name, keys, vals, dims, reps):
                  torch.empty(n, dtype=torch.int32, device=keys.device))
         t_rp = timed(lambda: p.permute(keys, vals, out=out_p, workspace=ws), reps)
         t_sort = timed(lambda: p.sort(keys, vals, out=out_s, workspace=ws), reps)
-        same = all(torch.equal(x, y) for x, y in zip(out_p, out_s))
+        same = all(torch.equal(x, y) for x, y in zip(out_p, out_s)) and \
+            certified(keys, vals, dims, perm, out_p)
         ip, isr = p.info(n), p.info(n, sort=True)
         # the hierarchical plan (LCO_FLAG_HIERARCHICAL): one stable sort per run of
         # rearrangement indices, where the permutation has >= 2 runs

@@ -74,6 +74,9 @@ Tuning read_tuning() {
   t.lsd_maxbits = num("LCO_LSD_MAXBITS", 1, 11, 0);
   t.stable_msd = flag("LCO_STABLE_MSD");
   t.no_single = flag("LCO_NO_SINGLE");
+  t.no_l3 = flag("LCO_NO_L3");
+  t.l3_flat = flag("LCO_L3_FLAT");
+  t.l3_bits = num("LCO_L3_BITS", -1, 8, 0);
   return t;
 }
 

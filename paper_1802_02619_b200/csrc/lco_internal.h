@@ -245,6 +245,9 @@ struct Tuning {
   int lsd_maxbits;  // LCO_LSD_MAXBITS (0: default), clamped to 1..11
   int stable_msd;   // LCO_STABLE_MSD: MSD passes of lco_permute ranked stably
   int no_single;    // LCO_NO_SINGLE: no single-tile pass for tiny inputs
+  int no_l3;        // LCO_NO_L3: no MSD level-3 re-split (oversize leaves stream)
+  int l3_flat;      // LCO_L3_FLAT: level-3 count / scatter one CTA per tile (debug)
+  int l3_bits;      // LCO_L3_BITS: level-3 digit bits (0: default 8; -1 via "z": 0 bits)
 };
 
 }  // namespace lco

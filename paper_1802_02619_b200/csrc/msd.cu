@@ -37,6 +37,13 @@ constexpr int kSmallBucket = 16;     // buckets up to this size are finished by 
 constexpr int kLeafThreads = 256;
 constexpr int kLeafWarps = kLeafThreads / 32;
 
+// Deferred-leaf list entry: leaf level code (0-4, three bits) and slot (< 2^29).
+constexpr int kEntryShift = 29;
+constexpr uint32_t kEntrySlot = (1u << kEntryShift) - 1u;
+__host__ __device__ __forceinline__ uint32_t leaf_entry(int level, uint32_t slot) {
+  return ((uint32_t)level << kEntryShift) | slot;
+}
+
 // ---------------------------------------------------------------------------------
 // k_msd_tiles: one CTA, thread b = level-1 bucket (<= 1024).  Buckets larger than `cap` get tiles
 // in the level-2 tile table; the rest are leaves.
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(1024) k_list_tiles(const uint32_t* __restrict_
     const uint32_t e = c0 + tid;
     uint32_t st = 0, sz = 0;
     if (e < m) {
-      const uint32_t slot = list[e] & ((1u << 30) - 1u);  // entries: level << 30 | slot
+      const uint32_t slot = list[e] & kEntrySlot;  // entries: leaf_entry(level, slot)
       st = base2[slot];
       sz = btot2[slot];
     }
@@ -233,7 +240,7 @@ struct LeafArgs {
   double* vals_out;
   uint32_t* perm_out;
   // leaves a warp could not sort (too large, or skewed buckets) go to a list that the
-  // block-level kernel drains: entry = level << 30 | slot
+  // block-level kernel drains: entry = leaf_entry(level, slot)
   uint32_t* defer;
   uint32_t* ndefer;
   const uint32_t* dlist;   // block kernel: deferred list to drain (null: slot mode)
@@ -312,14 +319,14 @@ __device__ __forceinline__ bool leaf_at(const LeafArgs& L, int level, uint32_t s
 }
 
 // Next leaf of this CTA at or after position `k` (stride gridDim.x) of its work list:
-// the deferred list (entries level << 30 | slot) or, without one, the slots of
+// the deferred list (entries leaf_entry(level, slot)) or, without one, the slots of
 // L.only_level.
 __device__ __forceinline__ bool next_leaf(const LeafArgs& L, uint32_t& k, LeafDesc* d) {
   if (L.dlist) {
     const uint32_t cnt = *L.dcount;
     for (; k < cnt; k += gridDim.x) {
       const uint32_t e = L.dlist[k];
-      if (leaf_at(L, (int)(e >> 30), e & ((1u << 30) - 1), d)) return true;
+      if (leaf_at(L, (int)(e >> kEntryShift), e & kEntrySlot, d)) return true;
     }
     return false;
   }
@@ -327,6 +334,17 @@ __device__ __forceinline__ bool next_leaf(const LeafArgs& L, uint32_t& k, LeafDe
   for (; k < nslots; k += gridDim.x)
     if (leaf_at(L, L.only_level, k, d)) return true;
   return false;
+}
+
+// Entry that sends the leaf at work-list position k to the next deferred list: the
+// slot of L.only_level, or (draining a list) the entry as it was listed.
+__device__ __forceinline__ uint32_t defer_entry(const LeafArgs& L, uint32_t k) {
+  return L.dlist ? L.dlist[k] : leaf_entry(L.only_level, k);
+}
+
+// Remaining key bits of a leaf: per level when draining a deferred list.
+__device__ __forceinline__ int leaf_rb(const LeafArgs& L, const LeafDesc& d) {
+  return !L.dlist ? L.rb : (d.level == 1 ? L.rb1 : (d.level == 4 ? L.rb4 : L.rb));
 }
 
 // Sort key of a staged record: the leaf's remaining bits of q = K' div T, or (tile path,
@@ -673,7 +691,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
     LeafDesc d;
     bool ok = myslot < nslots && leaf_at(L, level, (uint32_t)myslot, &d);
     if (ok && d.n > (uint32_t)kWCap) {  // larger than a warp leaf: defer
-      L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)level << 30) | (uint32_t)myslot;
+      L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(level, (uint32_t)myslot);
       ok = false;
     }
     uint32_t todo = __ballot_sync(0xffffffffu, ok);
@@ -750,7 +768,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
       }
       if (__any_sync(0xffffffffu, big)) {  // skewed leaf: the block kernel sorts it
         const uint32_t slot = (uint32_t)__shfl_sync(0xffffffffu, (uint32_t)myslot, l);
-        if (lane == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)level << 30) | slot;
+        if (lane == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(level, slot);
         __syncwarp();
         continue;
       }
@@ -814,16 +832,17 @@ __global__ void __launch_bounds__(kCThreads, (BIG && CAP > 4096) ? 1 : 2)
   __shared__ int s_big;
   const int tid = threadIdx.x;
   const bool want_pos = L.perm_out != nullptr;
-  const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
   uint32_t k = blockIdx.x;
   LeafDesc d;
   while (next_leaf(L, k, &d)) {
+    const int rbl = leaf_rb(L, d);
+    const uint64_t mask = rbl >= 64 ? ~0ull : ((1ull << rbl) - 1ull);
     const uint32_t n = d.n, start = d.start;
     const uint64_t* sk = d.src == 0 ? L.keys_in : (d.src == 1 ? L.kA : L.kB);
     const double* sv = d.src == 0 ? L.vals_in : (d.src == 1 ? L.vA : L.vB);
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)CAP) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
       k += gridDim.x;
       continue;
     }
@@ -982,7 +1001,7 @@ __global__ void __launch_bounds__(kCThreads, (BIG && CAP > 4096) ? 1 : 2)
             xb = t;
           }
         } else {
-          for (int sh = 0; sh < L.rb; sh += 8) {
+          for (int sh = 0; sh < rbl; sh += 8) {
             leaf_rank_pass<8, kCThreads>(L, K, mask, xa, xb, n, sh, WH, s_loff, s_cnt, s_warp);
             uint16_t* t = xa;
             xa = xb;
@@ -991,7 +1010,7 @@ __global__ void __launch_bounds__(kCThreads, (BIG && CAP > 4096) ? 1 : 2)
         }
         order = xa;
       } else {  // skewed leaf: the block-level kernel sorts it
-        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
         __syncthreads();
         k += gridDim.x;
         continue;
@@ -1062,7 +1081,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     const double* sv = d.src == 1 ? L.vA : L.vB;
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)kCCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
       k += gridDim.x;
       continue;
     }
@@ -1106,7 +1125,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     const uint64_t kmin = s_min, range = s_max - s_min;
     const int rbits = range ? 64 - __clzll((long long)range) : 0;
     if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
       k += gridDim.x;
       __syncthreads();
       continue;
@@ -1186,7 +1205,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     if (big) s_big = 1;
     __syncthreads();
     if (s_big) {  // skewed leaf: the block-level kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
       k += gridDim.x;
       __syncthreads();  // everyone has read s_big before the next leaf resets it
       continue;
@@ -1262,7 +1281,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
     const double* sv = d.src == 1 ? L.vA : L.vB;
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)kSCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
       k += gridDim.x;
       continue;
     }
@@ -1310,7 +1329,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       const uint64_t range = s_max - s_min;
       rbits = range ? 64 - __clzll((long long)range) : 0;
       if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
-        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
         k += gridDim.x;
         __syncthreads();
         continue;
@@ -1454,7 +1473,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       if (big) s_big = 1;
       __syncthreads();
       if (s_big) {  // skewed leaf: the block-level kernel sorts it
-        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = ((uint32_t)L.only_level << 30) | k;
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
         k += gridDim.x;
         __syncthreads();
         continue;
@@ -1826,7 +1845,7 @@ size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz, uint32_t tile) {
     s += (tiles2 * rbins2 * 2 + 255) / 256 * 256;   // thist2
     s += (tiles2 * rbins2 * 4 + 255) / 256 * 256;   // toff2
     s += l3_bytes(nb1, rbins2, nnz, tile);          // level-3 re-split tables
-    s = (s + 255) / 256 * 256 + (nb1 * rbins2 + nb1 + (size_t)l3_cap(nnz) * 256 + 64) * 4;
+    s = (s + 255) / 256 * 256 + 2 * (nb1 * rbins2 + nb1 + (size_t)l3_cap(nnz) * 256 + 64) * 4;
   } else {
     s += (2 * nb1 + 64) * 4;
   }
@@ -1956,14 +1975,17 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
                           (mp.levels == 2 ? (size_t)l3_cap(nnz) << kL3Bits : 0) + 64;
   uint32_t* defer = reinterpret_cast<uint32_t*>(cb);
   uint32_t* ndefer = defer + ndef_cap - 1;
+  uint32_t* defer2 = defer + ndef_cap;  // leaves the 8K-capacity drain could not sort
+  uint32_t* ndefer2 = defer2 + ndef_cap - 1;
   if ((e = cudaMemsetAsync(ndefer, 0, 4, Lc.stream)) != cudaSuccess) return e;
   L.defer = defer;
   L.ndefer = ndefer;
   // level 3 applies to CTA leaves with bits left to split
-  const bool lev3 = mp.levels == 2 && mp.cta && mp.rb >= 1;
+  const bool lev3 = mp.levels == 2 && mp.cta && mp.rb >= 1 && !(io.tune && io.tune->no_l3);
   // level-3 digit: 8 bits (4 bits measured: on Table 2's Laplacian the next bits of q hold
   // a mode the stencil ties to an earlier one, so 16 sub-buckets stayed oversize)
-  const int b3 = lev3 ? (mp.rb < kL3Digit ? mp.rb : kL3Digit) : 0;
+  int b3 = lev3 ? (mp.rb < kL3Digit ? mp.rb : kL3Digit) : 0;
+  if (lev3 && io.tune && io.tune->l3_bits) b3 = io.tune->l3_bits < 0 ? 0 : io.tune->l3_bits;
   if (mp.levels == 2) {
     LeafArgs L2 = L;
     L2.only_level = 2;
@@ -2005,9 +2027,14 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     a3.persist = 1;  // the table's length is known on the device only: persistent grids
     int sms = 148;
     if ((e = device_sms(&sms)) != cudaSuccess) return e;
-    const uint32_t g3 = (uint32_t)sms * (tile == (uint32_t)kTileL ? 1u : 2u);
+    uint32_t g3 = (uint32_t)sms * (tile == (uint32_t)kTileL ? 1u : 2u);
+    uint32_t gc3 = 4u * g3;
+    if (io.tune && io.tune->l3_flat) {
+      a3.persist = 0;
+      g3 = gc3 = (uint32_t)l3.tiles3;
+    }
     if (Lc.mark) Lc.mark(Lc.ctx, "k_count_l3");
-    if ((e = launch_count(kL3Bits, false, a3, io.kB, l3.thist3, l3.btot3, 4u * g3, Lc.stream)) !=
+    if ((e = launch_count(kL3Bits, false, a3, io.kB, l3.thist3, l3.btot3, gc3, Lc.stream)) !=
         cudaSuccess)
       return e;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg_l3");
@@ -2043,8 +2070,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     e = vals ? launch_leafw<true>(L1, Lc.stream) : launch_leafw<false>(L1, Lc.stream);
   }
   if (e != cudaSuccess) return e;
-  // deferred leaves (both levels share one list; rb depends on the entry's level)
-  if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf_deferred");
+  // deferred leaves (all levels share one list; rb depends on the entry's level)
   LeafArgs LD = L;
   LD.dlist = defer;
   LD.dcount = ndefer;
@@ -2057,6 +2083,22 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     LD.rb1 += log2T;
     LD.rb4 += log2T;
   }
+  if (lev3) {
+    // level-3 leaves a staged CTA leaf could not sort (larger than its capacity, or a
+    // crowded bucket): first one CTA per leaf with 64-bit keys in shared memory (k_leafc,
+    // up to 8,192 nonzeros), then the streaming sort drains what is left
+    if ((e = cudaMemsetAsync(ndefer2, 0, 4, Lc.stream)) != cudaSuccess) return e;
+    LeafArgs LC = LD;
+    LC.defer = defer2;
+    LC.ndefer = ndefer2;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_leafc_deferred");
+    e = vals ? launch_leafc_t<true, false>(LC, 1u << 30, Lc.stream)
+             : launch_leafc_t<false, false>(LC, 1u << 30, Lc.stream);
+    if (e != cudaSuccess) return e;
+    LD.dlist = defer2;
+    LD.dcount = ndefer2;
+  }
+  if (Lc.mark) Lc.mark(Lc.ctx, "k_leaf_deferred");
   return run_leaf(LD, 1u << 20, vals, Lc.stream);
 }
 

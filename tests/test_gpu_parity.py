@@ -719,3 +719,38 @@ def test_single_tile_path(nnz, cuda_device):
         check(dims, perm, keys, vals, idx=idx)
     w = workloads.config("C1")
     assert lco.plan(w.dims, w.perms[0]).info(w.keys.numel())["path"] == "single"
+
+
+@pytest.mark.parametrize("stable", [False, True])
+def test_msd_level3_crowded_leaves(stable, cuda_device, monkeypatch):
+    """C3b's operator under a forced two-level MSD plan: every q value is shared by 128+
+    nonzeros (the suffix modes z, z'), so level-2 leaves are oversize, level-3 leaves are
+    crowded and go to the deferred list as level-code-4 entries (a regression: the code
+    once overflowed the entry's 2-bit level field and those leaves were never written).
+    Both the unordered (K' tie-break) and the stable passes, bit-exact."""
+    monkeypatch.setenv("LCO_MSD", "1")
+    monkeypatch.setenv("LCO_MSD_CTA", "1")
+    if stable:
+        monkeypatch.setenv("LCO_STABLE_MSD", "1")
+    w = workloads.config("C3", scale=96)
+    dims, perm = w.dims, w.perms[1]
+    info = lco.plan(dims, perm).info(w.keys.numel())
+    assert info["path"] == "msd" and info["msd_levels"] == 2
+    check(dims, perm, _np_u64(w.keys), w.vals.numpy())
+
+
+def test_table2_laplacian_level3_full(cuda_device):
+    """Table 2's worst permutations at the paper's size (N = 2896, 42M nonzeros), default
+    plans (two MSD levels + level 3): permute and sort bit-exact against the oracle (the
+    all-cores run of the same definition, oracle.permute_par)."""
+    n = 2896
+    k, v = workloads.combinatorial_laplacian(n)
+    keys, vals = _np_u64(k), v.numpy()
+    dk, dv = k.to(cuda_device), v.to(cuda_device)
+    for perm, sort in (((3, 1, 2, 0), False), ((0, 2, 1, 3), True)):
+        p = lco.plan((n,) * 4, perm)
+        ko, vo, po = (p.sort if sort else p.permute)(dk, dv)
+        ek, ev, ep = oracle.permute_par((n,) * 4, perm, keys, vals)
+        assert np.array_equal(_np_u64(ko), ek), perm
+        assert np.array_equal(po.cpu().numpy().view(np.uint32), ep), perm
+        assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64)), perm
