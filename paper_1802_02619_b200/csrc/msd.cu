@@ -762,7 +762,9 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
         uint32_t r = lo;
         for (uint32_t j = lo; j < hi; ++j) {
           const uint64_t kj = RK[j];
-          r += (kj < k || (kj == k && X[j] < x)) ? 1u : 0u;
+          // (key, K', index), as k_leafs: equal keys in K' order (unordered MSD passes)
+          const uint16_t y = X[j];
+          r += (kj < k || (kj == k && (K[y] < K[x] || (K[y] == K[x] && y < x)))) ? 1u : 0u;
         }
         F[r] = x;
       }
@@ -1866,8 +1868,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   // by (remaining q bits, K'), and the deferred streaming sort by the low bits of K' that
   // hold those q bits and the suffix -- a power-of-two T keeps them contiguous.
   const int log2T = kp.divT.kind == 0 ? 0 : (kp.divT.kind == 1 ? (int)kp.divT.s : -1);
-  const bool unst = io.unique && mp.levels == 2 && mp.cta && log2T >= 0 &&
-                    mp.rb + mp.b2 + log2T <= 64;
+  const bool unst = io.unique && mp.levels == 2 && log2T >= 0 && mp.rb + mp.b2 + log2T <= 64;
   a.unstable = unst ? 1 : 0;
   // unordered passes after the first: 8,192-record tiles (twice as long a run per digit,
   // one CTA per SM); the first pass keeps 4,096 (two CTAs per SM measured faster there)

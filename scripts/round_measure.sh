@@ -15,15 +15,17 @@ done
 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/m_ref_C5.json 2> gpurun_out/m_ref_C5.err; echo "ref rc=$?"
 for c in C5 C4 C3a C3b C2a C2b C1; do
   lc=$(echo $c | tr A-Z a-z)
-  python bench.py --config $c --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_plain_$c.log 2>&1 && \
+  python bench.py --config $c --steps 2 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_plain_$c.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-      --csv --log-file gpurun_out/m_${lc}_launches.csv python bench.py --config $c --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_launch_$c.log 2>&1
+      --csv --log-file gpurun_out/m_${lc}_launches.csv python bench.py --config $c --steps 2 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_ncu_launch_$c.log 2>&1
   echo "launches $c rc=$?"
 done
-ncu --set full --clock-control none --import-source on -k regex:"k_leaf|k_scatter" -s 4 -c 3 \
-    -o gpurun_out/m_c5_full -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_c5.log 2>&1
+python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_plain_full5.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_leafs" -s 5 -c 3 \
+    -o gpurun_out/m_c5_full -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_ncu_c5.log 2>&1
 echo "c5 full rc=$?"
+python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_plain_full4.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"k_block_tiles|k_block_bounds" -s 2 -c 2 \
-    -o gpurun_out/m_c4_full -f python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu > gpurun_out/m_ncu_c4.log 2>&1
+    -o gpurun_out/m_c4_full -f python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_ncu_c4.log 2>&1
 echo "c4 full rc=$?"
 python benchmarks/table2.py --reps 5 --out gpurun_out/m_table2.md > gpurun_out/m_table2.log 2>&1; echo "table2 rc=$?"
