@@ -77,6 +77,7 @@ Tuning read_tuning() {
   t.no_l3 = flag("LCO_NO_L3");
   t.l3_flat = flag("LCO_L3_FLAT");
   t.l3_bits = num("LCO_L3_BITS", -1, 8, 0);
+  t.single_cta = flag("LCO_SINGLE_CTA");
   return t;
 }
 
@@ -357,7 +358,9 @@ cudaError_t execute(lco_plan_s* h, const OpPlan& op, bool unique, uint64_t nnz,
   io.kB = hasB ? reinterpret_cast<uint64_t*>(ws + w.kB) : nullptr;
   io.vB = hasB && mv ? reinterpret_cast<double*>(ws + w.vB) : nullptr;
   io.pB = hasB && mp ? reinterpret_cast<uint32_t*>(ws + w.pB) : nullptr;
-  if (cp.path == kPathSingle) return run_single_tile(cp.rb, cp.kp, io, L);
+  if (cp.path == kPathSingle)
+    return h->tune.single_cta ? run_single_tile(cp.rb, cp.kp, io, L)
+                              : run_single_cluster(cp.rb, cp.kp, io, L);
   if (cp.path == kPathOnesweep) return run_passes(cp.rb, cp.kp, io, L);
   if (cp.path == kPathTile) return run_tiles(cp.kp, cp.segdiv, cp.segments, h->key_bits, io, L);
   if (cp.path == kPathSeg) return run_seg(cp.msd.b1, cp.msd.b2, cp.kp, io, L);

@@ -99,6 +99,8 @@ cudaError_t run_pass(int rb, const PassParams& a, const PassIO& io, int j, bool 
 cudaError_t run_passes(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
 // nnz <= 8,192 and one digit of <= 10 bits: one CTA, one stable pass (kernels.cu)
 cudaError_t run_single_tile(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
+// the same pass on a cluster of 8 CTAs exchanging digit counts through DSMEM (small.cu)
+cudaError_t run_single_cluster(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L);
 // partition (io.splitters set): one pass; count_only stops after the digit totals
 // (io.counts64 written)
 cudaError_t run_partition(int rb, const KeyPlan& kp, const PassIO& io, const Launch& L,

@@ -247,7 +247,8 @@ struct Tuning {
   int no_single;    // LCO_NO_SINGLE: no single-tile pass for tiny inputs
   int no_l3;        // LCO_NO_L3: no MSD level-3 re-split (oversize leaves stream)
   int l3_flat;      // LCO_L3_FLAT: level-3 count / scatter one CTA per tile (debug)
-  int l3_bits;      // LCO_L3_BITS: level-3 digit bits (0: default 8; -1 via "z": 0 bits)
+  int l3_bits;      // LCO_L3_BITS: level-3 digit bits (0: default 8; -1: 0 bits)
+  int single_cta;   // LCO_SINGLE_CTA: the single-tile pass on one CTA, not a cluster
 };
 
 }  // namespace lco

@@ -248,6 +248,12 @@ struct LeafArgs {
   // level 3: segment-aligned tiles of the raw input (k_tile_bounds), tstart[0..ntiles]
   const uint32_t* tstart;
   uint32_t ntiles;
+  // tile path with the bounds found inline (k_leafc BIG): each CTA searches the boundaries
+  // of its tile and records them in tstart (for a deferred tile), no k_tile_bounds launch
+  int tile_inline;
+  FastDiv segd;
+  uint64_t segD;
+  uint32_t tileT;
   // MSD level 3 (leaf level code 4, data in buffer A): level-2 leaves that did not fit a
   // leaf were split again on the next b3 bits; entry e of the level-3 list owns slots
   // e << b3 .. (e << b3) + 2^b3 - 1 of base3 / btot3
@@ -334,6 +340,46 @@ __device__ __forceinline__ bool next_leaf(const LeafArgs& L, uint32_t& k, LeafDe
   for (; k < nslots; k += gridDim.x)
     if (leaf_at(L, L.only_level, k, d)) return true;
   return false;
+}
+
+// First segment boundary at or after position c * T (0 for c = 0, nnz past the end); one
+// warp, all lanes participate, the result is warp-uniform.
+__device__ __forceinline__ uint32_t seg_tile_bound(const uint64_t* __restrict__ keys, uint64_t nnz,
+                                                   const FastDiv& segd, uint64_t D, uint32_t T,
+                                                   uint32_t c) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t x = (uint64_t)c * T;
+  if (c == 0 || x >= nnz) return c == 0 ? 0u : (uint32_t)nnz;
+  const uint64_t sprev = fdiv(segd, __ldg(keys + x - 1));
+  if (fdiv(segd, __ldg(keys + x)) != sprev) return (uint32_t)x;
+  const uint64_t bound = (sprev + 1) * D;  // first key of the next segment, <= prod(dims)
+  uint64_t lo = x + 1, hi = nnz;  // answer in [lo, hi]: keys[lo-1] < bound, keys[hi] >= bound
+  while (hi - lo > 32) {
+    const uint64_t step = (hi - lo + 32) / 33;
+    const uint64_t pos = lo + (uint64_t)(lane + 1) * step - 1;  // lane 31: < hi
+    const bool below = pos < hi && __ldg(keys + pos) < bound;
+    const uint32_t m = __ballot_sync(0xffffffffu, below);  // a prefix of the lanes
+    const int nb = __popc(m);
+    const uint64_t nlo = nb ? lo + (uint64_t)nb * step : lo;  // first position not known below
+    const uint64_t nhi = nb < 32 ? lo + (uint64_t)(nb + 1) * step - 1 : hi;
+    lo = nlo;
+    hi = nhi < hi ? nhi : hi;
+  }
+  // at most 32 candidates left: one probe each
+  const uint64_t pos = lo + lane;
+  const bool below = pos < hi && __ldg(keys + pos) < bound;
+  const uint32_t m = __ballot_sync(0xffffffffu, below);
+  return (uint32_t)(lo + __popc(m));
+}
+
+__global__ void k_tile_bounds(const uint64_t* __restrict__ keys, uint64_t nnz, FastDiv segd,
+                              uint64_t D, uint32_t T, uint32_t ntiles, uint32_t* __restrict__ tstart,
+                              uint32_t* __restrict__ ndefer) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ndefer = 0u;  // the tile sort's deferred list
+  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c > ntiles) return;
+  const uint32_t b = seg_tile_bound(keys, nnz, segd, D, T, c);
+  if ((threadIdx.x & 31) == 0) tstart[c] = b;
 }
 
 // Entry that sends the leaf at work-list position k to the next deferred list: the
@@ -834,9 +880,33 @@ __global__ void __launch_bounds__(kCThreads, (BIG && CAP > 4096) ? 1 : 2)
   __shared__ int s_big;
   const int tid = threadIdx.x;
   const bool want_pos = L.perm_out != nullptr;
+  __shared__ uint32_t s_tb[2];
   uint32_t k = blockIdx.x;
   LeafDesc d;
-  while (next_leaf(L, k, &d)) {
+  for (;;) {
+    if (BIG && L.tile_inline) {  // tile path: this tile's bounds, searched here
+      if (k >= L.ntiles) break;
+      if (tid < 32) {
+        const uint32_t b0 = seg_tile_bound(L.keys_in, L.a.nnz, L.segd, L.segD, L.tileT, k);
+        const uint32_t b1 = seg_tile_bound(L.keys_in, L.a.nnz, L.segd, L.segD, L.tileT, k + 1);
+        if (tid == 0) {
+          s_tb[0] = b0;
+          s_tb[1] = b1;
+          uint32_t* ts = const_cast<uint32_t*>(L.tstart);  // a deferred tile is found there
+          ts[k] = b0;
+          ts[k + 1] = b1;
+        }
+      }
+      __syncthreads();
+      d = LeafDesc{s_tb[0], s_tb[1] - s_tb[0], 0, 3};
+      __syncthreads();  // s_tb is rewritten by the next tile
+      if (d.n == 0) {
+        k += gridDim.x;
+        continue;
+      }
+    } else if (!next_leaf(L, k, &d)) {
+      break;
+    }
     const int rbl = leaf_rb(L, d);
     const uint64_t mask = rbl >= 64 ? ~0ull : ((1ull << rbl) - 1ull);
     const uint32_t n = d.n, start = d.start;
@@ -1605,40 +1675,6 @@ static cudaError_t launch_leafc(const LeafArgs& L, bool vals, bool single, uint3
 // One warp per tile boundary: the 32 lanes probe 32 evenly spaced keys of the remaining
 // range, so every round of one L2 / HBM round trip narrows it 33-fold (4 rounds for a
 // million-nonzero search instead of 20 dependent probes).
-__global__ void k_tile_bounds(const uint64_t* __restrict__ keys, uint64_t nnz, FastDiv segd,
-                              uint64_t D, uint32_t T, uint32_t ntiles, uint32_t* __restrict__ tstart) {
-  const uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (c > ntiles) return;
-  const uint64_t x = (uint64_t)c * T;
-  if (c == 0 || x >= nnz) {
-    if (lane == 0) tstart[c] = c == 0 ? 0u : (uint32_t)nnz;
-    return;
-  }
-  const uint64_t sprev = fdiv(segd, __ldg(keys + x - 1));
-  if (fdiv(segd, __ldg(keys + x)) != sprev) {
-    if (lane == 0) tstart[c] = (uint32_t)x;
-    return;
-  }
-  const uint64_t bound = (sprev + 1) * D;  // first key of the next segment, <= prod(dims)
-  uint64_t lo = x + 1, hi = nnz;  // answer in [lo, hi]: keys[lo-1] < bound, keys[hi] >= bound
-  while (hi - lo > 32) {
-    const uint64_t step = (hi - lo + 32) / 33;
-    const uint64_t pos = lo + (uint64_t)(lane + 1) * step - 1;  // lane 31: < hi
-    const bool below = pos < hi && __ldg(keys + pos) < bound;
-    const uint32_t m = __ballot_sync(0xffffffffu, below);  // a prefix of the lanes
-    const int nb = __popc(m);
-    const uint64_t nlo = nb ? lo + (uint64_t)nb * step : lo;  // first position not known below
-    const uint64_t nhi = nb < 32 ? lo + (uint64_t)(nb + 1) * step - 1 : hi;
-    lo = nlo;
-    hi = nhi < hi ? nhi : hi;
-  }
-  // at most 32 candidates left: one probe each
-  const uint64_t pos = lo + lane;
-  const bool below = pos < hi && __ldg(keys + pos) < bound;
-  const uint32_t m = __ballot_sync(0xffffffffu, below);
-  if (lane == 0) tstart[c] = (uint32_t)(lo + __popc(m));
-}
 
 // Tiles of the segment-local path are sorted by k_leafc with a 4K cap (two CTAs per
 // SM).  Nominal tile: a tile overshoots it by at most one segment, and segments are
@@ -1667,11 +1703,10 @@ cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int
   uint32_t* tstart = io.ctrl;
   uint32_t* defer = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(io.ctrl) +
                                                 ((size_t)(nt + 1) * 4 + 255) / 256 * 256);
-  uint32_t* ndefer = defer + nt + 32;
-  if ((e = cudaMemsetAsync(ndefer, 0, 4, Lc.stream)) != cudaSuccess) return e;
+  uint32_t* ndefer = defer + nt + 32;  // zeroed by k_tile_bounds (one graph node fewer)
   if (Lc.mark) Lc.mark(Lc.ctx, "k_tile_bounds");
   k_tile_bounds<<<(nt + 1 + 7) / 8, 256, 0, Lc.stream>>>(io.keys_in, nnz, make_fastdiv(segdiv),
-                                                            segdiv, T, nt, tstart);
+                                                            segdiv, T, nt, tstart, ndefer);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   LeafArgs L;
   memset(&L, 0, sizeof L);
@@ -1697,6 +1732,9 @@ cudaError_t run_tiles(const KeyPlan& kp, uint64_t segdiv, uint64_t segments, int
   L.perm_out = io.perm_out;
   L.tstart = tstart;
   L.ntiles = nt;
+  // (tile_inline: each tile CTA searching its own bounds measured slower, C2b 0.052 ->
+  // 0.065 ms: two dependent searches per tile, not overlapped; k_tile_bounds kept)
+  L.tile_inline = 0;
   L.defer = defer;
   L.ndefer = ndefer;
   if (Lc.mark) Lc.mark(Lc.ctx, "k_leafc_tiles");

@@ -694,11 +694,15 @@ def test_msd_level3_laplacian_skew(perm, sort, cuda_device, monkeypatch):
     check((n,) * 4, perm, keys, None, sort=sort, return_perm=False)
 
 
-@pytest.mark.parametrize("nnz", [1, 100, 4095, 4097, 5000, 8192])
-def test_single_tile_path(nnz, cuda_device):
-    """Inputs of <= 8,192 nonzeros whose disturbed digits fit 10 bits: one stable pass of
-    one CTA, the tile order is the output order (C1's schedule); every permutation of
-    an order-3 shape, with / without values, permutation vector and idx_in."""
+@pytest.mark.parametrize("nnz,one_cta", [(1, False), (100, False), (4095, False), (4097, False),
+                                         (5000, False), (8192, False), (5000, True), (8192, True)])
+def test_single_tile_path(nnz, one_cta, cuda_device, monkeypatch):
+    """Inputs of <= 8,192 nonzeros whose disturbed digits fit 10 bits: one stable counting
+    pass (C1's schedule) -- on a cluster of 8 CTAs exchanging digit counts through DSMEM
+    (default), or one CTA whose tile order is the output order (LCO_SINGLE_CTA); every
+    permutation of an order-3 shape, with / without values, permutation vector, idx_in."""
+    if one_cta:
+        monkeypatch.setenv("LCO_SINGLE_CTA", "1")
     rng = np.random.default_rng(nnz)
     dims = (16, 12, 5)  # q of every permutation has <= 10 bits
     total = int(np.prod(dims))
