@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(kWWarps * 32) k_leafw(const __grid_constant__ 
   const bool want_pos = L.perm_out != nullptr;
   const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
   const int level = L.only_level;
-  const uint32_t nslots = leaf_slots(L, level);
+  const uint32_t nslots = level == 4 ? (*L.n3 << L.b3) : leaf_slots(L, level);
   const uint32_t W = gridDim.x * kWWarps;
   const uint32_t gw = blockIdx.x * kWWarps + warp;
   const uint32_t ltm = lanemask_lt();
@@ -1153,7 +1153,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     const double* sv = d.src == 1 ? L.vA : L.vB;
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)kCCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
       k += gridDim.x;
       continue;
     }
@@ -1197,7 +1197,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     const uint64_t kmin = s_min, range = s_max - s_min;
     const int rbits = range ? 64 - __clzll((long long)range) : 0;
     if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
       k += gridDim.x;
       __syncthreads();
       continue;
@@ -1277,7 +1277,7 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
     if (big) s_big = 1;
     __syncthreads();
     if (s_big) {  // skewed leaf: the block-level kernel sorts it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
       k += gridDim.x;
       __syncthreads();  // everyone has read s_big before the next leaf resets it
       continue;
@@ -1353,7 +1353,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
     const double* sv = d.src == 1 ? L.vA : L.vB;
     const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
     if (n > (uint32_t)kSCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
+      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
       k += gridDim.x;
       continue;
     }
@@ -1401,7 +1401,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       const uint64_t range = s_max - s_min;
       rbits = range ? 64 - __clzll((long long)range) : 0;
       if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
-        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
         k += gridDim.x;
         __syncthreads();
         continue;
@@ -1545,7 +1545,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       if (big) s_big = 1;
       __syncthreads();
       if (s_big) {  // skewed leaf: the block-level kernel sorts it
-        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = leaf_entry(L.only_level, k);
+        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
         k += gridDim.x;
         __syncthreads();
         continue;
@@ -2094,8 +2094,25 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     LeafArgs L4 = L;
     L4.only_level = 4;
     L4.rb = mp.rb - b3;
-    if (Lc.mark) Lc.mark(Lc.ctx, leafc_kernel(L4, false, false, true));
-    if ((e = launch_leafc(L4, vals, false, 1u << 30, Lc.stream)) != cudaSuccess) return e;
+    // level-3 leaves are small (a listed leaf of a few thousand nonzeros split 256 ways):
+    // one warp per leaf of <= 384; the larger ones are listed for the staged CTA leaves,
+    // and what those cannot sort goes to the k_leafc drain below
+    uint32_t* mlist = defer2;  // free until the drain below
+    uint32_t* nmlist = ndefer2;
+    if ((e = cudaMemsetAsync(nmlist, 0, 4, Lc.stream)) != cudaSuccess) return e;
+    L4.defer = mlist;
+    L4.ndefer = nmlist;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_leafw_l3");
+    if ((e = vals ? launch_leafw<true>(L4, Lc.stream) : launch_leafw<false>(L4, Lc.stream)) !=
+        cudaSuccess)
+      return e;
+    LeafArgs LM = L;  // drains the list into the final deferred list
+    LM.dlist = mlist;
+    LM.dcount = nmlist;
+    LM.rb = mp.rb - b3;
+    LM.rb4 = mp.rb - b3;
+    if (Lc.mark) Lc.mark(Lc.ctx, leafc_kernel(LM, false, false, true));
+    if ((e = launch_leafc(LM, vals, false, 1u << 30, Lc.stream)) != cudaSuccess) return e;
   }
   // level-1 buckets that were not split again sort the bits left after level 1
   LeafArgs L1 = L;
