@@ -232,9 +232,11 @@ constexpr int scatter_nt(int rb, int tile = kTile) {
   return tile > kTile ? 1024 : (rb <= 10 ? 512 : 256);
 }
 
-template <int RB, int TILE = kTile>
+template <int RB, int TILE = kTile, bool EARLY = false>
 constexpr size_t scatter_smem_bytes() {
-  return (size_t)TILE * (8 + 8 + 4 + 2) + (size_t)(1 << RB) * 8;
+  // EARLY: + the digit counters [bins] u32 and the slot -> input position map [tile] u16
+  return (size_t)TILE * (8 + 8 + 4 + 2) + (size_t)(1 << RB) * 8 +
+         (EARLY ? (size_t)TILE * 2 + (size_t)(1 << RB) * 4 : 0);
 }
 
 // NT threads (IT = kTile / NT nonzeros each): 512 for digits of <= 10 bits (more warps
@@ -252,6 +254,10 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   constexpr int IT = TILE / NT;
   constexpr int NB = BINS >= NT ? BINS / NT : 1;
   static_assert(UNST || W * BINS * 2 <= TILE * 8, "warp counters must fit in sV");
+  // first unordered pass: V in input order, loaded with the keys (measured: first pass
+  // 4.66 -> 4.24 ms on C5; the level-2 pass, one CTA per SM, 6.84 -> 7.44: its slot-order
+  // gathers from shared memory conflict more than the early loads save)
+  constexpr bool EARLY = UNST && FIRST;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* sK = reinterpret_cast<uint64_t*>(smem);              // [TILE]
   double* sV = reinterpret_cast<double*>(sK + TILE);              // [TILE]
@@ -260,6 +266,10 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   uint16_t* sdig = reinterpret_cast<uint16_t*>(sP + TILE);        // [TILE]
   uint32_t* gbase = reinterpret_cast<uint32_t*>(sdig + TILE);     // [BINS]
   uint32_t* loff = gbase + BINS;                                  // [BINS]
+  // EARLY: V stays in input order (loaded at the start of the tile, in flight during the
+  // ranking); sidx maps a slot to its input position
+  uint32_t* ucnt = loff + BINS;                                   // [BINS] (EARLY)
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(ucnt + BINS);      // [TILE] (EARLY)
   __shared__ uint32_t s_warp[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -289,8 +299,10 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
       prefetch_l2(io.toff + (size_t)t2 * BINS, (size_t)BINS * 4);
     }
   }
+  // UNST digit counters: their own array when V is staged early, else inside sV
+  uint32_t* cnt = EARLY ? ucnt : reinterpret_cast<uint32_t*>(whist);
   if (UNST) {
-    for (int i = tid; i < BINS; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
+    for (int i = tid; i < BINS; i += NT) cnt[i] = 0u;
   } else {
     for (int i = tid; i < W * BINS / 2; i += NT) reinterpret_cast<uint32_t*>(whist)[i] = 0u;
   }
@@ -301,6 +313,18 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   for (int it = 0; it < IT; ++it) {
     const uint32_t pos = warp * 32 * IT + it * 32 + lane;
     key[it] = pos < n ? __ldcs((FIRST ? io.keys_in : io.kin) + base + pos) : 0ull;
+  }
+  if (EARLY) {  // values in input order, in flight while the keys are ranked
+    const bool want_p0 = !FIRST && io.pout != nullptr;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const uint32_t pos = warp * 32 * IT + it * 32 + lane;
+      if (pos < n) {
+        if (VALS) cp_async8(sV + pos, (FIRST ? io.vals_in : io.vin) + base + pos);
+        if (want_p0) cp_async4(sP + pos, io.pin + base + pos);
+      }
+    }
+    cp_async_commit();
   }
   // global offsets of this tile's digit runs (from the exclusive scan)
 #pragma unroll
@@ -339,7 +363,6 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   if (UNST) {
     // ---- unordered slots: one shared atomic per record on the tile's digit counter;
     // tiles with few distinct digits aggregate a warp's equal digits first (match.any)
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(whist);
     const bool few = ADAPT && *a.distinct < (uint64_t)((a.tiles + 31) / 32) *
                                                 ((1u << a.kp.dbits[a.pass]) / 8);
     if (few) {
@@ -369,6 +392,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
         const uint32_t lp = loff[d] + (meta[it] >> 16);
         sK[lp] = key[it];
         sdig[lp] = (uint16_t)d;
+        if (EARLY) sidx[lp] = (uint16_t)(warp * 32 * IT + it * 32 + lane);
         meta[it] = d | (lp << 16);
       }
     }
@@ -447,6 +471,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   const bool want_p = io.pout != nullptr || io.direct;
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
+    if (EARLY) break;  // loaded in input order above
     if ((meta[it] & 0xFFFFu) == kInvalid) continue;
     const uint32_t pos = warp * 32 * IT + it * 32 + lane;
     const uint32_t lp = meta[it] >> 16;
@@ -483,6 +508,15 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
       io.dp[d][w] = sP[p];
     }
   } else {
+    if (EARLY) {
+      for (uint32_t p = tid; p < n; p += NT) {
+        const uint32_t g = gbase[sdig[p]] + p;
+        const uint32_t src = sidx[p];
+        io.kout[g] = sK[p];
+        if (VALS) io.vout[g] = sV[src];
+        if (io.pout) io.pout[g] = FIRST ? (uint32_t)(base + src) : sP[src];
+      }
+    } else
     for (uint32_t p = tid; p < n; p += NT) {
       const uint32_t g = gbase[sdig[p]] + p;
       io.kout[g] = sK[p];
@@ -621,7 +655,7 @@ static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const Scatte
   void (*fn)(const PassParams, const ScatterIO);
   if (a.unstable && !LST && a.tile == (uint32_t)kTileL) {  // large tiles, one CTA per SM
     constexpr int NL = scatter_nt(RB, kTileL);
-    smem = scatter_smem_bytes<RB, kTileL>();
+    smem = scatter_smem_bytes<RB, kTileL, F>();
     fn = vals ? k_scatter<RB, F, false, true, NL, false, true, kTileL>
               : k_scatter<RB, F, false, false, NL, false, true, kTileL>;
     cudaError_t e = kernel_setup(reinterpret_cast<const void*>(fn), smem, NL);
@@ -630,6 +664,7 @@ static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const Scatte
     return cudaGetLastError();
   }
   if (a.unstable && !LST) {  // MSD passes of lco_permute (the last pass is never one)
+    smem = scatter_smem_bytes<RB, kTile, F>();
     if (a.distinct) fn = vals ? k_scatter<RB, F, false, true, NT, true, true> : k_scatter<RB, F, false, false, NT, true, true>;
     else fn = vals ? k_scatter<RB, F, false, true, NT, false, true> : k_scatter<RB, F, false, false, NT, false, true>;
   } else if (a.distinct) {
