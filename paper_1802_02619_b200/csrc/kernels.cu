@@ -226,10 +226,21 @@ __global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ Pa
 //   write   one loop writes K', V and the position of each slot to toff + rank:
 //           consecutive threads write consecutive slots, i.e. runs of equal digit.
 // Shared memory: sK [tile] u64 | sV [tile] f64 (holds the per-warp counters while
-// ranking) | sP [tile] u32 | sdig [tile] u16 | gbase [bins] u32 | loff [bins] u32.
+// ranking) | sP [tile] u32 | gbase [bins] u32 | loff [bins] u32 | (first unordered pass:
+// counters [bins] u32, slot -> input position [tile] u16) | sdig [tile] u16, left out
+// in passes after the first when the write loop shifts the digit out of the staged K'
+// (power-of-two T; the L1 keeps the 16 KB: C5 level-2 pass 6.71 -> 6.28 ms, C3b middle
+// pass -5 %; first passes measured slower with the dependent load).
 // ---------------------------------------------------------------------------------
 constexpr int scatter_nt(int rb, int tile = kTile) {
   return tile > kTile ? 1024 : (rb <= 10 ? 512 : 256);
+}
+
+// The write loop of a pass after the first takes a slot's digit from its staged K' (a
+// shift: q = K' >> qshift) instead of a staged copy; the launch then leaves out the sdig
+// array (more L1).
+__host__ __device__ inline bool scatter_keydig(const PassParams& a) {
+  return a.qshift >= 0 && !a.splitters;
 }
 
 template <int RB, int TILE = kTile, bool EARLY = false>
@@ -263,13 +274,16 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   double* sV = reinterpret_cast<double*>(sK + TILE);              // [TILE]
   uint16_t* whist = reinterpret_cast<uint16_t*>(sV);              // [W][BINS] (ranking only)
   uint32_t* sP = reinterpret_cast<uint32_t*>(sV + TILE);          // [TILE]
-  uint16_t* sdig = reinterpret_cast<uint16_t*>(sP + TILE);        // [TILE]
-  uint32_t* gbase = reinterpret_cast<uint32_t*>(sdig + TILE);     // [BINS]
+  uint32_t* gbase = reinterpret_cast<uint32_t*>(sP + TILE);       // [BINS]
   uint32_t* loff = gbase + BINS;                                  // [BINS]
   // EARLY: V stays in input order (loaded at the start of the tile, in flight during the
   // ranking); sidx maps a slot to its input position
   uint32_t* ucnt = loff + BINS;                                   // [BINS] (EARLY)
-  uint16_t* sidx = reinterpret_cast<uint16_t*>(ucnt + BINS);      // [TILE] (EARLY)
+  uint16_t* sidx = reinterpret_cast<uint16_t*>(ucnt + (EARLY ? BINS : 0));  // [TILE] (EARLY)
+  // slot digits, last: absent (not allocated) when the write loop takes the digit from
+  // the staged key (a shift of K', scatter_keydig)
+  uint16_t* sdig = sidx + (EARLY ? TILE : 0);                     // [TILE]
+  const bool kdig = !FIRST && scatter_keydig(a) && !io.direct && !io.keep_old_key;
   __shared__ uint32_t s_warp[32];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -391,7 +405,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
       if (d != kInvalid) {
         const uint32_t lp = loff[d] + (meta[it] >> 16);
         sK[lp] = key[it];
-        sdig[lp] = (uint16_t)d;
+        if (!kdig) sdig[lp] = (uint16_t)d;
         if (EARLY) sidx[lp] = (uint16_t)(warp * 32 * IT + it * 32 + lane);
         meta[it] = d | (lp << 16);
       }
@@ -461,7 +475,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
     if (d != kInvalid) {
       const uint32_t lp = loff[d] + whist[warp * BINS + d] + (meta[it] >> 16);
       sK[lp] = key[it];
-      sdig[lp] = (uint16_t)d;
+      if (!kdig) sdig[lp] = (uint16_t)d;
       meta[it] = d | (lp << 16);
     }
   }
@@ -508,18 +522,21 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
       io.dp[d][w] = sP[p];
     }
   } else {
+    const DigitFn dgw(a);
     if (EARLY) {
       for (uint32_t p = tid; p < n; p += NT) {
-        const uint32_t g = gbase[sdig[p]] + p;
+        const uint64_t k = sK[p];
+        const uint32_t g = gbase[kdig ? dgw(a, k) : (uint32_t)sdig[p]] + p;
         const uint32_t src = sidx[p];
-        io.kout[g] = sK[p];
+        io.kout[g] = k;
         if (VALS) io.vout[g] = sV[src];
         if (io.pout) io.pout[g] = FIRST ? (uint32_t)(base + src) : sP[src];
       }
     } else
     for (uint32_t p = tid; p < n; p += NT) {
-      const uint32_t g = gbase[sdig[p]] + p;
-      io.kout[g] = sK[p];
+      const uint64_t k = sK[p];
+      const uint32_t g = gbase[kdig ? dgw(a, k) : (uint32_t)sdig[p]] + p;
+      io.kout[g] = k;
       if (VALS) io.vout[g] = sV[p];
       if (want_p) {
         const uint32_t v = sP[p];
@@ -651,11 +668,13 @@ template <int RB, bool F, bool LST>
 static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const ScatterIO& io,
                                    uint32_t grid, cudaStream_t s) {
   constexpr int NT = scatter_nt(RB);
-  size_t smem = scatter_smem_bytes<RB>();
+  // no sdig array (the last one) when the write loop takes digits from the keys
+  const bool kdig = !F && scatter_keydig(a) && !io.direct && !io.keep_old_key;
+  size_t smem = scatter_smem_bytes<RB>() - (kdig ? (size_t)kTile * 2 : 0);
   void (*fn)(const PassParams, const ScatterIO);
   if (a.unstable && !LST && a.tile == (uint32_t)kTileL) {  // large tiles, one CTA per SM
     constexpr int NL = scatter_nt(RB, kTileL);
-    smem = scatter_smem_bytes<RB, kTileL, F>();
+    smem = scatter_smem_bytes<RB, kTileL, F>() - (kdig ? (size_t)kTileL * 2 : 0);
     fn = vals ? k_scatter<RB, F, false, true, NL, false, true, kTileL>
               : k_scatter<RB, F, false, false, NL, false, true, kTileL>;
     cudaError_t e = kernel_setup(reinterpret_cast<const void*>(fn), smem, NL);
@@ -664,7 +683,7 @@ static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const Scatte
     return cudaGetLastError();
   }
   if (a.unstable && !LST) {  // MSD passes of lco_permute (the last pass is never one)
-    smem = scatter_smem_bytes<RB, kTile, F>();
+    smem = scatter_smem_bytes<RB, kTile, F>() - (kdig ? (size_t)kTile * 2 : 0);
     if (a.distinct) fn = vals ? k_scatter<RB, F, false, true, NT, true, true> : k_scatter<RB, F, false, false, NT, true, true>;
     else fn = vals ? k_scatter<RB, F, false, true, NT, false, true> : k_scatter<RB, F, false, false, NT, false, true>;
   } else if (a.distinct) {

@@ -24,6 +24,7 @@ struct Setup {
 std::mutex g_mu;
 std::map<std::tuple<int, const void*, size_t, int>, Setup> g_setup;
 std::map<int, int> g_sms;
+std::map<std::pair<int, const void*>, size_t> g_attr;  // largest attribute set per kernel
 
 }  // namespace
 
@@ -52,10 +53,15 @@ cudaError_t kernel_setup(const void* fn, size_t smem, int threads, int* per_sm, 
   std::lock_guard<std::mutex> lk(g_mu);
   auto it = g_setup.find(key);
   if (it == g_setup.end()) {
-    if (smem > 48 * 1024 &&
-        (e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-            cudaSuccess)
-      return e;
+    // the attribute only grows: a kernel launched with several shared-memory sizes keeps
+    // the largest one set
+    size_t& cur = g_attr[std::make_pair(dev, fn)];
+    if (smem > 48 * 1024 && smem > cur) {
+      if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+          cudaSuccess)
+        return e;
+      cur = smem;
+    }
     int n = 1;
     if (threads > 0 &&
         (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem)) != cudaSuccess)
