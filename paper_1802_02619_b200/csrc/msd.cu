@@ -1326,15 +1326,17 @@ constexpr int kSCap = 2304;
 constexpr int kSThreads = 256;
 constexpr int kSBucketBits = 12;  // 4,096 buckets (~0.5 nonzero each), u16 counts packed in pairs
 constexpr int kSSmall = 8;        // buckets up to this size are insertion-sorted by one thread
-constexpr size_t kSSmem = (size_t)kSCap * (8 + 8 + 4 + 4 + 2 + 2) + ((size_t)1 << kSBucketBits) * 2;
+// K / V / P get 2 / 2 / 4 spare slots: a leaf is staged at an offset that makes its
+// shared and global addresses congruent mod 16 (16-byte L2-only copies, stage_cg)
+constexpr size_t kSSmem = (size_t)kSCap * (8 + 8 + 4 + 4 + 2 + 2) + 48 + ((size_t)1 << kSBucketBits) * 2;
 
 template <bool VALS>
 __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ LeafArgs L) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* K = reinterpret_cast<uint64_t*>(smem);   // [cap] K' (input order)
-  double* V = reinterpret_cast<double*>(K + kSCap);   // [cap] values
-  uint32_t* P = reinterpret_cast<uint32_t*>(V + kSCap);  // [cap] positions
-  uint32_t* R = P + kSCap;                            // [cap] key - min
+  uint64_t* K0 = reinterpret_cast<uint64_t*>(smem);      // [cap + 2] K' (input order)
+  double* V0 = reinterpret_cast<double*>(K0 + kSCap + 2);  // [cap + 2] values
+  uint32_t* P0 = reinterpret_cast<uint32_t*>(V0 + kSCap + 2);  // [cap + 4] positions
+  uint32_t* R = P0 + kSCap + 4;                       // [cap] key - min
   uint16_t* X = reinterpret_cast<uint16_t*>(R + kSCap);  // [cap] bucket order
   uint16_t* F = X + kSCap;                            // [cap] final order
   uint32_t* B = reinterpret_cast<uint32_t*>(F + kSCap);  // [2^11] buckets
@@ -1357,11 +1359,14 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
       k += gridDim.x;
       continue;
     }
-    for (uint32_t i = tid; i < n; i += kSThreads) {
-      cp_async8(K + i, sk + (uint64_t)start + i);
-      if (VALS) cp_async8(V + i, sv + (uint64_t)start + i);
-      if (want_pos) cp_async4(P + i, sp + (uint64_t)start + i);
-    }
+    // staged at offsets congruent to the global addresses mod 16: 16-byte copies that
+    // hold no L1 lines in flight (three CTAs' stages leave the L1 ~40 KB)
+    uint64_t* K = K0 + (start & 1u);
+    double* V = V0 + (start & 1u);
+    uint32_t* P = P0 + (start & 3u);
+    stage_cg<8>(K, sk + start, n, tid, kSThreads);
+    if (VALS) stage_cg<8>(V, sv + start, n, tid, kSThreads);
+    if (want_pos) stage_cg<4>(P, sp + start, n, tid, kSThreads);
     cp_async_commit();
     if (tid == 0) {
       s_min = ~0ull;
