@@ -265,10 +265,11 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   constexpr int IT = TILE / NT;
   constexpr int NB = BINS >= NT ? BINS / NT : 1;
   static_assert(UNST || W * BINS * 2 <= TILE * 8, "warp counters must fit in sV");
-  // first unordered pass: V in input order, loaded with the keys (measured: first pass
-  // 4.66 -> 4.24 ms on C5; the level-2 pass, one CTA per SM, 6.84 -> 7.44: its slot-order
-  // gathers from shared memory conflict more than the early loads save)
-  constexpr bool EARLY = UNST && FIRST;
+  // unordered passes: V (and P) in input order, loaded with the keys, gathered by slot in
+  // the write loop -- first pass per-lane cp.async (C5 4.66 -> 4.24 ms), later passes
+  // 16-byte L2-only copies that hold no L1 lines (C5 level 2 6.28 -> 5.90 ms; the same
+  // with per-lane copies was slower, 7.44)
+  constexpr bool EARLY = UNST;
   extern __shared__ __align__(16) unsigned char smem[];
   uint64_t* sK = reinterpret_cast<uint64_t*>(smem);              // [TILE]
   double* sV = reinterpret_cast<double*>(sK + TILE);              // [TILE]
@@ -328,7 +329,11 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
     const uint32_t pos = warp * 32 * IT + it * 32 + lane;
     key[it] = pos < n ? __ldcs((FIRST ? io.keys_in : io.kin) + base + pos) : 0ull;
   }
-  if (EARLY) {  // values in input order, in flight while the keys are ranked
+  if (EARLY && !FIRST) {  // 16-byte L2-only copies of V and P in input order
+    if (VALS) stage_cg<8>(sV, io.vin + base, n, tid, NT);
+    if (io.pout != nullptr) stage_cg<4>(sP, io.pin + base, n, tid, NT);
+    cp_async_commit();
+  } else if (EARLY) {  // values in input order, in flight while the keys are ranked
     const bool want_p0 = !FIRST && io.pout != nullptr;
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
@@ -674,7 +679,7 @@ static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const Scatte
   void (*fn)(const PassParams, const ScatterIO);
   if (a.unstable && !LST && a.tile == (uint32_t)kTileL) {  // large tiles, one CTA per SM
     constexpr int NL = scatter_nt(RB, kTileL);
-    smem = scatter_smem_bytes<RB, kTileL, F>() - (kdig ? (size_t)kTileL * 2 : 0);
+    smem = scatter_smem_bytes<RB, kTileL, true>() - (kdig ? (size_t)kTileL * 2 : 0);
     fn = vals ? k_scatter<RB, F, false, true, NL, false, true, kTileL>
               : k_scatter<RB, F, false, false, NL, false, true, kTileL>;
     cudaError_t e = kernel_setup(reinterpret_cast<const void*>(fn), smem, NL);
@@ -683,7 +688,7 @@ static cudaError_t launch_scatter_t(bool vals, const PassParams& a, const Scatte
     return cudaGetLastError();
   }
   if (a.unstable && !LST) {  // MSD passes of lco_permute (the last pass is never one)
-    smem = scatter_smem_bytes<RB, kTile, F>() - (kdig ? (size_t)kTile * 2 : 0);
+    smem = scatter_smem_bytes<RB, kTile, true>() - (kdig ? (size_t)kTile * 2 : 0);
     if (a.distinct) fn = vals ? k_scatter<RB, F, false, true, NT, true, true> : k_scatter<RB, F, false, false, NT, true, true>;
     else fn = vals ? k_scatter<RB, F, false, true, NT, false, true> : k_scatter<RB, F, false, false, NT, false, true>;
   } else if (a.distinct) {
