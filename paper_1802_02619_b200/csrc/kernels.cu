@@ -324,15 +324,29 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   // ---- load keys; warp w owns a contiguous slice, lanes consecutive ----
   uint64_t key[IT];
   uint32_t meta[IT];
-#pragma unroll
-  for (int it = 0; it < IT; ++it) {
-    const uint32_t pos = warp * 32 * IT + it * 32 + lane;
-    key[it] = pos < n ? __ldcs((FIRST ? io.keys_in : io.kin) + base + pos) : 0ull;
-  }
-  if (EARLY && !FIRST) {  // 16-byte L2-only copies of V and P in input order
+  if (EARLY && !FIRST) {
+    // 16-byte L2-only copies in input order: the keys (one group, read back into
+    // registers below), then V and P (still in flight while the keys are ranked)
+    stage_cg<8>(sK, io.kin + base, n, tid, NT);
+    cp_async_commit();
     if (VALS) stage_cg<8>(sV, io.vin + base, n, tid, NT);
     if (io.pout != nullptr) stage_cg<4>(sP, io.pin + base, n, tid, NT);
     cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const uint32_t pos = warp * 32 * IT + it * 32 + lane;
+      key[it] = pos < n ? sK[pos] : 0ull;  // slots overwrite sK only after the ranking barrier
+    }
+  } else {
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const uint32_t pos = warp * 32 * IT + it * 32 + lane;
+      key[it] = pos < n ? __ldcs((FIRST ? io.keys_in : io.kin) + base + pos) : 0ull;
+    }
+  }
+  if (EARLY && !FIRST) {
   } else if (EARLY) {  // values in input order, in flight while the keys are ranked
     const bool want_p0 = !FIRST && io.pout != nullptr;
 #pragma unroll
