@@ -227,28 +227,32 @@ __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // 16 bytes, cached in L2 only: no L1 line is held while the data is in flight
-__device__ __forceinline__ void cp_async16_cg(void* smem_dst, const void* gsrc) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gsrc) : "memory");
+__device__ __forceinline__ void cp_async16_cg(uint32_t smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
 
 __device__ __forceinline__ uint32_t smem_addr16(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-// Stage n elements of E (4 or 8) bytes g[0..n) into s[0..n) with CTA threads tid / nt,
-// where s and g are congruent mod 16: 16-byte L2-only copies for the aligned body, one
-// element copies for the head and tail.
+// Stage n elements of E (4 or 8) bytes g[0..n) into s[0..n) with CTA threads tid / nt:
+// where s and g are congruent mod 16, 16-byte L2-only copies for the aligned body and
+// one-element copies for the head and tail (else one-element copies throughout).
 template <int E>
 __device__ __forceinline__ void stage_cg(void* s, const void* g, uint32_t n, int tid, int nt) {
   constexpr uint32_t PER = 16 / E;
-  char* sb = static_cast<char*>(s);
+  const uint32_t sa = smem_addr16(s);
   const char* gb = static_cast<const char*>(g);
   const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(gb) & 15u);
-  const bool cong = ((reinterpret_cast<uintptr_t>(gb) ^ (uintptr_t)smem_addr16(sb)) & 15u) == 0;
+  const bool cong = ((reinterpret_cast<uintptr_t>(gb) ^ sa) & 15u) == 0;
   const uint32_t h = cong ? (uint32_t)umin64(n, mis ? (16u - mis) / E : 0u) : n;
   const uint32_t m = (n - h) / PER;  // 16-byte chunks
-  for (uint32_t c = tid; c < m; c += nt) cp_async16_cg(sb + (size_t)(h + c * PER) * E, gb + (size_t)(h + c * PER) * E);
+  {
+    const uint32_t s0 = sa + h * E;
+    const char* g0 = gb + (size_t)h * E;
+    for (uint32_t c = tid; c < m; c += nt) cp_async16_cg(s0 + c * 16u, g0 + (size_t)c * 16u);
+  }
   const uint32_t t0 = h + m * PER;
+  char* sb = static_cast<char*>(s);
   for (uint32_t i = tid; i < h + (n - t0); i += nt) {  // head [0, h) and tail [t0, n)
     const uint32_t e = i < h ? i : t0 + (i - h);
     if (E == 8) cp_async8(sb + (size_t)e * 8, gb + (size_t)e * 8);
