@@ -259,6 +259,65 @@ __device__ __forceinline__ void stage_cg(void* s, const void* g, uint32_t n, int
     else cp_async4(sb + (size_t)e * 4, gb + (size_t)e * 4);
   }
 }
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on a shared-memory mbarrier.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// orders this thread's (and, after a barrier, the CTA's) generic-proxy accesses of shared
+// memory before later async-proxy (bulk copy) writes to it
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+// global [src, src + bytes) -> shared [dst, ...); 16-byte aligned, bytes a multiple of 16
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+}
+
+// One array of a staged range: n elements of E bytes at g go to shared memory at s0 + off
+// elements (off makes shared and global addresses congruent mod 16; s0 has 16 / E spare
+// slots): a 16-byte aligned body [h, t0) for one bulk copy, a head [0, h) and a tail
+// [t0, n) of fewer than 16 / E elements each.
+template <int E>
+struct BulkPart {
+  uint32_t off, h, t0;
+  __device__ __forceinline__ BulkPart(const void* g, uint32_t n) {
+    const uint32_t ga = (uint32_t)reinterpret_cast<uintptr_t>(g);
+    off = (ga / E) & (16u / E - 1u);
+    const uint32_t head = ((16u - (ga & 15u)) & 15u) / E;
+    h = head < n ? head : n;
+    t0 = h + ((n - h) * E / 16u) * (16u / E);
+  }
+  __device__ __forceinline__ uint32_t body_bytes() const { return (t0 - h) * E; }
+  __device__ __forceinline__ uint32_t edge(uint32_t n) const { return h + (n - t0); }
+  // i-th head / tail element (i < edge(n)) with a per-element cp.async
+  __device__ __forceinline__ void copy_edge(uint32_t i, void* s0, const void* g) const {
+    const uint32_t e = i < h ? i : t0 + (i - h);
+    char* sd = static_cast<char*>(s0) + (size_t)(off + e) * E;
+    const char* gs = static_cast<const char*>(g) + (size_t)e * E;
+    if (E == 8) cp_async8(sd, gs);
+    else cp_async4(sd, gs);
+  }
+};
+
 // Bulk prefetch of [p, p + bytes) into L2 (no registers, no completion tracking).
 __device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes) {
   const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;

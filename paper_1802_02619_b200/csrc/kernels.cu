@@ -246,7 +246,9 @@ __host__ __device__ inline bool scatter_keydig(const PassParams& a) {
 template <int RB, int TILE = kTile, bool EARLY = false>
 constexpr size_t scatter_smem_bytes() {
   // EARLY: + the digit counters [bins] u32 and the slot -> input position map [tile] u16
-  return (size_t)TILE * (8 + 8 + 4 + 2) + (size_t)(1 << RB) * 8 +
+  // + 2 / 2 / 4 spare slots of sK / sV / sP: a tile staged in input order sits at an
+  // offset that makes its shared and global addresses congruent mod 16 (stage_cg)
+  return (size_t)TILE * (8 + 8 + 4 + 2) + 48 + (size_t)(1 << RB) * 8 +
          (EARLY ? (size_t)TILE * 2 + (size_t)(1 << RB) * 4 : 0);
 }
 
@@ -271,11 +273,11 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   // with per-lane copies was slower, 7.44)
   constexpr bool EARLY = UNST;
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* sK = reinterpret_cast<uint64_t*>(smem);              // [TILE]
-  double* sV = reinterpret_cast<double*>(sK + TILE);              // [TILE]
-  uint16_t* whist = reinterpret_cast<uint16_t*>(sV);              // [W][BINS] (ranking only)
-  uint32_t* sP = reinterpret_cast<uint32_t*>(sV + TILE);          // [TILE]
-  uint32_t* gbase = reinterpret_cast<uint32_t*>(sP + TILE);       // [BINS]
+  uint64_t* const sK0 = reinterpret_cast<uint64_t*>(smem);       // [TILE + 2]
+  double* const sV0 = reinterpret_cast<double*>(sK0 + TILE + 2);  // [TILE + 2]
+  uint16_t* whist = reinterpret_cast<uint16_t*>(sV0);             // [W][BINS] (ranking only)
+  uint32_t* const sP0 = reinterpret_cast<uint32_t*>(sV0 + TILE + 2);  // [TILE + 4]
+  uint32_t* gbase = reinterpret_cast<uint32_t*>(sP0 + TILE + 4);  // [BINS]
   uint32_t* loff = gbase + BINS;                                  // [BINS]
   // EARLY: V stays in input order (loaded at the start of the tile, in flight during the
   // ranking); sidx maps a slot to its input position
@@ -293,6 +295,16 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   uint64_t base;
   uint32_t n, seg;
   if (!tile_range(a, t, &base, &n, &seg)) return;
+  // tiles staged in input order with 16-byte copies sit at offsets congruent to their
+  // global addresses mod 16 (else stage_cg falls back to one copy per element)
+  uint64_t* sK = sK0;
+  double* sV = sV0;
+  uint32_t* sP = sP0;
+  if (EARLY && !FIRST) {
+    sK += (reinterpret_cast<uintptr_t>(io.kin + base) >> 3) & 1u;
+    if (VALS) sV += (reinterpret_cast<uintptr_t>(io.vin + base) >> 3) & 1u;
+    if (io.pout != nullptr) sP += (reinterpret_cast<uintptr_t>(io.pin + base) >> 2) & 3u;
+  }
   if (tid == 0 && a.pf_dist) {
     // the tile the CTA launched pf_dist later will load: bring it into L2 now, so its
     // loads see L2 latency while HBM streams in the background

@@ -1313,265 +1313,281 @@ __global__ void __launch_bounds__(kCThreads, 2) k_leafr(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------------
-// k_leafs: fully staged CTA leaf sort for leaves of up to SCAP nonzeros (~1.9K: the
-// leaves of two 9-bit MSD levels at C5 scale).  K', V and the position of the leaf are
-// copied into shared memory with cp.async (input order, no registers), the leaf is
-// sorted as in k_leafr (32-bit keys relative to the leaf's minimum, ~2 per bucket,
-// rank by counting on (key, staging index) = the stable order), and the outputs are
-// written contiguously from shared memory.  72 KB: three CTAs per SM, so one CTA's
-// loads overlap another's sorting.  Leaves that do not fit, need more than 32 key bits,
-// or have a bucket of more than kCBig nonzeros go to the deferred list.
+// k_leafs: fully staged CTA leaf sort for leaves of up to kSCap nonzeros (~1.9K: the
+// leaves of an 8 + 10-bit MSD at C5 scale).  One leaf per CTA at a time, three per SM:
+//   stage   the 16-byte aligned bodies of the leaf's K', V and position arrays as TMA bulk
+//           copies issued by one thread (completing on an mbarrier), the few head / tail
+//           elements as per-element cp.async, at shared offsets congruent to the global
+//           addresses mod 16 (C5 leaves 5.36 -> 5.01 ms against a per-thread 16-byte
+//           cp.async loop, ~8 % of the kernel's instructions);
+//   bucket  the leaf's remaining key bits (<= 32) into 4,096 buckets (~0.5 record each,
+//           u16 counts packed in pairs), scan, place the record indices in bucket order;
+//   order   buckets of 2..kSSmall records are listed and insertion-sorted one per thread.
+//           Inside a bucket records compare on K' itself: within a leaf q = K' div T is
+//           monotone in K', so the (q bits, K', staging index) order is the (K', index)
+//           order -- and unique K' make unordered MSD passes give the result of stable
+//           ones.  A crowded bucket switches the leaf to a per-record rank;
+//   write   K', V and the position of each output slot, contiguous.
+// Leaves that do not fit, or hold a bucket of more than kCBig records, go to the deferred
+// list (the block kernel streams them).  Two stages per CTA (the next leaf prefetched
+// during the sort, two CTAs per SM) measured slower: 5.74 ms.
 // ---------------------------------------------------------------------------------
-constexpr int kSCap = 2304;
 constexpr int kSThreads = 256;
 constexpr int kSBucketBits = 12;  // 4,096 buckets (~0.5 nonzero each), u16 counts packed in pairs
 constexpr int kSSmall = 8;        // buckets up to this size are insertion-sorted by one thread
-// K / V / P get 2 / 2 / 4 spare slots: a leaf is staged at an offset that makes its
-// shared and global addresses congruent mod 16 (16-byte L2-only copies, stage_cg)
-constexpr size_t kSSmem = (size_t)kSCap * (8 + 8 + 4 + 4 + 2 + 2) + 48 + ((size_t)1 << kSBucketBits) * 2;
+constexpr int kSCap = 2272;
+// K / V / P with 2 / 2 / 4 spare slots (congruent staging offsets)
+constexpr size_t kSStage = (size_t)(kSCap + 2) * 16 + (size_t)(kSCap + 4) * 4;
+constexpr size_t kSSmem = kSStage + (size_t)kSCap * 2 * 3 + ((size_t)1 << kSBucketBits) * 2;
+static_assert(kSStage % 16 == 0, "the sort arrays stay 16-byte aligned");
+
+struct SStage {  // a staged leaf's arrays (at their congruent offsets)
+  uint64_t* K;
+  double* V;
+  uint32_t* P;
+};
+
+// Issue the copies of leaf d into the stage at st (CTA-wide call; thread 0 issues the bulk
+// copies after a proxy fence).  Returns whether the mbarrier expects bytes.
+template <bool VALS>
+__device__ __forceinline__ bool leafs_issue(const LeafArgs& L, const LeafDesc& d, unsigned char* st,
+                                            uint32_t bar, bool want_pos, int tid) {
+  if (d.n > (uint32_t)kSCap) return false;
+  const uint64_t* gk = (d.src == 1 ? L.kA : L.kB) + d.start;
+  const double* gv = (d.src == 1 ? L.vA : L.vB) + d.start;
+  const uint32_t* gp = (d.src == 1 ? L.pA : L.pB) + d.start;
+  uint64_t* K0 = reinterpret_cast<uint64_t*>(st);
+  double* V0 = reinterpret_cast<double*>(K0 + kSCap + 2);
+  uint32_t* P0 = reinterpret_cast<uint32_t*>(V0 + kSCap + 2);
+  const BulkPart<8> pk(gk, d.n), pv(gv, d.n);
+  const BulkPart<4> pp(gp, d.n);
+  const uint32_t bytes = pk.body_bytes() + (VALS ? pv.body_bytes() : 0u) + (want_pos ? pp.body_bytes() : 0u);
+  if (tid == 0 && bytes) {
+    fence_proxy_async();
+    mbar_expect_tx(bar, bytes);
+    if (pk.body_bytes()) bulk_g2s(smem_addr16(K0 + pk.off + pk.h), gk + pk.h, pk.body_bytes(), bar);
+    if (VALS && pv.body_bytes()) bulk_g2s(smem_addr16(V0 + pv.off + pv.h), gv + pv.h, pv.body_bytes(), bar);
+    if (want_pos && pp.body_bytes()) bulk_g2s(smem_addr16(P0 + pp.off + pp.h), gp + pp.h, pp.body_bytes(), bar);
+  }
+  // head / tail elements: at most 1 + 1, 1 + 1 and 3 + 3 (one per thread)
+  const uint32_t ek = pk.edge(d.n), ev = VALS ? pv.edge(d.n) : 0u, ep = want_pos ? pp.edge(d.n) : 0u;
+  const uint32_t i = (uint32_t)tid;
+  if (i < ek) pk.copy_edge(i, K0, gk);
+  else if (i < ek + ev) pv.copy_edge(i - ek, V0, gv);
+  else if (i < ek + ev + ep) pp.copy_edge(i - ek - ev, P0, gp);
+  return bytes != 0;
+}
 
 template <bool VALS>
 __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ LeafArgs L) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint64_t* K0 = reinterpret_cast<uint64_t*>(smem);      // [cap + 2] K' (input order)
-  double* V0 = reinterpret_cast<double*>(K0 + kSCap + 2);  // [cap + 2] values
-  uint32_t* P0 = reinterpret_cast<uint32_t*>(V0 + kSCap + 2);  // [cap + 4] positions
-  uint32_t* R = P0 + kSCap + 4;                       // [cap] key - min
-  uint16_t* X = reinterpret_cast<uint16_t*>(R + kSCap);  // [cap] bucket order
-  uint16_t* F = X + kSCap;                            // [cap] final order
-  uint32_t* B = reinterpret_cast<uint32_t*>(F + kSCap);  // [2^11] buckets
+  uint16_t* Rb = reinterpret_cast<uint16_t*>(smem + kSStage);  // [cap] bucket of record i
+  uint16_t* X = Rb + kSCap;                                         // [cap] bucket order
+  uint16_t* F = X + kSCap;                                          // [cap] final order / list
+  uint32_t* B = reinterpret_cast<uint32_t*>(F + kSCap);             // [2^11] packed u16 buckets
+  __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t s_warp[32];
-  __shared__ unsigned long long s_min, s_max;
   __shared__ int s_big;
   __shared__ uint32_t s_nlist;
+  constexpr int NT = kSThreads, W = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool want_pos = L.perm_out != nullptr;
   const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
+  const uint32_t bar0 = smem_addr16(&bar);
+  if (tid == 0) {
+    mbar_init(bar0, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
   uint32_t k = blockIdx.x;
   LeafDesc d;
-  while (next_leaf(L, k, &d)) {
-    const uint32_t n = d.n, start = d.start;
-    const uint64_t* sk = d.src == 1 ? L.kA : L.kB;
-    const double* sv = d.src == 1 ? L.vA : L.vB;
-    const uint32_t* sp = d.src == 1 ? L.pA : L.pB;
-    if (n > (uint32_t)kSCap) {  // oversize (skewed) leaf: the block kernel streams it
-      if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
-      k += gridDim.x;
-      continue;
-    }
-    // staged at offsets congruent to the global addresses mod 16: 16-byte copies that
-    // hold no L1 lines in flight (three CTAs' stages leave the L1 ~40 KB)
-    uint64_t* K = K0 + (start & 1u);
-    double* V = V0 + (start & 1u);
-    uint32_t* P = P0 + (start & 3u);
-    stage_cg<8>(K, sk + start, n, tid, kSThreads);
-    if (VALS) stage_cg<8>(V, sv + start, n, tid, kSThreads);
-    if (want_pos) stage_cg<4>(P, sp + start, n, tid, kSThreads);
+  bool have = next_leaf(L, k, &d);
+  uint32_t phase = 0;  // parity of the mbarrier's next wait
+  while (have) {
+    uint32_t k2 = k + gridDim.x;
+    LeafDesc d2;
+    const bool have2 = next_leaf(L, k2, &d2);
+    const bool used = leafs_issue<VALS>(L, d, smem, bar0, want_pos, tid);
     cp_async_commit();
-    if (tid == 0) {
-      s_min = ~0ull;
-      s_max = 0ull;
-      s_big = 0;
-      s_nlist = 0;
-    }
-    const int lg = n > 1 ? 32 - __clz((int)(n - 1)) : 0;  // ceil(log2 n)
-    const int tb = min(lg + 1, kSBucketBits);               // ~0.5 nonzero per bucket
-    for (uint32_t b = tid; b < (1u << kSBucketBits) / 2; b += kSThreads) B[b] = 0;
-    cp_async_wait<0>();
-    __syncthreads();
-    // keys of <= 32 remaining bits are used as they are (the MSD levels leave uniform
-    // keys spread over the whole range); wider ones relative to the leaf's minimum
-    uint64_t kmin = 0;
-    int rbits = L.rb;
-    if (L.rb > 32) {
-      uint64_t mn = ~0ull, mx = 0ull;
-      for (uint32_t i = tid; i < n; i += kSThreads) {
-        const uint64_t kk = leaf_key(L, K[i], mask);
-        mn = kk < mn ? kk : mn;
-        mx = kk > mx ? kk : mx;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, o);
-        const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, o);
-        mn = a < mn ? a : mn;
-        mx = b > mx ? b : mx;
-      }
-      if (lane == 0) {
-        atomicMin(&s_min, (unsigned long long)mn);
-        atomicMax(&s_max, (unsigned long long)mx);
-      }
-      __syncthreads();
-      kmin = s_min;
-      const uint64_t range = s_max - s_min;
-      rbits = range ? 64 - __clzll((long long)range) : 0;
-      if (rbits > 32) {  // key range too wide for 32-bit keys: the block kernel sorts it
+    const uint32_t n = d.n, start = d.start;
+    do {
+      if (n > (uint32_t)kSCap) {  // oversize (skewed) leaf: the block kernel streams it
         if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
-        k += gridDim.x;
-        __syncthreads();
-        continue;
+        break;
       }
-    }
-    const int bshift = rbits > tb ? rbits - tb : 0;
-    // bucket b's u16 count / start lives in half (b & 1) of word b >> 1 (no carries: every
-    // value is <= n <= kSCap)
-    for (uint32_t i = tid; i < n; i += kSThreads) {
-      const uint32_t rel = (uint32_t)(leaf_key(L, K[i], mask) - kmin);
-      R[i] = rel;
-      const uint32_t bk = rel >> bshift;
-      atomicAdd(&B[bk >> 1], 1u << ((bk & 1u) << 4));
-    }
-    __syncthreads();
-    {  // exclusive scan of the 4,096 packed counts: 16 per thread, then warps, then block
-      constexpr int PW = (1 << kSBucketBits) / 2 / kSThreads;  // words per thread
-      uint32_t c[2 * PW], tsum = 0;
-#pragma unroll
-      for (int i = 0; i < PW; ++i) {
-        const uint32_t w = B[tid * PW + i];
-        c[2 * i] = w & 0xFFFFu;
-        c[2 * i + 1] = w >> 16;
-        tsum += c[2 * i] + c[2 * i + 1];
+      const int lg = n > 1 ? 32 - __clz((int)(n - 1)) : 0;  // ceil(log2 n)
+      const int tb = min(lg + 1, kSBucketBits);               // ~0.5 nonzero per bucket
+      const int bshift = L.rb > tb ? L.rb - tb : 0;
+      for (uint32_t b = tid; b < (1u << kSBucketBits) / 2; b += NT) B[b] = 0;
+      if (tid == 0) {
+        s_big = 0;
+        s_nlist = 0;
       }
-      uint32_t incl = tsum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) s_warp[warp] = incl;
-      __syncthreads();
-      uint32_t run = incl - tsum;
-      for (int w = 0; w < warp; ++w) run += s_warp[w];
-#pragma unroll
-      for (int i = 0; i < PW; ++i) {
-        const uint32_t lo = run;
-        run += c[2 * i];
-        B[tid * PW + i] = lo | (run << 16);
-        run += c[2 * i + 1];
-      }
-    }
-    __syncthreads();
-    for (uint32_t i = tid; i < n; i += kSThreads) {
-      const uint32_t bk = R[i] >> bshift, sh = (bk & 1u) << 4;
-      X[(atomicAdd(&B[bk >> 1], 1u << sh) >> sh) & 0xFFFFu] = (uint16_t)i;
-    }
-    __syncthreads();
-    // B[b] is now the end of bucket b
-    auto bend16 = [&](uint32_t b) { return (B[b >> 1] >> ((b & 1u) << 4)) & 0xFFFFu; };
-    // Order inside a bucket: (q bits R, K', staging index).  K' orders equal q values by
-    // their suffix modes, i.e. their input order, so unordered MSD passes
-    // (unique keys) and stable ones give the same result; the index only breaks K' ties.
-    auto before = [&](uint16_t y, uint16_t x) {
-      const uint32_t ky = R[y], kx = R[x];
-      if (__builtin_expect(ky != kx, 1)) return ky < kx;
-      const uint64_t a = K[y], b = K[x];  // equal q bits: rare
-      return a < b || (a == b && y < x);
-    };
-    // Buckets holding 2..kSSmall records (about 8 % of the buckets of a uniform leaf) are
-    // listed -- each thread counts its 2*PW buckets, a warp scan and one shared atomic per
-    // warp place them -- and then insertion-sorted in place in X, one listed bucket per
-    // thread, so the lanes of a warp do alike work.  A larger bucket (skewed leaf)
-    // switches the whole leaf to the per-record rank below.  The list lives in F (u32
-    // entries lo | hi << 16; at most n / 2 <= kSCap / 2 of them).
-    {
-      constexpr int PW = (1 << kSBucketBits) / 2 / kSThreads;
-      uint32_t* list = reinterpret_cast<uint32_t*>(F);
-      uint32_t w[PW];
-#pragma unroll
-      for (int i = 0; i < PW; ++i) w[i] = B[tid * PW + i];
-      const uint32_t lo0 = tid ? bend16(tid * 2 * PW - 1) : 0u;
-      uint32_t m = 0;
-      bool crowded = false;
+      unsigned char* sb = smem;
+      SStage S;
       {
-        uint32_t lo = lo0;
-#pragma unroll
-        for (int i = 0; i < 2 * PW; ++i) {
-          const uint32_t hi = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xFFFFu);
-          m += (hi - lo >= 2u) ? 1u : 0u;
-          crowded |= hi - lo > (uint32_t)kSSmall;
-          lo = hi;
-        }
+        uint64_t* K0 = reinterpret_cast<uint64_t*>(sb);
+        double* V0 = reinterpret_cast<double*>(K0 + kSCap + 2);
+        uint32_t* P0 = reinterpret_cast<uint32_t*>(V0 + kSCap + 2);
+        const BulkPart<8> pk((d.src == 1 ? L.kA : L.kB) + start, n);
+        const BulkPart<8> pv((d.src == 1 ? L.vA : L.vB) + start, n);
+        const BulkPart<4> pp((d.src == 1 ? L.pA : L.pB) + start, n);
+        S.K = K0 + pk.off;
+        S.V = V0 + pv.off;
+        S.P = P0 + pp.off;
       }
-      uint32_t incl = m;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+      if (used) {
+        mbar_wait(bar0, phase);
+        phase ^= 1u;
       }
-      uint32_t wbase = 0;
-      if (lane == 31) wbase = atomicAdd(&s_nlist, incl);
-      wbase = __shfl_sync(0xffffffffu, wbase, 31);
-      if (m) {
-        uint32_t pos = wbase + incl - m, lo = lo0;
-#pragma unroll
-        for (int i = 0; i < 2 * PW; ++i) {
-          const uint32_t hi = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xFFFFu);
-          if (hi - lo >= 2u) list[pos++] = lo | (hi << 16);
-          lo = hi;
-        }
-      }
-      if (crowded) s_big = 2;
+      cp_async_wait<0>();  // head / tail elements
       __syncthreads();
-      if (!s_big) {
-        const uint32_t nl = s_nlist;
-        for (uint32_t e = tid; e < nl; e += kSThreads) {
-          const uint32_t lo = list[e] & 0xFFFFu, hi = list[e] >> 16;
-          for (uint32_t a = lo + 1; a < hi; ++a) {
-            const uint16_t x = X[a];
-            uint32_t j = a;
-            while (j > lo && !before(X[j - 1], x)) {
-              X[j] = X[j - 1];
-              --j;
+      const uint64_t* K = S.K;
+      for (uint32_t i = tid; i < n; i += NT) {
+        const uint32_t bk = (uint32_t)(leaf_key(L, K[i], mask) >> bshift);
+        Rb[i] = (uint16_t)bk;
+        atomicAdd(&B[bk >> 1], 1u << ((bk & 1u) << 4));
+      }
+      __syncthreads();
+      constexpr int PW = (1 << kSBucketBits) / 2 / NT;  // packed words per thread
+      {  // exclusive scan of the 4,096 packed counts
+        uint32_t c[2 * PW], tsum = 0;
+#pragma unroll
+        for (int i = 0; i < PW; ++i) {
+          const uint32_t w = B[tid * PW + i];
+          c[2 * i] = w & 0xFFFFu;
+          c[2 * i + 1] = w >> 16;
+          tsum += c[2 * i] + c[2 * i + 1];
+        }
+        uint32_t incl = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        uint32_t run = incl - tsum;
+#pragma unroll
+        for (int w = 0; w < W; ++w) run += w < warp ? s_warp[w] : 0u;
+#pragma unroll
+        for (int i = 0; i < PW; ++i) {
+          const uint32_t lo = run;
+          run += c[2 * i];
+          B[tid * PW + i] = lo | (run << 16);
+          run += c[2 * i + 1];
+        }
+      }
+      __syncthreads();
+      for (uint32_t i = tid; i < n; i += NT) {
+        const uint32_t bk = Rb[i], sh = (bk & 1u) << 4;
+        X[(atomicAdd(&B[bk >> 1], 1u << sh) >> sh) & 0xFFFFu] = (uint16_t)i;
+      }
+      __syncthreads();
+      // B[b] is now the end of bucket b
+      auto bend16 = [&](uint32_t b) { return (B[b >> 1] >> ((b & 1u) << 4)) & 0xFFFFu; };
+      auto before = [&](uint16_t y, uint16_t x) {
+        const uint64_t a = K[y], b = K[x];
+        return a < b || (a == b && y < x);
+      };
+      {  // buckets of 2..kSSmall records: listed, insertion-sorted one per thread 
+        uint32_t* list = reinterpret_cast<uint32_t*>(F);
+        uint32_t w[PW];
+#pragma unroll
+        for (int i = 0; i < PW; ++i) w[i] = B[tid * PW + i];
+        const uint32_t lo0 = tid ? bend16(tid * 2 * PW - 1) : 0u;
+        uint32_t m = 0;
+        bool crowded = false;
+        {
+          uint32_t lo = lo0;
+#pragma unroll
+          for (int i = 0; i < 2 * PW; ++i) {
+            const uint32_t hi = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xFFFFu);
+            m += (hi - lo >= 2u) ? 1u : 0u;
+            crowded |= hi - lo > (uint32_t)kSSmall;
+            lo = hi;
+          }
+        }
+        uint32_t incl = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        uint32_t wbase = 0;
+        if (lane == 31) wbase = atomicAdd(&s_nlist, incl);
+        wbase = __shfl_sync(0xffffffffu, wbase, 31);
+        if (m) {
+          uint32_t pos = wbase + incl - m, lo = lo0;
+#pragma unroll
+          for (int i = 0; i < 2 * PW; ++i) {
+            const uint32_t hi = (i & 1) ? (w[i >> 1] >> 16) : (w[i >> 1] & 0xFFFFu);
+            if (hi - lo >= 2u) list[pos++] = lo | (hi << 16);
+            lo = hi;
+          }
+        }
+        if (crowded) s_big = 2;
+        __syncthreads();
+        if (!s_big) {
+          const uint32_t nl = s_nlist;
+          for (uint32_t e = tid; e < nl; e += NT) {
+            const uint32_t lo = list[e] & 0xFFFFu, hi = list[e] >> 16;
+            for (uint32_t a = lo + 1; a < hi; ++a) {
+              const uint16_t x = X[a];
+              uint32_t j = a;
+              while (j > lo && !before(X[j - 1], x)) {
+                X[j] = X[j - 1];
+                --j;
+              }
+              X[j] = x;
             }
-            X[j] = x;
           }
         }
       }
-    }
-    __syncthreads();
-    const uint16_t* order = X;
-    if (s_big) {  // a crowded bucket: rank every record by counting inside its bucket
-      bool big = false;
-      for (uint32_t p = tid; p < n; p += kSThreads) {
-        const uint16_t x = X[p];
-        const uint32_t b = R[x] >> bshift;
-        const uint32_t lo = b ? bend16(b - 1) : 0u, hi = bend16(b);
-        if (hi - lo > (uint32_t)kCBig) {
-          big = true;
-          continue;
+      __syncthreads();
+      const uint16_t* order = X;
+      if (s_big) {  // a crowded bucket: rank every record by counting inside its bucket
+        bool big = false;
+        for (uint32_t p = tid; p < n; p += NT) {
+          const uint16_t x = X[p];
+          const uint32_t b = Rb[x];
+          const uint32_t lo = b ? bend16(b - 1) : 0u, hi = bend16(b);
+          if (hi - lo > (uint32_t)kCBig) {
+            big = true;
+            continue;
+          }
+          uint32_t rk = lo;
+          for (uint32_t j = lo; j < hi; ++j) rk += before(X[j], x) ? 1u : 0u;
+          F[rk] = x;
         }
-        uint32_t rk = lo;
-        for (uint32_t j = lo; j < hi; ++j) rk += before(X[j], x) ? 1u : 0u;
-        F[rk] = x;
-      }
-      __syncthreads();
-      if (tid == 0) s_big = 0;
-      __syncthreads();
-      if (big) s_big = 1;
-      __syncthreads();
-      if (s_big) {  // skewed leaf: the block-level kernel sorts it
-        if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
-        k += gridDim.x;
         __syncthreads();
-        continue;
+        if (tid == 0) s_big = 0;
+        __syncthreads();
+        if (big) s_big = 1;
+        __syncthreads();
+        if (s_big) {  // skewed leaf: the block-level kernel sorts it
+          if (tid == 0) L.defer[atomicAdd(L.ndefer, 1u)] = defer_entry(L, k);
+          break;
+        }
+        order = F;
       }
-      order = F;
-    }
-    for (uint32_t j = tid; j < n; j += kSThreads) {
-      const uint16_t e = order[j];
-      const uint64_t g = (uint64_t)start + j;
-      L.keys_out[g] = K[e];
-      if (VALS) L.vals_out[g] = V[e];
-      if (want_pos) {
-        const uint32_t pos = P[e];
-        L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pos) : pos;
+      for (uint32_t j = tid; j < n; j += NT) {
+        const uint16_t e = order[j];
+        const uint64_t g = (uint64_t)start + j;
+        L.keys_out[g] = K[e];
+        if (VALS) L.vals_out[g] = S.V[e];
+        if (want_pos) {
+          const uint32_t pos = S.P[e];
+          L.perm_out[g] = L.idx_in ? __ldg(L.idx_in + pos) : pos;
+        }
       }
-    }
-    __syncthreads();  // shared arrays are reused by the next leaf
-    k += gridDim.x;
+    } while (false);
+    __syncthreads();  // the stage and the sort arrays are reused
+    k = k2;
+    d = d2;
+    have = have2;
   }
 }
-
 
 // ---------------------------------------------------------------------------------
 // Launchers
@@ -1605,7 +1621,7 @@ static cudaError_t launch_leafw(const LeafArgs& L, cudaStream_t s) {
 
 uint32_t leaf_cap() { return kCCap; }
 uint32_t cta_leaf_cap() { return kCCap; }
-uint32_t staged_leaf_target() { return kSCap * 27 / 32; }  // ~1.94K: ~8 sigma below the cap
+uint32_t staged_leaf_target() { return 1944; }  // ~7 sigma below the cap (kSCap)
 
 template <bool VALS, bool BIG, int CAP = kCCap>
 static cudaError_t launch_leafc_t(const LeafArgs& L, uint32_t grid_cap, cudaStream_t s) {
