@@ -1348,11 +1348,17 @@ struct SStage {  // a staged leaf's arrays (at their congruent offsets)
 };
 
 // Issue the copies of leaf d into the stage at st (CTA-wide call; thread 0 issues the bulk
-// copies after a proxy fence).  Returns whether the mbarrier expects bytes.
+// copies after a proxy fence): the keys on barK (needed first), V and the positions on
+// barVP (needed only by the write loop).  Head / tail elements: cp.async group 1 keys,
+// group 2 the rest.  Returns bit 0 / 1: barK / barVP expects bytes.
 template <bool VALS>
-__device__ __forceinline__ bool leafs_issue(const LeafArgs& L, const LeafDesc& d, unsigned char* st,
-                                            uint32_t bar, bool want_pos, int tid) {
-  if (d.n > (uint32_t)kSCap) return false;
+__device__ __forceinline__ uint32_t leafs_issue(const LeafArgs& L, const LeafDesc& d, unsigned char* st,
+                                                uint32_t barK, uint32_t barVP, bool want_pos, int tid) {
+  if (d.n > (uint32_t)kSCap) {
+    cp_async_commit();
+    cp_async_commit();
+    return 0u;
+  }
   const uint64_t* gk = (d.src == 1 ? L.kA : L.kB) + d.start;
   const double* gv = (d.src == 1 ? L.vA : L.vB) + d.start;
   const uint32_t* gp = (d.src == 1 ? L.pA : L.pB) + d.start;
@@ -1361,21 +1367,28 @@ __device__ __forceinline__ bool leafs_issue(const LeafArgs& L, const LeafDesc& d
   uint32_t* P0 = reinterpret_cast<uint32_t*>(V0 + kSCap + 2);
   const BulkPart<8> pk(gk, d.n), pv(gv, d.n);
   const BulkPart<4> pp(gp, d.n);
-  const uint32_t bytes = pk.body_bytes() + (VALS ? pv.body_bytes() : 0u) + (want_pos ? pp.body_bytes() : 0u);
-  if (tid == 0 && bytes) {
+  const uint32_t kb = pk.body_bytes(), vb = VALS ? pv.body_bytes() : 0u, pb = want_pos ? pp.body_bytes() : 0u;
+  if (tid == 0) {
     fence_proxy_async();
-    mbar_expect_tx(bar, bytes);
-    if (pk.body_bytes()) bulk_g2s(smem_addr16(K0 + pk.off + pk.h), gk + pk.h, pk.body_bytes(), bar);
-    if (VALS && pv.body_bytes()) bulk_g2s(smem_addr16(V0 + pv.off + pv.h), gv + pv.h, pv.body_bytes(), bar);
-    if (want_pos && pp.body_bytes()) bulk_g2s(smem_addr16(P0 + pp.off + pp.h), gp + pp.h, pp.body_bytes(), bar);
+    if (kb) {
+      mbar_expect_tx(barK, kb);
+      bulk_g2s(smem_addr16(K0 + pk.off + pk.h), gk + pk.h, kb, barK);
+    }
+    if (vb + pb) {
+      mbar_expect_tx(barVP, vb + pb);
+      if (vb) bulk_g2s(smem_addr16(V0 + pv.off + pv.h), gv + pv.h, vb, barVP);
+      if (pb) bulk_g2s(smem_addr16(P0 + pp.off + pp.h), gp + pp.h, pb, barVP);
+    }
   }
   // head / tail elements: at most 1 + 1, 1 + 1 and 3 + 3 (one per thread)
   const uint32_t ek = pk.edge(d.n), ev = VALS ? pv.edge(d.n) : 0u, ep = want_pos ? pp.edge(d.n) : 0u;
   const uint32_t i = (uint32_t)tid;
   if (i < ek) pk.copy_edge(i, K0, gk);
-  else if (i < ek + ev) pv.copy_edge(i - ek, V0, gv);
-  else if (i < ek + ev + ep) pp.copy_edge(i - ek - ev, P0, gp);
-  return bytes != 0;
+  cp_async_commit();
+  if (i >= ek && i < ek + ev) pv.copy_edge(i - ek, V0, gv);
+  else if (i >= ek + ev && i < ek + ev + ep) pp.copy_edge(i - ek - ev, P0, gp);
+  cp_async_commit();
+  return (kb ? 1u : 0u) | (vb + pb ? 2u : 0u);
 }
 
 template <bool VALS>
@@ -1385,7 +1398,7 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
   uint16_t* X = Rb + kSCap;                                         // [cap] bucket order
   uint16_t* F = X + kSCap;                                          // [cap] final order / list
   uint32_t* B = reinterpret_cast<uint32_t*>(F + kSCap);             // [2^11] packed u16 buckets
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bars[2];
   __shared__ uint32_t s_warp[32];
   __shared__ int s_big;
   __shared__ uint32_t s_nlist;
@@ -1393,22 +1406,22 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool want_pos = L.perm_out != nullptr;
   const uint64_t mask = L.rb >= 64 ? ~0ull : ((1ull << L.rb) - 1ull);
-  const uint32_t bar0 = smem_addr16(&bar);
+  const uint32_t barK = smem_addr16(&bars[0]), barVP = barK + 8;
   if (tid == 0) {
-    mbar_init(bar0, 1);
+    mbar_init(barK, 1);
+    mbar_init(barVP, 1);
     fence_mbar_init();
   }
   __syncthreads();
   uint32_t k = blockIdx.x;
   LeafDesc d;
   bool have = next_leaf(L, k, &d);
-  uint32_t phase = 0;  // parity of the mbarrier's next wait
+  uint32_t phase = 0;  // bit 0 / 1: parity of the next wait on barK / barVP
   while (have) {
     uint32_t k2 = k + gridDim.x;
     LeafDesc d2;
     const bool have2 = next_leaf(L, k2, &d2);
-    const bool used = leafs_issue<VALS>(L, d, smem, bar0, want_pos, tid);
-    cp_async_commit();
+    uint32_t used = leafs_issue<VALS>(L, d, smem, barK, barVP, want_pos, tid);
     const uint32_t n = d.n, start = d.start;
     do {
       if (n > (uint32_t)kSCap) {  // oversize (skewed) leaf: the block kernel streams it
@@ -1436,11 +1449,11 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
         S.V = V0 + pv.off;
         S.P = P0 + pp.off;
       }
-      if (used) {
-        mbar_wait(bar0, phase);
+      if (used & 1u) {
+        mbar_wait(barK, phase & 1u);
         phase ^= 1u;
       }
-      cp_async_wait<0>();  // head / tail elements
+      cp_async_wait<1>();  // the keys' head / tail elements
       __syncthreads();
       const uint64_t* K = S.K;
       for (uint32_t i = tid; i < n; i += NT) {
@@ -1571,6 +1584,13 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
         }
         order = F;
       }
+      if (used & 2u) {  // V and the positions (in flight during the sort)
+        mbar_wait(barVP, (phase >> 1) & 1u);
+        phase ^= 2u;
+        used &= ~2u;
+      }
+      cp_async_wait<0>();
+      __syncthreads();
       for (uint32_t j = tid; j < n; j += NT) {
         const uint16_t e = order[j];
         const uint64_t g = (uint64_t)start + j;
@@ -1582,6 +1602,11 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
         }
       }
     } while (false);
+    if (used & 2u) {  // a deferred leaf: its V / P copies land before the stage is reused
+      mbar_wait(barVP, (phase >> 1) & 1u);
+      phase ^= 2u;
+    }
+    cp_async_wait<0>();
     __syncthreads();  // the stage and the sort arrays are reused
     k = k2;
     d = d2;
