@@ -79,6 +79,32 @@ __global__ void __launch_bounds__(256, 2) k_pattern(uint64_t N, int per, const u
   }
 }
 
+// Same pattern with (K', V) interleaved as one 16-byte record per slot (one STG.128) and
+// the position in its own array: the record layout an interleaved intermediate would use.
+__global__ void __launch_bounds__(256, 2) k_pattern_kv(uint64_t N, int per, const uint64_t* __restrict__ k,
+                                                       const double* __restrict__ v, uint4* __restrict__ kvo,
+                                                       uint32_t* __restrict__ po, uint64_t nb) {
+  const uint64_t tile = blockIdx.x;
+  const uint64_t base = tile * TILE;
+  uint64_t acc = 0;
+  double vacc = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    acc += __ldcs(k + base + r * 256 + threadIdx.x);
+    vacc += __ldcs(v + base + r * 256 + threadIdx.x);
+  }
+  const uint64_t stride = N / nb;
+  const uint64_t vb = (uint64_t)__double_as_longlong(vacc);
+#pragma unroll 4
+  for (int p = threadIdx.x; p < TILE; p += 256) {
+    const uint64_t bk = (uint64_t)(p / per) % nb;
+    const uint64_t d = bk * stride + (tile * per + p % per) % stride;
+    const uint64_t a = acc + p, b = vb + p;
+    kvo[d] = make_uint4((uint32_t)a, (uint32_t)(a >> 32), (uint32_t)b, (uint32_t)(b >> 32));
+    po[d] = (uint32_t)a;
+  }
+}
+
 int main() {
   const uint64_t N = 256ull << 20;  // 256 Mi records: 4 GiB in, 4 GiB out
   uint64_t *k, *ko;
@@ -109,10 +135,13 @@ int main() {
   time("copy", 0, [&] { k_copy<<<148 * 8, 512>>>(N, k, v, ko, vo); });
   uint32_t* po;
   cudaMalloc(&po, N * 4 + (64ull << 20));
+  uint4* kvo;
+  cudaMalloc(&kvo, N * 16 + (64ull << 20));
   for (int per : {64, 16, 13, 8, 4}) {
     const uint64_t nb = TILE / per;
     time(per == 13 ? "2arr r13" : "2arr", per, [&] { k_pattern<false><<<N / TILE, 256>>>(N, per, k, v, ko, vo, po, nb); });
     time(per == 13 ? "3arr r13" : "3arr", per, [&] { k_pattern<true><<<N / TILE, 256>>>(N, per, k, v, ko, vo, po, nb); });
+    time(per == 13 ? "kv+p r13" : "kv+p", per, [&] { k_pattern_kv<<<N / TILE, 256>>>(N, per, k, v, kvo, po, nb); });
   }
   return 0;
 }
