@@ -2031,6 +2031,9 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess)
       return e;
     PassParams a2 = a;
+    // L2 prefetch half a wave ahead (one 8K-tile CTA per SM): C5 level 2 5.66 -> 5.49 ms
+    // (a wave: 5.66, none: 5.71, 3/4: 5.60, 1/4: 5.50)
+    a2.pf_dist = prefetch_distance() / 2;
     a2.pass = 1;
     a2.ttab = ttab;
     a2.ntiles = ntiles;
