@@ -342,6 +342,14 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
       prefetch_l2(io.toff + (size_t)t2 * BINS, (size_t)BINS * 4);
     }
   }
+  // global offsets of this tile's digit runs (from the exclusive scan): issued first, so
+  // their latency hides behind the tile's loads (C5 level 2: 7.7 % of stall samples)
+  uint32_t tv[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int d = tid + b * NT;
+    tv[b] = (d < BINS && !a.single) ? __ldcs(io.toff + (size_t)t * BINS + d) : 0u;
+  }
   // UNST digit counters: their own array when V is staged early, else inside sV
   uint32_t* cnt = EARLY ? ucnt : reinterpret_cast<uint32_t*>(whist);
   if (UNST) {
@@ -387,11 +395,11 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
     }
     cp_async_commit();
   }
-  // global offsets of this tile's digit runs (from the exclusive scan)
+  // global offsets of this tile's digit runs (loaded at the top of the tile)
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int d = tid + b * NT;
-    if (d < BINS) gbase[d] = a.single ? 0u : __ldcs(io.toff + (size_t)t * BINS + d);
+    if (d < BINS) gbase[d] = tv[b];
   }
   {
     const DigitFn dg(a);
