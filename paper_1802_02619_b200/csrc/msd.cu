@@ -1417,17 +1417,28 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
   LeafDesc d;
   bool have = next_leaf(L, k, &d);
   uint32_t phase = 0;  // bit 0 / 1: parity of the next wait on barK / barVP
+  // the next leaf's descriptor: found by one thread (its table loads stay off the other
+  // threads' path), handed over in shared memory (two slots: iteration parity)
+  __shared__ LeafDesc s_d2[2];
+  __shared__ uint32_t s_k2[2];
+  __shared__ int s_have2[2];
+  uint32_t it = 0;
   while (have) {
-    uint32_t k2 = k + gridDim.x;
-    LeafDesc d2;
-    const bool have2 = next_leaf(L, k2, &d2);
     uint32_t used = leafs_issue<VALS>(L, d, smem, barK, barVP, want_pos, tid);
-    if (tid == 32 && have2 && d2.n <= (uint32_t)kSCap) {
-      // the next leaf of this CTA into L2 now: its bulk copies then see L2, not HBM,
-      // latency (C5 leaves 4.89 -> 4.75 ms; two leaves ahead: 4.97)
-      prefetch_l2((d2.src == 1 ? L.kA : L.kB) + d2.start, (size_t)d2.n * 8);
-      if (VALS) prefetch_l2((d2.src == 1 ? L.vA : L.vB) + d2.start, (size_t)d2.n * 8);
-      if (want_pos) prefetch_l2((d2.src == 1 ? L.pA : L.pB) + d2.start, (size_t)d2.n * 4);
+    if (tid == 32) {
+      uint32_t k2 = k + gridDim.x;
+      LeafDesc d2;
+      const bool have2 = next_leaf(L, k2, &d2);
+      if (have2 && d2.n <= (uint32_t)kSCap) {
+        // the next leaf of this CTA into L2 now: its bulk copies then see L2, not HBM,
+        // latency (C5 leaves 4.89 -> 4.75 ms; two leaves ahead: 4.97)
+        prefetch_l2((d2.src == 1 ? L.kA : L.kB) + d2.start, (size_t)d2.n * 8);
+        if (VALS) prefetch_l2((d2.src == 1 ? L.vA : L.vB) + d2.start, (size_t)d2.n * 8);
+        if (want_pos) prefetch_l2((d2.src == 1 ? L.pA : L.pB) + d2.start, (size_t)d2.n * 4);
+      }
+      s_d2[it & 1u] = d2;
+      s_k2[it & 1u] = k2;
+      s_have2[it & 1u] = have2 ? 1 : 0;
     }
     const uint32_t n = d.n, start = d.start;
     do {
@@ -1615,9 +1626,10 @@ __global__ void __launch_bounds__(kSThreads, 3) k_leafs(const __grid_constant__ 
     }
     cp_async_wait<0>();
     __syncthreads();  // the stage and the sort arrays are reused
-    k = k2;
-    d = d2;
-    have = have2;
+    k = s_k2[it & 1u];
+    d = s_d2[it & 1u];
+    have = s_have2[it & 1u] != 0;
+    ++it;
   }
 }
 
