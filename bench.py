@@ -428,7 +428,8 @@ def run_single(args):
         "markers": names,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": info["launches"] * args.steps,
+        # one profiling marker per kernel launch of the call (lco_profile), times steps
+        "gpu_launches": (len(names) if names else info["launches"]) * args.steps,
         "clocks": clk,
         "wall_s_timed": wall,
         "gen_s": gen_s,

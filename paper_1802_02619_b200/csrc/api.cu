@@ -70,6 +70,8 @@ Tuning read_tuning() {
   t.leafs_force = flag("LCO_LEAFS");
   t.no_leafs = flag("LCO_NO_LEAFS");
   t.no_leafr = flag("LCO_NO_LEAFR");
+  t.no_sampled = flag("LCO_NO_SAMPLED");
+  t.sampled_test = flag("LCO_SAMPLED_TEST");
   t.no_match = flag("LCO_NO_MATCH");
   t.lsd_maxbits = num("LCO_LSD_MAXBITS", 1, 11, 0);
   t.stable_msd = flag("LCO_STABLE_MSD");
@@ -197,6 +199,8 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz, const Tuning& tu) {
     mcost = 8 + 36 + 8 + 40 + 40;
   }
   if (tu.leafs_force) m.staged = 1;
+  // sampled level 1 for large two-level plans with an 8-bit first digit (set below, once
+  // b1 is final): C5 saves the 0.66 ms count pass
   // schedule overrides for tests and A/B measurements (the defaults above otherwise),
   // kept inside the key: b1 + b2 < B
   if (tu.msd_b1) m.b1 = tu.msd_b1 < B - 1 ? tu.msd_b1 : B - 1;
@@ -204,6 +208,8 @@ CallPlan choose_plan(const OpPlan& op, uint64_t nnz, const Tuning& tu) {
   if (m.levels == 2 && m.b2 < 1) m.levels = 1, m.b2 = 0;
   if (tu.msd_cta >= 0) m.cta = tu.msd_cta;
   m.rb = B - m.b1 - m.b2;
+  m.sampled = m.levels == 2 && m.b1 == 8 && nnz >= (1ull << 24) && !tu.no_sampled &&
+              sampled_capacity(nnz) < (1ull << 32);
   // MSD leaves are sized for uniformly spread keys; structured keys (stencil operators,
   // identity-prefix segments) make them uneven, so MSD is taken only without a prefix
   // and with a clear modelled win.
@@ -242,12 +248,13 @@ WsLayout layout_for(const CallPlan& c, uint64_t nnz) {
                                                : tile_ctrl_bytes(nnz, c.segments))));
     // the tile path needs both buffers only as scratch of the rare streaming fallback
     if (msd || tile || c.passes >= 2) {
+      const uint64_t na = msd && c.msd.sampled ? sampled_capacity(nnz) : nnz;
       w.kA = off;
-      off += align_up(nnz * 8);
+      off += align_up(na * 8);
       w.vA = off;
-      off += align_up(nnz * 8);
+      off += align_up(na * 8);
       w.pA = off;
-      off += align_up(nnz * 4);
+      off += align_up(na * 4);
     }
     if (msd || tile || c.passes >= 3) {
       w.kB = off;
@@ -1049,6 +1056,9 @@ lco_status lco_plan_query(lco_handle h, uint64_t nnz, int sort, lco_plan_info* i
     else if (cp.path == kPathBlock) launches = 5; // bounds, counts, 2 scan, tiles
     else if (cp.path == kPathOnesweep) launches = 4 * cp.passes;
     else launches = 4 + (cp.msd.levels == 2 ? 5 : 0) + 2;  // passes, leaves, deferred
+    // (a sampled level 1 adds sample, caps, the cursor scatter and the finish; level 3
+    // and the deferred drains add up to 8 more, most of them empty)
+    if (cp.path == kPathMsd && cp.msd.sampled) launches += 4;
   }
   info->launches = launches;
   return LCO_OK;

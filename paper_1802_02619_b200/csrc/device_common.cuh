@@ -143,6 +143,14 @@ struct PassParams {
   uint32_t tile;  // records per tile of unsegmented passes (0: kTile)
   int persist;    // persistent grid: each CTA loops over tiles (tile table length on device)
   int single;     // the whole input is one tile: its sorted order is the output order
+  // sampled level 1 (msd.cu): the unordered first pass takes each tile's run bases from
+  // per-digit cursors into capacity-padded buckets (no count / scan / offsets kernels);
+  // a tile whose run would pass its bucket's end writes nothing and raises *overflow
+  uint32_t* cursor;
+  const uint32_t* cap_end;
+  uint32_t* overflow;
+  // the exact fallback of a sampled level 1: its kernels return at once unless *run_if
+  const uint32_t* run_if;
 };
 
 // PER consecutive uint16 tile-histogram entries in, PER uint32 offsets out (vector

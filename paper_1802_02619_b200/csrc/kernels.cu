@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
                                                     uint32_t* __restrict__ csum) {
   constexpr int BINS = 1 << RB;
   __shared__ uint32_t h[BINS];
+  if (a.run_if && *a.run_if == 0u) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // one tile per CTA, or (a.persist: tile tables whose length only the device knows)
   // tiles blockIdx.x, + gridDim.x, ... of a persistent grid
@@ -151,8 +152,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ cs
                                                        uint32_t* __restrict__ bucket,
                                                        uint32_t* __restrict__ done,
                                                        uint64_t* __restrict__ counts64,
-                                                       int ncounts) {
+                                                       int ncounts, const uint32_t* run_if) {
   constexpr int BINS = 1 << RB;
+  if (run_if && *run_if == 0u) return;
   constexpr int LANES = BINS >= 32 ? 32 : BINS;  // bins per CTA (one warp-wide row)
   constexpr int SPLIT = kScanThreads / LANES;    // chunk groups per bin
   __shared__ uint32_t part[kScanThreads];
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(kThreads) k_offsets(const __grid_constant__ Pa
                                                       const uint32_t* __restrict__ csum,
                                                       const uint32_t* __restrict__ bucket,
                                                       uint32_t* __restrict__ toff) {
+  if (a.run_if && *a.run_if == 0u) return;
   constexpr int BINS = 1 << RB;
   constexpr int PER = BINS / kThreads;
   static_assert(PER == 1 || PER == 4 || PER == 8, "digit widths 8, 10, 11");
@@ -304,6 +307,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   uint16_t* sdig = sidx + (EARLY ? TILE : 0);                     // [TILE]
   const bool kdig = !FIRST && scatter_keydig(a) && !io.direct && !io.keep_old_key;
   __shared__ uint32_t s_warp[32];
+  __shared__ int s_ovf;
+  if (a.run_if && *a.run_if == 0u) return;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // one tile per CTA, or (a.persist) tiles blockIdx.x, + gridDim.x, ... of a persistent grid
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
       prefetch_l2((FIRST ? io.keys_in : io.kin) + b2, (size_t)m * 8);
       if (VALS) prefetch_l2((FIRST ? io.vals_in : io.vin) + b2, (size_t)m * 8);
       if (!FIRST && io.pout) prefetch_l2(io.pin + b2, (size_t)m * 4);
-      prefetch_l2(io.toff + (size_t)t2 * BINS, (size_t)BINS * 4);
+      if (io.toff) prefetch_l2(io.toff + (size_t)t2 * BINS, (size_t)BINS * 4);
     }
   }
   // global offsets of this tile's digit runs (from the exclusive scan): issued first, so
@@ -348,8 +353,9 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
     const int d = tid + b * NT;
-    tv[b] = (d < BINS && !a.single) ? __ldcs(io.toff + (size_t)t * BINS + d) : 0u;
+    tv[b] = (d < BINS && !a.single && !a.cursor) ? __ldcs(io.toff + (size_t)t * BINS + d) : 0u;
   }
+  if (FIRST && UNST && tid == 0) s_ovf = 0;
   // UNST digit counters: their own array when V is staged early, else inside sV
   uint32_t* cnt = EARLY ? ucnt : reinterpret_cast<uint32_t*>(whist);
   if (UNST) {
@@ -454,6 +460,21 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
     }
     __syncthreads();
     block_scan_bins<NT, BINS>(cnt, loff, s_warp);
+    if (FIRST && a.cursor) {  // sampled level 1: this tile's run of digit d from its cursor
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int d = tid + b * NT;
+        if (d < BINS) {
+          const uint32_t c = cnt[d];
+          uint32_t g0 = 0;
+          if (c) {
+            g0 = atomicAdd(a.cursor + d, c);
+            if (g0 + c > a.cap_end[d] || g0 + c < g0) s_ovf = 1;
+          }
+          gbase[d] = g0;
+        }
+      }
+    }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const uint32_t d = meta[it] & 0xFFFFu;
@@ -566,6 +587,10 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
   }
   cp_async_wait<0>();
   __syncthreads();
+  if (FIRST && UNST && a.cursor && s_ovf) {  // a bucket overflowed: the exact path redoes it
+    if (tid == 0) atomicOr(a.overflow, 1u);
+    return;
+  }
   // ---- one write loop: K', V, position of each slot ----
   const bool remap = !FIRST && LAST && io.idx_in != nullptr;
   if (io.direct) {  // partition: the scatter IS the exchange (stores to peer memory)
@@ -686,8 +711,9 @@ PassCtrl pass_ctrl_layout(int rb, uint64_t nnz, uint32_t* ctrl, uint32_t tile) {
 template <int RB, int ITEMS>
 static cudaError_t launch_count_t(bool first, const PassParams& a, const uint64_t* keys,
                                   uint16_t* thist, uint32_t* csum, uint32_t grid, cudaStream_t s) {
-  if (a.persist) {  // table-driven later passes only (MSD level 3)
-    k_count<RB, false, false, ITEMS, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+  if (a.persist) {  // table-driven later passes (MSD level 3), sampled level 1's fallback
+    if (first) k_count<RB, true, false, ITEMS, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
+    else k_count<RB, false, false, ITEMS, true><<<grid, kThreads, 0, s>>>(a, keys, thist, csum);
     return cudaGetLastError();
   }
   if (a.distinct) {
@@ -846,8 +872,17 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
     return e;  // chunk sums, totals, bucket starts, k_scan's completion counter, distinct
   if (a0.adapt) a.distinct = c.done + 1;  // LSD passes (run_passes) only
   const uint64_t* in_keys = first ? io.keys_in : ((j % 2 == 1) ? io.kA : io.kB);
+  // a persistent pass (the predicated fallback of a sampled level 1, usually a no-op):
+  // grids of a few CTAs per SM loop over the tiles
+  uint32_t gcount = c.tiles, gscat = c.tiles;
+  if (a.persist) {
+    int sms = 148;
+    if ((e = device_sms(&sms)) != cudaSuccess) return e;
+    gcount = c.tiles < (uint32_t)sms * 8u ? c.tiles : (uint32_t)sms * 8u;
+    gscat = c.tiles < (uint32_t)sms * 2u ? c.tiles : (uint32_t)sms * 2u;
+  }
   if (L.mark) L.mark(L.ctx, first ? "k_count_first" : "k_count");
-  if ((e = launch_count(rb, first, a, in_keys, c.thist, c.csum, c.tiles, L.stream)) != cudaSuccess)
+  if ((e = launch_count(rb, first, a, in_keys, c.thist, c.csum, gcount, L.stream)) != cudaSuccess)
     return e;
   if (L.mark) L.mark(L.ctx, "k_scan");
   const int scan_grid = BINS >= 32 ? BINS / 32 : 1;
@@ -855,17 +890,17 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
     case 8:
       k_scan<8><<<scan_grid, kScanThreads, 0, L.stream>>>(c.csum, c.nchunks, c.totals, c.bucket,
                                                           c.done, part ? io.counts64 : nullptr,
-                                                          io.world);
+                                                          io.world, a.run_if);
       break;
     case 10:
       k_scan<10><<<scan_grid, kScanThreads, 0, L.stream>>>(c.csum, c.nchunks, c.totals, c.bucket,
                                                            c.done, part ? io.counts64 : nullptr,
-                                                           io.world);
+                                                           io.world, a.run_if);
       break;
     case 11:
       k_scan<11><<<scan_grid, kScanThreads, 0, L.stream>>>(c.csum, c.nchunks, c.totals, c.bucket,
                                                            c.done, part ? io.counts64 : nullptr,
-                                                           io.world);
+                                                           io.world, a.run_if);
       break;
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -893,7 +928,7 @@ cudaError_t run_pass(int rb, const PassParams& a0, const PassIO& io, int j, bool
                        : (first && last ? "k_scatter_single"
                                         : (first ? "k_scatter_first"
                                                  : (last ? "k_scatter_last" : "k_scatter_mid"))));
-  return launch_scatter(rb, first, last, io.vals_out != nullptr, a, s, c.tiles, L.stream);
+  return launch_scatter(rb, first, last, io.vals_out != nullptr, a, s, gscat, L.stream);
 }
 
 // Stable LSD radix sort over all passes of the key plan (or one partition pass).

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
+
 #include "lco_internal.h"
 
 namespace lco {
@@ -78,7 +80,17 @@ struct MsdPlan {
   int rb;
   int cta;     // leaves sorted by one CTA per leaf instead of k_leafw (one warp)
   int staged;  // CTA leaves of <= ~2K nonzeros: the fully staged k_leafs
+  int sampled; // level 1 from sampled capacities (buffer A padded: sampled_capacity)
 };
+// Buffer A's length (records) for a sampled level 1: a bound on the padded capacities'
+// sum (k_caps: est_d + 6 sqrt(256 est_d) + 4,096 over 256 digits, sum est_d <= nnz + 256;
+// Cauchy-Schwarz: sum sqrt(est_d) <= 16 sqrt(nnz + 256)).
+inline uint64_t sampled_capacity(uint64_t nnz) {
+  uint64_t r = (uint64_t)std::sqrt((double)(nnz + 256));
+  while (r * r < nnz + 256) ++r;  // ceil(sqrt(nnz + 256))
+  return nnz + 256 + 1536 * r + 256 * 4096 + 4096;
+}
+constexpr size_t kSampledCtrlBytes = 5 * 1024;
 
 struct PassParams;
 struct ScatterIO;

@@ -241,6 +241,8 @@ struct Tuning {
   int leafs_force;  // LCO_LEAFS: fully staged CTA leaves whenever they fit
   int no_leafs;     // LCO_NO_LEAFS
   int no_leafr;     // LCO_NO_LEAFR
+  int no_sampled;   // LCO_NO_SAMPLED: level 1 of the MSD schedule counted exactly
+  int sampled_test; // LCO_SAMPLED_TEST: sampled capacities halved (forces the exact fallback)
   int no_match;     // LCO_NO_MATCH: LSD passes never rank with match.any
   int lsd_maxbits;  // LCO_LSD_MAXBITS (0: default), clamped to 1..11
   int stable_msd;   // LCO_STABLE_MSD: MSD passes of lco_permute ranked stably

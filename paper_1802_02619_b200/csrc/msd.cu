@@ -45,6 +45,118 @@ __host__ __device__ __forceinline__ uint32_t leaf_entry(int level, uint32_t slot
 }
 
 // ---------------------------------------------------------------------------------
+// Sampled level 1 (lco_permute, two unordered MSD levels, 8-bit first digit, large
+// inputs): the first pass needs each tile's run bases, which an exact count pass (one
+// full read of the keys, C5 0.66 ms, plus scan and offsets) provides.  Instead:
+//   k_sample1  the level-1 digit histogram of one key in every kSampleStride (at a
+//              hashed offset inside each stride: no aliasing with periodic structure);
+//   k_caps     per digit a padded capacity (estimate + 6 sd + 4,096) and its start in
+//              buffer A (exclusive scan), the cursors, and the overflow flag if the
+//              capacities exceed the buffer;
+//   first pass one atomicAdd per (tile, digit) on the digit's cursor (k_scatter cursor
+//              mode); a run that would pass its bucket's end makes its tile write
+//              nothing and raise the flag;
+//   exact path count / scan / offsets / scatter predicated on the flag (return at once
+//              when it is clear), rewriting A exactly;
+//   k_fin1     bucket sizes and exact output starts from the cursors (flag clear), or
+//              the exact path's starts as the read bases (flag set).
+// Buckets then hold gaps in A, so every level-1 bucket goes through level 2 (whose
+// tiles read A at the padded starts and write B at the exact ones); B and the outputs
+// stay exact.
+// ---------------------------------------------------------------------------------
+constexpr uint32_t kSampleStride = 256;  // launch.h sampled_capacity assumes it
+
+__device__ __forceinline__ uint32_t sample_mix(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  return (uint32_t)x;
+}
+
+template <int RB>
+__global__ void __launch_bounds__(256) k_sample1(const __grid_constant__ PassParams a,
+                                                 const uint64_t* __restrict__ keys,
+                                                 uint32_t* __restrict__ hist) {
+  constexpr int BINS = 1 << RB;
+  __shared__ uint32_t h[BINS];
+  for (int i = threadIdx.x; i < BINS; i += 256) h[i] = 0u;
+  __syncthreads();
+  const DigitFn dg(a);
+  const bool direct = !a.splitters && a.kp.ndmv[0] >= 0;
+  const uint64_t nsamp = (a.nnz + kSampleStride - 1) / kSampleStride;
+  constexpr int U = 8;  // samples per thread in flight
+  const uint64_t stride = gridDim.x * 256ull;
+  for (uint64_t s0 = blockIdx.x * 256ull + threadIdx.x; s0 < nsamp; s0 += U * stride) {
+    uint64_t k[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t sidx = s0 + u * stride;
+      const uint64_t i = sidx * kSampleStride + (sample_mix(sidx) & (kSampleStride - 1u));
+      ok[u] = sidx < nsamp && i < a.nnz;
+      k[u] = ok[u] ? __ldcs(keys + i) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t d;
+      if (direct) {
+        d = digit_from_old(a.kp, 0, k[u]);
+      } else {
+        uint64_t kk[1] = {k[u]};
+        reencode_keys<1>(a.kp, kk);
+        d = dg(a, kk[0]);
+      }
+      if (ok[u]) atomicAdd(&h[d], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < BINS; i += 256)
+    if (h[i]) atomicAdd(hist + i, h[i]);
+}
+
+// One CTA, thread d = digit (BINS == 256).
+__global__ void __launch_bounds__(256) k_caps(const uint32_t* __restrict__ hist, uint64_t capA, int test,
+                                              uint32_t* __restrict__ bucketA, uint32_t* __restrict__ cursor,
+                                              uint32_t* __restrict__ cap_end, uint32_t* __restrict__ flag) {
+  __shared__ uint32_t cap[256], start[256];
+  __shared__ uint32_t s_warp[32];
+  const int d = threadIdx.x;
+  const uint64_t est = (uint64_t)hist[d] * kSampleStride;
+  // count ~ Binomial(n_d, 1 / stride): sd(est) ~ sqrt(est * stride); six of them + 4,096
+  uint64_t c = test ? est / 2
+                    : est + (uint64_t)(6.0 * sqrt((double)est * kSampleStride)) + 4096;
+  if (c > 0xffffffffull) c = 0xffffffffull;
+  cap[d] = (uint32_t)c;
+  __syncthreads();
+  block_scan_bins<256, 256>(cap, start, s_warp);
+  const uint64_t end = (uint64_t)start[d] + cap[d];
+  bucketA[d] = start[d];
+  cursor[d] = start[d];
+  cap_end[d] = (uint32_t)(end < 0xffffffffull ? end : 0xffffffffull);
+  if (d == 255 && end > capA) *flag = 1u;  // (the scan wraps past 2^32 only beyond capA)
+}
+
+// One CTA, thread d = digit: exact bucket sizes and starts from the cursors (flag clear),
+// or the exact path's starts as the read bases (flag set).
+__global__ void __launch_bounds__(256) k_fin1(const uint32_t* __restrict__ flag,
+                                              const uint32_t* __restrict__ cursor,
+                                              uint32_t* __restrict__ bucketA,
+                                              uint32_t* __restrict__ totals1,
+                                              uint32_t* __restrict__ bucket1) {
+  __shared__ uint32_t tot[256];
+  __shared__ uint32_t s_warp[32];
+  const int d = threadIdx.x;
+  if (*flag) {
+    bucketA[d] = bucket1[d];
+    return;
+  }
+  tot[d] = cursor[d] - bucketA[d];
+  totals1[d] = tot[d];
+  __syncthreads();
+  block_scan_bins<256, 256>(tot, bucket1, s_warp);
+}
+
+// ---------------------------------------------------------------------------------
 // k_msd_tiles: one CTA, thread b = level-1 bucket (<= 1024).  Buckets larger than `cap` get tiles
 // in the level-2 tile table; the rest are leaves.
 // ---------------------------------------------------------------------------------
@@ -1942,6 +2054,7 @@ size_t msd_ctrl_bytes(int b1, int b2, uint64_t nnz, uint32_t tile) {
   const size_t nb1 = (size_t)1 << b1;
   const uint64_t tiles2 = pass_tiles(nnz, tile) + nb1;
   size_t s = (pass_ctrl_bytes(pass_rb(b1), nnz, tile) + 255) / 256 * 256;
+  s += kSampledCtrlBytes;  // sampled level 1: histogram, read starts, cursors, ends, flag
   if (b2 > 0) {
     const size_t rbins2 = (size_t)1 << pass_rb(b2);
     s += (tiles2 * sizeof(TileEntry) + 255) / 256 * 256;
@@ -2011,8 +2124,49 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
   PassIO io1 = io;
   io1.ctrl = reinterpret_cast<uint32_t*>(cb);
   cb += (pass_ctrl_bytes(rb1, nnz, kTile) + 255) / 256 * 256;
-  if ((e = run_pass(rb1, a, io1, 0, true, false, Lc)) != cudaSuccess) return e;
+  uint32_t* sblk = reinterpret_cast<uint32_t*>(cb);
+  cb += kSampledCtrlBytes;
+  uint32_t* const s_hist = sblk;
+  uint32_t* const s_bucketA = sblk + 256;
+  uint32_t* const s_cursor = sblk + 512;
+  uint32_t* const s_end = sblk + 768;
+  uint32_t* const s_flag = sblk + 1024;
   const PassCtrl c1 = pass_ctrl_layout(rb1, nnz, io1.ctrl, kTile);
+  // sampled level 1 (see k_sample1): unordered passes, 8-bit first digit, A padded
+  const bool sampled = mp.sampled && unst && rb1 == 8 && io.kA != nullptr;
+  if (sampled) {
+    if ((e = cudaMemsetAsync(sblk, 0, kSampledCtrlBytes, Lc.stream)) != cudaSuccess) return e;
+    int sms = 148;
+    if ((e = device_sms(&sms)) != cudaSuccess) return e;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_sample1");
+    k_sample1<8><<<sms * 4, 256, 0, Lc.stream>>>(a, io.keys_in, s_hist);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_caps");
+    k_caps<<<1, 256, 0, Lc.stream>>>(s_hist, sampled_capacity(nnz), io.tune ? io.tune->sampled_test : 0,
+                                     s_bucketA, s_cursor, s_end, s_flag);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    PassParams af = a;
+    af.tile = kTile;
+    af.pass = 0;
+    af.tiles = (uint32_t)pass_tiles(nnz, kTile);
+    af.cursor = s_cursor;
+    af.cap_end = s_end;
+    af.overflow = s_flag;
+    const ScatterIO s1 = pass_buffers(io1, 0, false, nullptr);
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_scatter_first");
+    if ((e = launch_scatter(rb1, true, false, vals, af, s1, af.tiles, Lc.stream)) != cudaSuccess)
+      return e;
+    // the exact path, run only if a bucket overflowed its capacity
+    PassParams ax = a;
+    ax.run_if = s_flag;
+    ax.persist = 1;
+    if ((e = run_pass(rb1, ax, io1, 0, true, false, Lc)) != cudaSuccess) return e;
+    if (Lc.mark) Lc.mark(Lc.ctx, "k_fin1");
+    k_fin1<<<1, 256, 0, Lc.stream>>>(s_flag, s_cursor, s_bucketA, c1.totals, c1.bucket);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else {
+    if ((e = run_pass(rb1, a, io1, 0, true, false, Lc)) != cudaSuccess) return e;
+  }
   a.tile = tile;  // later passes
   L.totals1 = c1.totals;
   L.bucket1 = c1.bucket;
@@ -2036,9 +2190,11 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     uint32_t* toff2 = reinterpret_cast<uint32_t*>(cb);
     cb += (tiles2 * rbins2 * 4 + 255) / 256 * 256;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
-    k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1,
-                                          mp.cta ? kCCap : kLeafCap, tile, ttab, tfirst, tcnt,
-                                          ntiles);
+    // (sampled level 1: tiles read A at the padded starts; no level-1 leaves, whose
+    // outputs would land at the read positions)
+    k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, sampled ? s_bucketA : c1.bucket, (int)nb1,
+                                          sampled ? 0u : (mp.cta ? kCCap : kLeafCap), tile, ttab,
+                                          tfirst, tcnt, ntiles);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess)
       return e;

@@ -424,6 +424,22 @@ def test_msd_leaf_variants(env, cuda_device, monkeypatch):
         check(dims, (1, 4, 0, 3, 2), keys, None)
 
 
+@pytest.mark.parametrize("env", [{}, {"LCO_SAMPLED_TEST": "1"}, {"LCO_NO_SAMPLED": "1"}])
+def test_msd_sampled_level1(env, cuda_device, monkeypatch):
+    """Sampled level 1 (>= 2^24 nonzeros, two unordered MSD levels): run bases from
+    per-digit cursors into sampled, padded bucket capacities; LCO_SAMPLED_TEST halves the
+    capacities so every run overflows and the predicated exact path redoes level 1;
+    LCO_NO_SAMPLED counts exactly.  All bit-exact vs the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(97)
+    dims = (4096,) * 5
+    n = 17_500_000
+    keys = np.unique(rng.integers(0, 2 ** 60, n + n // 20, dtype=np.int64))[:n].astype(np.uint64)
+    assert lco.plan(dims, (4, 3, 2, 1, 0)).info(len(keys))["msd_levels"] == 2
+    check(dims, (4, 3, 2, 1, 0), keys, rng.standard_normal(len(keys)))
+
+
 # ------------------------------------------------------------------ segmented single pass
 @pytest.mark.parametrize("dims,perm,nnz", [((256, 16, 64, 32), (0, 2, 1, 3), 1_000_000),
                                            ((128, 16, 2048, 4), (0, 2, 1, 3), 1_000_000),
