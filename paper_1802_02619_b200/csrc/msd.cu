@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(256) k_fin1(const uint32_t* __restrict__ flag,
 // k_msd_tiles: one CTA, thread b = level-1 bucket (<= 1024).  Buckets larger than `cap` get tiles
 // in the level-2 tile table; the rest are leaves.
 // ---------------------------------------------------------------------------------
+constexpr int kMsdTilesCtas = 32;
 __global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__ totals1,
                                                    const uint32_t* __restrict__ bucket1,
                                                    int nb1, uint32_t cap, uint32_t tile,
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__
   cnt[b] = nt;
   __syncthreads();
   block_scan_bins<1024, 1024>(cnt, off, s_warp);
-  if (b < nb1) {
+  if (b < nb1 && blockIdx.x == 0) {
     tfirst[b] = off[b];
     tcnt[b] = nt;
   }
@@ -186,10 +187,11 @@ __global__ void __launch_bounds__(1024) k_msd_tiles(const uint32_t* __restrict__
   if (b == 1023) cnt[0] = off[1023] + nt;  // cnt is free after the scan
   __syncthreads();
   const uint32_t total = cnt[0];
-  if (b == 0) *ntiles = total;
-  // all threads write the table in order (coalesced): tile t belongs to the last bucket
-  // whose first tile is <= t (buckets without tiles share their successor's offset)
-  for (uint32_t t = b; t < total; t += 1024) {
+  if (b == 0 && blockIdx.x == 0) *ntiles = total;
+  // all threads of all CTAs write the table in order (coalesced): tile t belongs to the
+  // last bucket whose first tile is <= t (buckets without tiles share their successor's
+  // offset); every CTA repeats the small bucket scan (one CTA: C5 42 us for 61K tiles)
+  for (uint32_t t = blockIdx.x * 1024u + b; t < total; t += gridDim.x * 1024u) {
     int x = 0;
 #pragma unroll
     for (int st = 512; st > 0; st >>= 1)
@@ -216,15 +218,20 @@ __global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __rest
                                                           const uint16_t* __restrict__ thist,
                                                           uint32_t* __restrict__ base2,
                                                           uint32_t* __restrict__ toff,
+                                                          uint32_t nseg_max,
                                                           const uint32_t* __restrict__ nseg = nullptr) {
   constexpr int BINS = 1 << RB;
   __shared__ uint32_t tot[BINS];
   __shared__ uint32_t ex[BINS];
   __shared__ uint32_t s_warp[32];
-  const int b = blockIdx.x;
-  if (nseg && (uint32_t)b >= *nseg) return;  // list-driven segments (level 3)
+  // segments b = blockIdx.x, + gridDim.x, ... (level 3: list-driven, at most *nseg of
+  // a capacity the host sizes the grid for -- a smaller grid loops instead of launching
+  // thousands of CTAs that find no segment)
+  const uint32_t nsegs = nseg ? *nseg : 0xffffffffu;
+  for (uint32_t b = blockIdx.x; b < nsegs && b < nseg_max; b += gridDim.x) {
   const uint32_t nt = tcnt[b];
-  if (nt == 0) return;
+  if (nt == 0) continue;
+  __syncthreads();  // tot / ex of the previous segment are read
   for (int d = threadIdx.x; d < BINS; d += kThreads) tot[d] = btot[(size_t)b * BINS + d];
   __syncthreads();
   block_scan_bins<kThreads, BINS>(tot, ex, s_warp);
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __rest
   constexpr int PER = BINS >= kThreads ? BINS / kThreads : 1;
   constexpr int U = 4;
   const int d0 = threadIdx.x * PER;
-  if (d0 >= BINS) return;
+  if (d0 >= BINS) continue;
   uint32_t run[PER];
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
@@ -255,6 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __rest
       }
     }
   }
+  }  // segments
 }
 
 // ---------------------------------------------------------------------------------
@@ -290,6 +298,15 @@ __global__ void __launch_bounds__(1024) k_list_tiles(const uint32_t* __restrict_
   __syncthreads();
   for (uint32_t c0 = 0; c0 < cap; c0 += 1024) {
     const uint32_t e = c0 + tid;
+    if (c0 >= m) {  // past the listed entries (uniform): empty rows, no scan
+      if (e < cap) {
+        start3[e] = 0;
+        size3[e] = 0;
+        tfirst3[e] = s_carry;
+        tcnt3[e] = 0;
+      }
+      continue;
+    }
     uint32_t st = 0, sz = 0;
     if (e < m) {
       const uint32_t slot = list[e] & kEntrySlot;  // entries: leaf_entry(level, slot)
@@ -1970,7 +1987,7 @@ cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const L
   cb += (tiles2 * rbins2 * 2 + 255) / 256 * 256;
   uint32_t* toff2 = reinterpret_cast<uint32_t*>(cb);
   if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
-  k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1, 0u, (uint32_t)kTile, ttab,
+  k_msd_tiles<<<kMsdTilesCtas, 1024, 0, Lc.stream>>>(c1.totals, c1.bucket, (int)nb1, 0u, (uint32_t)kTile, ttab,
                                         tfirst, tcnt, ntiles);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(btot, 0, (size_t)nb1 * rbins2 * 4, Lc.stream)) != cudaSuccess) return e;
@@ -1985,9 +2002,9 @@ cudaError_t run_seg(int gb, int mb, const KeyPlan& kp, const PassIO& io, const L
     return e;
   if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg");
   switch (rb2) {
-    case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
-    case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
-    case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+    case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
+    case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
+    case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
   }
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const ScatterIO sio = pass_buffers(io, 0, true, toff2);
@@ -2192,7 +2209,7 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     if (Lc.mark) Lc.mark(Lc.ctx, "k_msd_tiles");
     // (sampled level 1: tiles read A at the padded starts; no level-1 leaves, whose
     // outputs would land at the read positions)
-    k_msd_tiles<<<1, 1024, 0, Lc.stream>>>(c1.totals, sampled ? s_bucketA : c1.bucket, (int)nb1,
+    k_msd_tiles<<<kMsdTilesCtas, 1024, 0, Lc.stream>>>(c1.totals, sampled ? s_bucketA : c1.bucket, (int)nb1,
                                           sampled ? 0u : (mp.cta ? kCCap : kLeafCap), tile, ttab,
                                           tfirst, tcnt, ntiles);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -2212,9 +2229,9 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
       return e;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg");
     switch (rb2) {
-      case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
-      case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
-      case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2); break;
+      case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
+      case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
+      case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const ScatterIO s = pass_buffers(io, 1, false, toff2);
@@ -2301,9 +2318,9 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
         cudaSuccess)
       return e;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg_l3");
-    k_offsets_seg<kL3Bits><<<cap3, kThreads, 0, Lc.stream>>>(l3.start3, l3.tfirst3, l3.tcnt3,
-                                                            l3.btot3, l3.thist3, l3.base3,
-                                                            l3.toff3, l3.n3);
+    k_offsets_seg<kL3Bits><<<cap3 < (uint32_t)sms * 4u ? cap3 : (uint32_t)sms * 4u, kThreads, 0,
+                             Lc.stream>>>(l3.start3, l3.tfirst3, l3.tcnt3, l3.btot3, l3.thist3,
+                                          l3.base3, l3.toff3, cap3, l3.n3);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const ScatterIO s3 = pass_buffers(io, 2, false, l3.toff3);
     if (Lc.mark) Lc.mark(Lc.ctx, "k_scatter_l3");
