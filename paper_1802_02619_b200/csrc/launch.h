@@ -82,13 +82,16 @@ struct MsdPlan {
   int staged;  // CTA leaves of <= ~2K nonzeros: the fully staged k_leafs
   int sampled; // level 1 from sampled capacities (buffer A padded: sampled_capacity)
 };
+// Sampled MSD level 1: one key in kSampleStride is histogrammed (msd.cu k_sample1).
+constexpr uint32_t kSampleStride = 512;
 // Buffer A's length (records) for a sampled level 1: a bound on the padded capacities'
-// sum (k_caps: est_d + 6 sqrt(256 est_d) + 4,096 over 256 digits, sum est_d <= nnz + 256;
-// Cauchy-Schwarz: sum sqrt(est_d) <= 16 sqrt(nnz + 256)).
+// sum (k_caps: est_d + 6 sqrt(S est_d) + 4,096 over 256 digits, S = kSampleStride,
+// sum est_d <= nnz + S; Cauchy-Schwarz: sum sqrt(est_d) <= 16 sqrt(nnz + S)).
 inline uint64_t sampled_capacity(uint64_t nnz) {
-  uint64_t r = (uint64_t)std::sqrt((double)(nnz + 256));
-  while (r * r < nnz + 256) ++r;  // ceil(sqrt(nnz + 256))
-  return nnz + 256 + 1536 * r + 256 * 4096 + 4096;
+  uint64_t r = (uint64_t)std::sqrt((double)(nnz + kSampleStride));
+  while (r * r < nnz + kSampleStride) ++r;  // ceil(sqrt(nnz + S))
+  const uint64_t k = (uint64_t)std::ceil(96.0 * std::sqrt((double)kSampleStride));  // 6 * 16
+  return nnz + kSampleStride + k * r + 256 * 4096 + 4096;
 }
 constexpr size_t kSampledCtrlBytes = 5 * 1024;
 

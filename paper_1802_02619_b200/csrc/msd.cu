@@ -64,7 +64,6 @@ __host__ __device__ __forceinline__ uint32_t leaf_entry(int level, uint32_t slot
 // tiles read A at the padded starts and write B at the exact ones); B and the outputs
 // stay exact.
 // ---------------------------------------------------------------------------------
-constexpr uint32_t kSampleStride = 256;  // launch.h sampled_capacity assumes it
 
 __device__ __forceinline__ uint32_t sample_mix(uint64_t x) {
   x ^= x >> 33;
@@ -298,15 +297,7 @@ __global__ void __launch_bounds__(1024) k_list_tiles(const uint32_t* __restrict_
   __syncthreads();
   for (uint32_t c0 = 0; c0 < cap; c0 += 1024) {
     const uint32_t e = c0 + tid;
-    if (c0 >= m) {  // past the listed entries (uniform): empty rows, no scan
-      if (e < cap) {
-        start3[e] = 0;
-        size3[e] = 0;
-        tfirst3[e] = s_carry;
-        tcnt3[e] = 0;
-      }
-      continue;
-    }
+    if (c0 >= m) break;  // past the listed entries (uniform; readers stop at *n3)
     uint32_t st = 0, sz = 0;
     if (e < m) {
       const uint32_t slot = list[e] & kEntrySlot;  // entries: leaf_entry(level, slot)
