@@ -71,6 +71,7 @@ Tuning read_tuning() {
   t.no_leafs = flag("LCO_NO_LEAFS");
   t.no_leafr = flag("LCO_NO_LEAFR");
   t.no_sampled = flag("LCO_NO_SAMPLED");
+  t.no_cursor2 = flag("LCO_NO_CURSOR2");
   t.sampled_test = flag("LCO_SAMPLED_TEST");
   t.no_match = flag("LCO_NO_MATCH");
   t.lsd_maxbits = num("LCO_LSD_MAXBITS", 1, 11, 0);

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads) k_count(const __grid_constant__ Pass
   uint32_t* cs = csum + (size_t)seg * BINS;  // chunk sums, or segment totals (segmented)
   for (int d = tid; d < BINS; d += kThreads) {
     const uint32_t v = h[d];
-    row[d] = (uint16_t)v;
+    if (thist) row[d] = (uint16_t)v;  // (null: cursor-based scatter, totals only)
     if (v) atomicAdd(cs + d, v);
   }
   if (ADAPT && (t & 31u) == 0) {  // distinct digits of every 32nd tile
@@ -460,7 +460,11 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
     }
     __syncthreads();
     block_scan_bins<NT, BINS>(cnt, loff, s_warp);
-    if (FIRST && a.cursor) {  // sampled level 1: this tile's run of digit d from its cursor
+    if (a.cursor) {
+      // this tile's run of digit d from the digit's cursor: sampled level 1 (one row;
+      // a run past its bucket's capacity raises the overflow), or the segmented level 2
+      // (one row per level-1 bucket, exact totals: no per-tile offsets)
+      uint32_t* crow = a.cursor + (FIRST ? 0u : (size_t)seg * BINS);
 #pragma unroll
       for (int b = 0; b < NB; ++b) {
         const int d = tid + b * NT;
@@ -468,8 +472,8 @@ __global__ void __launch_bounds__(NT, (NT >= 1024 ? 1 : 2))
           const uint32_t c = cnt[d];
           uint32_t g0 = 0;
           if (c) {
-            g0 = atomicAdd(a.cursor + d, c);
-            if (g0 + c > a.cap_end[d] || g0 + c < g0) s_ovf = 1;
+            g0 = atomicAdd(crow + d, c);
+            if (FIRST && (g0 + c > a.cap_end[d] || g0 + c < g0)) s_ovf = 1;
           }
           gbase[d] = g0;
         }

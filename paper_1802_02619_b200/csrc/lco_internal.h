@@ -242,6 +242,7 @@ struct Tuning {
   int no_leafs;     // LCO_NO_LEAFS
   int no_leafr;     // LCO_NO_LEAFR
   int no_sampled;   // LCO_NO_SAMPLED: level 1 of the MSD schedule counted exactly
+  int no_cursor2;   // LCO_NO_CURSOR2: unordered level 2 with per-tile offsets (A/B)
   int sampled_test; // LCO_SAMPLED_TEST: sampled capacities halved (forces the exact fallback)
   int no_match;     // LCO_NO_MATCH: LSD passes never rank with match.any
   int lsd_maxbits;  // LCO_LSD_MAXBITS (0: default), clamped to 1..11

@@ -247,6 +247,11 @@ __global__ void __launch_bounds__(kThreads) k_offsets_seg(const uint32_t* __rest
     run[i] = start + ex[d0 + i];
     base2[(size_t)b * BINS + d0 + i] = run[i];
   }
+  if (!thist) {  // cursor-based scatter: toff holds one cursor row per segment
+#pragma unroll
+    for (int i = 0; i < PER; ++i) toff[(size_t)b * BINS + d0 + i] = run[i];
+    continue;
+  }
   for (uint32_t j = 0; j < nt; j += U) {
     uint32_t h[U][PER];
 #pragma unroll
@@ -2214,18 +2219,24 @@ cudaError_t run_msd(const MsdPlan& mp, const KeyPlan& kp, const PassIO& io, cons
     a2.ttab = ttab;
     a2.ntiles = ntiles;
     a2.tiles = (uint32_t)tiles2;
+    // unordered level 2: run bases from one cursor row per level-1 bucket (atomicAdd per
+    // tile and digit) instead of per-tile offsets -- no tile histograms (125 MB at C5),
+    // no offset rows (251 MB); the cursor rows live where the offset rows would
+    const bool cur2 = unst && !(io.tune && io.tune->no_cursor2);
+    uint16_t* const th2 = cur2 ? nullptr : thist2;
+    if (cur2) a2.cursor = toff2;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_count_seg");
-    if ((e = launch_count(rb2, false, a2, io.kA, thist2, btot, (uint32_t)tiles2, Lc.stream)) !=
+    if ((e = launch_count(rb2, false, a2, io.kA, th2, btot, (uint32_t)tiles2, Lc.stream)) !=
         cudaSuccess)
       return e;
     if (Lc.mark) Lc.mark(Lc.ctx, "k_offsets_seg");
     switch (rb2) {
-      case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
-      case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
-      case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, thist2, base2, toff2, nb1); break;
+      case 8: k_offsets_seg<8><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, th2, base2, toff2, nb1); break;
+      case 10: k_offsets_seg<10><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, th2, base2, toff2, nb1); break;
+      case 11: k_offsets_seg<11><<<nb1, kThreads, 0, Lc.stream>>>(c1.bucket, tfirst, tcnt, btot, th2, base2, toff2, nb1); break;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const ScatterIO s = pass_buffers(io, 1, false, toff2);
+    const ScatterIO s = pass_buffers(io, 1, false, cur2 ? nullptr : toff2);
     if (Lc.mark) Lc.mark(Lc.ctx, "k_scatter_seg");
     if ((e = launch_scatter(rb2, false, false, vals, a2, s, (uint32_t)tiles2, Lc.stream)) !=
         cudaSuccess)
