@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) k_block_bounds(uint64_t nnz, const uint64
 // (2 lane, 2 lane + 1) of the warp's 64-key chunk u; a pair's outer neighbours come from
 // one lane rotation per direction.
 template <int U2>
-__global__ void __launch_bounds__(256) k_block_bounds2(uint64_t nnz, const uint64_t* __restrict__ keys,
+__global__ void __launch_bounds__(256) k_block_bounds(uint64_t nnz, const uint64_t* __restrict__ keys,
                                                        FastDiv fF, uint32_t* __restrict__ bstart,
                                                        uint32_t* __restrict__ bend) {
   const int lane = threadIdx.x & 31;
@@ -501,7 +501,7 @@ cudaError_t run_block(const KeyPlan& kp, const KeyPlan& kb, uint64_t nblocks, ui
   // 16-byte key loads when the keys are 16-byte aligned (C4 bounds 0.090 -> 0.080 ms)
   if (L.mark) L.mark(L.ctx, "k_block_bounds");
   if ((reinterpret_cast<uintptr_t>(io.keys_in) & 15) == 0) {
-    k_block_bounds2<4><<<(unsigned)((nnz + 2047) / 2048), 256, 0, L.stream>>>(nnz, io.keys_in, fF, bstart, bend);
+    k_block_bounds<4><<<(unsigned)((nnz + 2047) / 2048), 256, 0, L.stream>>>(nnz, io.keys_in, fF, bstart, bend);
   } else {
     const unsigned gn = (unsigned)((nnz + 256 * kBkU - 1) / (256 * kBkU));  // 8 warps x 256
     k_block_bounds<<<gn, 256, 0, L.stream>>>(nnz, io.keys_in, fF, bstart, bend);

@@ -21,7 +21,7 @@ for c in C5 C4 C3a C3b C2a C2b C1; do
   echo "launches $c rc=$?"
 done
 python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_plain_full5.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_leafs" -s 5 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"k_scatter|k_leafs" -s 6 -c 4 \
     -o gpurun_out/m_c5_full -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_ncu_c5.log 2>&1
 echo "c5 full rc=$?"
 python bench.py --config C4 --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > gpurun_out/m_plain_full4.log 2>&1 && \

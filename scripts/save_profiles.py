@@ -59,7 +59,8 @@ for c, rep in (("C5", "m_c5_full.ncu-rep"), ("C4", "m_c4_full.ncu-rep")):
     traffic.setdefault(c, {})["by_kernel"] = {k: sum(v) / len(v) for k, v in per.items()}
 tp = os.path.join(P, "traffic.json")
 old = json.load(open(tp)) if os.path.exists(tp) else {}
-old.update(traffic)
+for c, v in traffic.items():  # per config: keep entries this capture did not produce
+    old.setdefault(c, {}).update(v)
 json.dump(old, open(tp, "w"), indent=1)
 for src, dst in (("m_table2.md", "table2.md"), ("m_table2.json", "table2.json"),
                  ("m_addition.json", "addition.json"), ("m_addition_hier.json", "addition_hier.json"),
