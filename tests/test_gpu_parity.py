@@ -644,6 +644,20 @@ def test_block_path(dims, perm, cuda_device):
     check(w.dims, w.perms[0], _np_u64(w.keys), w.vals.numpy())
 
 
+@pytest.mark.parametrize("nnz", [20_479, 20_480, 20_481, 20_543, 20_545])
+def test_block_bounds_window_edges(nnz, cuda_device):
+    """k_block_bounds' 16-byte path: each warp reads 512 keys as 256 lane pairs, so the
+    ragged last warp (nnz = 10 x 2,048 +- 1, odd and even tails) and block boundaries
+    between the two keys of a pair or across lanes, chunks and warps must all be found;
+    compared with the oracle bit-exactly, aligned (vector) and shifted (scalar path)."""
+    dims, perm = (37, 41, 1000), (1, 0, 2)
+    rng = np.random.default_rng(nnz)
+    keys, vals = _rand_sorted(rng, dims, nnz)
+    assert lco.plan(dims, perm).info(len(keys))["path"] == "block"
+    check(dims, perm, keys, vals)
+    check(dims, perm, keys, vals, shift=1)
+
+
 # ------------------------------------------------------------------ concurrency (lco.h threading)
 def test_one_handle_two_threads_two_streams(cuda_device):
     """include/lco.h: a handle may be used concurrently from several host threads on
