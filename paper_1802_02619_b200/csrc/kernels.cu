@@ -166,18 +166,41 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(uint32_t* __restrict__ cs
   const int g = tid / LANES;
   const uint32_t per = (nchunks + SPLIT - 1) / SPLIT;
   const uint32_t c0 = min(nchunks, g * per), c1 = min(nchunks, c0 + per);
+  // the first RC chunk sums stay in registers for the write-back; the rest are re-read in
+  // batches of 8 (a load-then-store loop over csum serializes one L2 round trip per
+  // chunk: the store may alias the next load)
+  constexpr int RC = 24;
+  uint32_t cache[RC];
   uint32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < RC; ++i) {
+    cache[i] = c0 + i < c1 ? __ldcg(csum + (size_t)(c0 + i) * BINS + d) : 0u;
+    sum += cache[i];
+  }
 #pragma unroll 8
-  for (uint32_t c = c0; c < c1; ++c) sum += __ldcg(csum + (size_t)c * BINS + d);
+  for (uint32_t c = c0 + RC; c < c1; ++c) sum += __ldcg(csum + (size_t)c * BINS + d);
   part[tid] = sum;
   __syncthreads();
   uint32_t run = 0;
   for (int g2 = 0; g2 < g; ++g2) run += part[g2 * LANES + tid % LANES];
-  for (uint32_t c = c0; c < c1; ++c) {
-    const size_t o = (size_t)c * BINS + d;
-    const uint32_t v = __ldcg(csum + o);
-    csum[o] = run;
-    run += v;
+#pragma unroll
+  for (int i = 0; i < RC; ++i) {
+    if (c0 + i < c1) {
+      csum[(size_t)(c0 + i) * BINS + d] = run;
+      run += cache[i];
+    }
+  }
+  for (uint32_t c = c0 + RC; c < c1; c += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = c + u < c1 ? __ldcg(csum + (size_t)(c + u) * BINS + d) : 0u;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (c + u < c1) {
+        csum[(size_t)(c + u) * BINS + d] = run;
+        run += v[u];
+      }
+    }
   }
   if (g == SPLIT - 1) totals[d] = run;
   __threadfence();
