@@ -142,7 +142,7 @@ LCO_API lco_status lco_permute_host(lco_handle h, uint64_t nnz, const uint64_t* 
  *              input order; send_keys carries the OLD key (the receiver re-runs
  *              lco_permute with idx_in = received send_idx).
  *   send_counts world uint64 (device): records per destination.
- * world in 1..4096.  vals may be NULL (both). */
+ * world in 1..2048 (one 11-bit multisplit pass; larger values return LCO_ERR_ARG).  vals may be NULL (both). */
 LCO_API lco_status lco_partition(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
                          const double* vals_in, uint32_t idx_base, int world,
                          const uint64_t* splitters, uint64_t* send_keys, double* send_vals,
@@ -168,7 +168,7 @@ LCO_API lco_status lco_partition_direct(lco_handle h, uint64_t nnz, const uint64
                                 void* workspace, size_t workspace_bytes, void* stream);
 
 /* Only the per-destination record counts of the partition (device send_counts[world]):
- * the count and scan of the multisplit pass, no data movement.  world in 1..4096. */
+ * the count and scan of the multisplit pass, no data movement.  world in 1..2048 (one 11-bit multisplit pass; larger values return LCO_ERR_ARG). */
 LCO_API lco_status lco_partition_counts(lco_handle h, uint64_t nnz, const uint64_t* keys_in,
                                 int world, const uint64_t* splitters, uint64_t* send_counts,
                                 void* workspace, size_t workspace_bytes, void* stream);
