@@ -252,6 +252,7 @@ struct Tuning {
   int l3_flat;      // LCO_L3_FLAT: level-3 count / scatter one CTA per tile (debug)
   int l3_bits;      // LCO_L3_BITS: level-3 digit bits (0: default 8; -1: 0 bits)
   int single_cta;   // LCO_SINGLE_CTA: the single-tile pass on one CTA, not a cluster
+  int no_prefix_msd;  // LCO_NO_PREFIX_MSD: identity-prefix plans never switch to the full-key MSD
 };
 
 }  // namespace lco

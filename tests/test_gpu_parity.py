@@ -788,3 +788,20 @@ def test_table2_laplacian_level3_full(cuda_device):
         assert np.array_equal(_np_u64(ko), ek), perm
         assert np.array_equal(po.cpu().numpy().view(np.uint32), ep), perm
         assert np.array_equal(vo.cpu().numpy().view(np.uint64), ev.view(np.uint64)), perm
+
+
+# ------------------------------------------------------------------ prefix plans on the full key
+@pytest.mark.parametrize("nnz", [300_000, 2_500_000])
+def test_prefix_plan_sorts_full_key_by_msd(nnz, cuda_device):
+    """An identity prefix with a shaved key of >= 4 LSD passes runs the MSD schedule of the
+    full new key instead (api.cu permute_op; the prefix digits are
+    already in order, so both stable sorts give one output).  One- and two-level MSD,
+    bit-exact against the oracle, with and without the permutation vector."""
+    rng = np.random.default_rng(77)
+    dims, perm = (64,) * 7, (0, 6, 5, 4, 3, 2, 1)
+    info = lco.Plan(dims, perm).info(nnz)
+    assert info["path"] == "msd" and info["sort_bits"] == 42
+    assert info["msd_levels"] == (1 if nnz < 1_000_000 else 2)
+    keys, vals = _rand_sorted(rng, dims, nnz)
+    check(dims, perm, keys, vals)
+    check(dims, perm, keys, vals, return_perm=False)

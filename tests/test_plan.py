@@ -312,3 +312,25 @@ def test_partition_world_bound_and_tuning_read_once(monkeypatch):
     monkeypatch.setenv("LCO_MSD", "1")
     monkeypatch.setenv("LCO_NO_BLOCK", "1")
     assert q.info(1_308_672) == before
+
+
+def test_prefix_plan_takes_full_key_msd_only_when_modelled_faster():
+    """api.cu permute_op: with an identity prefix the flat plan sorts the shaved key q by
+    LSD passes; from 4 passes on, the MSD schedule of the full new key K' models below it
+    and is taken (same output: the prefix digits are non-decreasing in the input,
+    PAPER.md:245-247).  Three-pass plans (C3b, Table 2's 2 % tensor) and segment/tile
+    plans stay as they were; the workspace covers either choice."""
+    p = lco.Plan((2896,) * 4, (0, 3, 2, 1))
+    i = p.info(41_910_912)
+    assert (i["path"], i["sort_bits"], i["model_bytes"]) == ("msd", 46, 132.0)
+    i = lco.Plan((4096,) * 5, (0, 4, 3, 2, 1)).info(500_000_000)
+    assert (i["path"], i["sort_bits"], i["msd_levels"]) == ("msd", 60, 2)
+    i = lco.Plan((128,) * 6, (0, 3, 1, 4, 2, 5)).info(14_581_760)  # C3b
+    assert (i["path"], i["sort_bits"], i["passes"]) == ("lsd", 28, 3)
+    i = lco.Plan((200,) * 4, (0, 3, 2, 1)).info(32_000_000)
+    assert (i["path"], i["sort_bits"]) == ("lsd", 23)
+    i = lco.Plan((64,) * 7, (0, 6, 5, 4, 3, 2, 1)).info(300_000)
+    assert (i["path"], i["msd_levels"]) == ("msd", 1)
+    # lco_workspace_size is the maximum over the permute and the sort plan
+    q = lco.Plan((2896,) * 4, (3, 2, 1, 0))  # no prefix: MSD on the same 46 bits
+    assert p.workspace_size(41_910_912) >= q.workspace_size(41_910_912)
