@@ -36,6 +36,10 @@ k3, v3 = workloads.random_tensor((64,) * 7, 3_000_000, seed=9, values="normal", 
 cases += [("random 64^7 3M", (64,) * 7, (0, 6, 5, 4, 3, 2, 1), k3, v3)]
 k4 = k3[:300_000].contiguous()
 cases += [("random 64^7 300K (low keys)", (64,) * 7, (0, 6, 5, 4, 3, 2, 1), k4, v3[:300_000].contiguous())]
+k5 = k[:6_000_000].contiguous()  # the lowest 3 % of the keys: 8 of 256 first digits used
+cases += [("random 4096^5, lowest 6M of 200M keys", (4096,) * 5, (0, 4, 3, 2, 1), k5, v[:6_000_000].contiguous())]
+k6 = k[:40_000_000].contiguous()
+cases += [("random 4096^5, lowest 40M of 200M keys", (4096,) * 5, (0, 4, 3, 2, 1), k6, v[:40_000_000].contiguous())]
 out = []
 for name, dims, perm, kk, vv in cases:
     p = lco.Plan(dims, perm)

@@ -795,13 +795,18 @@ def test_table2_laplacian_level3_full(cuda_device):
 def test_prefix_plan_sorts_full_key_by_msd(nnz, cuda_device):
     """An identity prefix with a shaved key of >= 4 LSD passes runs the MSD schedule of the
     full new key instead (api.cu permute_op; the prefix digits are
-    already in order, so both stable sorts give one output).  One- and two-level MSD,
+    already in order, so both stable sorts give one output), from two MSD levels on;
     bit-exact against the oracle, with and without the permutation vector."""
     rng = np.random.default_rng(77)
     dims, perm = (64,) * 7, (0, 6, 5, 4, 3, 2, 1)
     info = lco.Plan(dims, perm).info(nnz)
-    assert info["path"] == "msd" and info["sort_bits"] == 42
-    assert info["msd_levels"] == (1 if nnz < 1_000_000 else 2)
+    if nnz < 1_000_000:  # below two MSD levels the shaved key stays on LSD passes
+        assert (info["path"], info["sort_bits"]) == ("lsd", 36)
+    else:
+        assert (info["path"], info["sort_bits"], info["msd_levels"]) == ("msd", 42, 2)
     keys, vals = _rand_sorted(rng, dims, nnz)
     check(dims, perm, keys, vals)
     check(dims, perm, keys, vals, return_perm=False)
+    # unevenly filled prefix digits: the lowest third of the keys only (level 3 re-splits)
+    third = len(keys) // 3
+    check(dims, perm, keys[:third], vals[:third])
